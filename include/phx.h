@@ -1,0 +1,178 @@
+/*
+ * phx.h — C ABI of the B200-native phi-combination engine (libphx.so).
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2509.26475
+ * ("phiact"): parameter selection (Alg. 1) and the block evaluator (Alg. 3).
+ * Each entry point names the reference C++ interface it replaces
+ * (paths relative to the reference's proj/ directory).  Plain pointers and
+ * sizes only; host buffers are column-major like the reference's Eigen
+ * matrices (include/phiact/linop.hpp:12).  The C++ wrapper in
+ * include/phx/phiact.hpp restores the reference names and exception types on
+ * top of this header.
+ *
+ * Every compute entry point runs on an NVIDIA B200 (sm_100a).  There is no CPU
+ * fallback: without a usable device every call returns PHX_ECUDA.
+ *
+ * Error model: functions return a phx_status; on failure phx_last_error()
+ * returns the thread-local message.  The codes map onto the reference's
+ * exception types (include/phiact headers):
+ *   PHX_EINVAL  -> std::invalid_argument (bad input)
+ *   PHX_ENUMERIC-> std::runtime_error    (divergence, non-convergence,
+ *                                          mu overflow, rejected operator)
+ *   PHX_ELOGIC  -> std::logic_error      (empty operator, shape)
+ *   PHX_ECUDA   -> CUDA / device failure (no reference analogue)
+ * Messages reproduce the reference's text where one exists.
+ */
+#ifndef PHX_H
+#define PHX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PHX_OK = 0,
+  PHX_EINVAL = 1,
+  PHX_ENUMERIC = 2,
+  PHX_ELOGIC = 3,
+  PHX_ECUDA = 4,
+  PHX_ENOMEM = 5
+} phx_status;
+
+/* Opaque handles. */
+typedef struct phx_op_s* phx_op;       /* device-resident CSR operator      */
+typedef struct phx_basis_s* phx_basis; /* device-resident power basis       */
+
+/* ScalingShift (include/phiact/params.hpp:34-41).  Same fields, same meaning:
+ * s = real scaling, xi = spectral shift, s0 = preliminary scale, f_min =
+ * padded objective value, m = Taylor degree, r = accepted power count. */
+typedef struct {
+  double s;
+  double xi;
+  double s0;
+  double f_min;
+  int32_t m;
+  int32_t r;
+} phx_scaling_shift;
+
+/* RunRecord (include/phiact/phi_single.hpp:16-21).  series_lens_F is a
+ * caller-owned array of lens_capacity ints; n_sweeps = s_effective - 1 is the
+ * number of entries the evaluation produced (entries beyond the capacity are
+ * dropped, n_sweeps still reports the full count). */
+typedef struct {
+  int64_t s_effective;
+  int32_t series_len_S;
+  int32_t n_sweeps;
+  int32_t* series_lens_F;
+  int64_t lens_capacity;
+  int64_t matvecs;
+} phx_run_record;
+
+/* ---------------------------------------------------------------------------
+ * Operator (replaces LinearOperator, include/phiact/linop.hpp:19-37, for CSR
+ * operators; the reference's ApplyFn is an opaque host callback that cannot
+ * cross to the device, so the operator is a CSR descriptor instead).
+ * row_ptr has n+1 entries, col_idx/vals have row_ptr[n] entries; column
+ * indices are used in storage order (the product accumulates each row in that
+ * order).  The handle owns device copies; the host arrays may be freed after
+ * the call.  Immutable after creation; concurrent calls on one handle are
+ * serialised internally.  device < 0 selects the current device.
+ * Rejects n < 1, nnz >= 2^31, out-of-range indices, non-finite values
+ * (dense_operator's checks, linop.cpp:26-38).
+ * ------------------------------------------------------------------------- */
+phx_status phx_op_create_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                             const double* vals, int32_t device, phx_op* out);
+phx_status phx_op_destroy(phx_op op);
+int64_t phx_op_dim(phx_op op);
+int64_t phx_op_nnz(phx_op op);
+
+/* Y = A*X (LinearOperator::apply, linop.cpp:10-24) and (A - xi I) X
+ * (shifted_apply, linop.cpp:40-49) on host column-major blocks of k columns
+ * with leading dimensions ldx/ldy >= n. */
+phx_status phx_apply(phx_op op, const double* X, int64_t ldx, int64_t k, double* Y, int64_t ldy);
+phx_status phx_shifted_apply(phx_op op, double xi, const double* X, int64_t ldx, int64_t k,
+                             double* Y, int64_t ldy);
+
+/* ---------------------------------------------------------------------------
+ * Parameter selection (include/phiact/params.hpp:50-77).
+ * ------------------------------------------------------------------------- */
+/* select_parameters(op, m = 61, tol = -1 (2^-53), delta = 0.8)
+ * (params.hpp:75-77, params.cpp:241-247). */
+phx_status phx_select_parameters(phx_op op, int32_t m, double tol, double delta,
+                                 phx_scaling_shift* out);
+
+/* build_power_basis (params.hpp:50-51, params.cpp:81-154).  The basis lives
+ * on the device, column-major n x (m+1). */
+phx_status phx_basis_build(phx_op op, int32_t m, double delta, phx_basis* out);
+phx_status phx_basis_destroy(phx_basis b);
+/* r, m, s0; logs (r entries) and log_binom (m+1 entries) may be NULL;
+ * columns (n*(m+1), column-major) may be NULL — copying it is a D2H. */
+phx_status phx_basis_info(phx_basis b, int32_t* r, int32_t* m, double* s0, double* logs,
+                          double* log_binom, double* columns);
+/* objective(basis, xi) (params.hpp:56, params.cpp:156-170). */
+phx_status phx_objective(phx_basis b, double xi, double* f);
+/* minimize_shift(basis) (params.hpp:61, params.cpp:172-189).  path (may be
+ * NULL) receives the Brent trial points as (u, f(u)) pairs. */
+phx_status phx_minimize_shift(phx_basis b, double* xi, double* f_min, double* path,
+                              int64_t path_capacity, int64_t* path_len);
+/* parameters_for_shift(op, basis, xi, tol) (params.hpp:70-72,
+ * params.cpp:213-239). */
+phx_status phx_parameters_for_shift(phx_op op, phx_basis b, double xi, double tol,
+                                    phx_scaling_shift* out);
+
+/* ---------------------------------------------------------------------------
+ * Block evaluator: phimv_block(op, BlockPhiRequest) (phi_block.hpp:30-31,
+ * phi_block.cpp:48-157).  w_i = sum_j alpha_i^j phi_j(t_i A) v_j, i < r.
+ *   t, alpha : r values each (BlockPhiRequest::t / ::alpha)
+ *   V        : n x (p+1) column-major host block [v_0 .. v_p], leading dim ldv
+ *   tol      : <= 0 means 2^-53
+ *   params   : from phx_select_parameters (or any ScalingShift)
+ *   W        : n x r column-major host output, leading dim ldw
+ *   rec      : may be NULL
+ * ------------------------------------------------------------------------- */
+phx_status phx_phimv_block(phx_op op, int32_t r, const double* t, const double* alpha, int32_t p,
+                           const double* V, int64_t ldv, double tol,
+                           const phx_scaling_shift* params, double* W, int64_t ldw,
+                           phx_run_record* rec);
+
+/* Same evaluation on device-resident data: d_V is a device n x (p+1)
+ * column-major block (leading dim n), d_W a device n x r column-major output
+ * (leading dim n).  Runs on the operator's stream; returns after the result
+ * and the record are complete.  Used to time the evaluation without host
+ * copies. */
+phx_status phx_phimv_block_device(phx_op op, int32_t r, const double* t, const double* alpha,
+                                  int32_t p, const double* d_V, double tol,
+                                  const phx_scaling_shift* params, double* d_W,
+                                  phx_run_record* rec);
+
+/* Single-combination evaluator phimv (phi_single.hpp:44, phi_single.cpp:38-127):
+ * w = sum_j alpha^j phi_j(tA) v_j with the single variant's operation order.
+ * exp_v0 / tail (n values each) may be NULL. */
+phx_status phx_phimv(phx_op op, double t, double alpha, int32_t p, const double* V, int64_t ldv,
+                     double tol, const phx_scaling_shift* params, double* w, double* exp_v0,
+                     double* tail, phx_run_record* rec);
+
+/* ---------------------------------------------------------------------------
+ * Introspection.
+ * ------------------------------------------------------------------------- */
+const char* phx_last_error(void);
+/* Number of device kernels this process has launched through libphx. */
+int64_t phx_kernel_launches(void);
+/* Device-event time (ms) of the last phimv_block evaluation kernel, and the
+ * number of grid-wide steps it executed (S terms + promotion + recovery
+ * terms + sweep ends). */
+phx_status phx_last_eval_stats(double* kernel_ms, int64_t* steps);
+/* Set a device-side trace buffer capacity (0 disables).  When enabled,
+ * phimv_block records (kind, a, b) triples per grid step: kind 0 = initial
+ * S norms, 1 = S term (c2, ||S||), 2 = sweep start (||F||, ||E||), 3 = recovery
+ * term (d2, ||E||) — the same records the oracle emits. */
+phx_status phx_set_trace(int64_t capacity);
+phx_status phx_get_trace(double* out, int64_t capacity, int64_t* len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PHX_H */

@@ -1,0 +1,354 @@
+"""ctypes wrapper of the CPU oracle (oracle/liboracle.so) — TEST INFRASTRUCTURE.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm import this module; the product (paper_2509_26475_b200) never does.  The
+oracle is a plain C++ restatement of the reference's select_parameters /
+phimv_block / phimv (see phx_oracle.cpp for the file:line citations).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+dp = C.POINTER(C.c_double)
+i64p = C.POINTER(C.c_int64)
+i32p = C.POINTER(C.c_int32)
+
+
+class ScalingShiftC(C.Structure):
+    _fields_ = [("s", C.c_double), ("xi", C.c_double), ("s0", C.c_double),
+                ("f_min", C.c_double), ("m", C.c_int32), ("r", C.c_int32)]
+
+
+class OracleError(Exception):
+    pass
+
+
+class OracleInvalidArgument(OracleError, ValueError):
+    pass
+
+
+class OracleRuntimeError(OracleError, RuntimeError):
+    pass
+
+
+def build():
+    import subprocess
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            build()
+        L = C.CDLL(path)
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_rng_new.restype = C.c_void_p
+        L.orc_rng_new.argtypes = [C.c_uint64]
+        L.orc_rng_free.argtypes = [C.c_void_p]
+        L.orc_rng_normals.argtypes = [C.c_void_p, C.c_int64, dp]
+        L.orc_rng_uniforms.argtypes = [C.c_void_p, C.c_int64, dp]
+        L.orc_unit_vector.argtypes = [C.c_uint64, C.c_int64, dp]
+        L.orc_stable_norm.restype = C.c_double
+        L.orc_stable_norm.argtypes = [dp, C.c_int64]
+        L.orc_norm2.restype = C.c_double
+        L.orc_norm2.argtypes = [dp, C.c_int64]
+        L.orc_inf_norm.restype = C.c_double
+        L.orc_inf_norm.argtypes = [dp, C.c_int64, C.c_int64, C.c_int64]
+        L.orc_apply.argtypes = [C.c_int64, i64p, i32p, dp, dp, C.c_int64, dp]
+        L.orc_basis_build.restype = C.c_void_p
+        L.orc_basis_build.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int32, C.c_double, i32p]
+        L.orc_basis_free.argtypes = [C.c_void_p]
+        L.orc_basis_info.argtypes = [C.c_void_p, i32p, i32p, dp, dp, dp, dp]
+        L.orc_objective.argtypes = [C.c_void_p, C.c_double, dp]
+        L.orc_minimize_shift.argtypes = [C.c_void_p, dp, dp, dp, C.c_int64, i64p]
+        L.orc_parameters_for_shift.argtypes = [C.c_int64, i64p, i32p, dp, C.c_void_p, C.c_double,
+                                               C.c_double, C.POINTER(ScalingShiftC)]
+        L.orc_log_shifted_power.argtypes = [C.c_int64, i64p, i32p, dp, dp, C.c_double, C.c_int32, dp]
+        L.orc_select_parameters.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int32, C.c_double,
+                                            C.c_double, C.POINTER(ScalingShiftC)]
+        L.orc_phimv_block.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int64, dp, dp, C.c_int32, dp,
+                                      C.c_int64, C.c_double, C.POINTER(ScalingShiftC), dp,
+                                      C.c_int64, i64p, i32p, C.c_int64, dp, C.c_int64, i64p]
+        L.orc_phimv.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, C.c_double, C.c_int32, dp,
+                                C.c_int64, C.c_double, C.POINTER(ScalingShiftC), dp, dp, dp, i64p,
+                                i32p, C.c_int64]
+        L.orc_reference_w.argtypes = [C.c_int64, dp, C.c_int32, dp, C.c_double, C.c_double, dp]
+        L.orc_dense_phi.argtypes = [C.c_int64, dp, C.c_double, C.c_int32, dp]
+        L.orc_jexp_chain.argtypes = [C.c_double, C.c_double, C.c_int32, dp]
+        _LIB = L
+    return _LIB
+
+
+def _check(code):
+    if code == 0:
+        return
+    msg = lib().orc_last_error().decode()
+    if code == 1:
+        raise OracleInvalidArgument(msg)
+    if code == 2:
+        raise OracleRuntimeError(msg)
+    raise OracleError(msg)
+
+
+def _d(a):
+    return a.ctypes.data_as(dp)
+
+
+# ---------------------------------------------------------------------------
+# operators
+# ---------------------------------------------------------------------------
+@dataclass
+class Csr:
+    n: int
+    rp: np.ndarray   # int64, n+1
+    ci: np.ndarray   # int32
+    av: np.ndarray   # float64
+    dense: np.ndarray | None = field(default=None, repr=False)
+
+    def args(self):
+        return (self.n, self.rp.ctypes.data_as(i64p), self.ci.ctypes.data_as(i32p), _d(self.av))
+
+
+def csr_from_dense(A) -> Csr:
+    """Dense matrix as a CSR operator with every entry stored in column
+    order, so the CSR product is the naive ascending-k dot product."""
+    A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
+    n = A.shape[0]
+    rp = np.arange(0, n * n + 1, n, dtype=np.int64)
+    ci = np.tile(np.arange(n, dtype=np.int32), n)
+    av = np.ascontiguousarray(A.reshape(-1))
+    return Csr(n, rp, ci, av, dense=A)
+
+
+def csr_from_arrays(n, rp, ci, av) -> Csr:
+    return Csr(int(n), np.ascontiguousarray(rp, dtype=np.int64),
+               np.ascontiguousarray(ci, dtype=np.int32),
+               np.ascontiguousarray(av, dtype=np.float64))
+
+
+# ---------------------------------------------------------------------------
+# Rng
+# ---------------------------------------------------------------------------
+class Rng:
+    """Reference Rng (rng.hpp:15-62) through the oracle: one stream."""
+
+    def __init__(self, seed: int):
+        self._h = lib().orc_rng_new(C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().orc_rng_free(self._h)
+            self._h = None
+
+    def normals(self, count):
+        out = np.empty(count, dtype=np.float64)
+        lib().orc_rng_normals(self._h, count, _d(out))
+        return out
+
+    def uniforms(self, count):
+        out = np.empty(count, dtype=np.float64)
+        lib().orc_rng_uniforms(self._h, count, _d(out))
+        return out
+
+    def uniform(self):
+        return float(self.uniforms(1)[0])
+
+    def matrix(self, rows, cols):
+        """column-major fill, returned as an (rows, cols) array"""
+        return self.normals(rows * cols).reshape(cols, rows).T.copy()
+
+    def vector(self, n):
+        return self.normals(n)
+
+
+def unit_vector(seed, n):
+    out = np.empty(n)
+    _check(lib().orc_unit_vector(C.c_uint64(seed), n, _d(out)))
+    return out
+
+
+def stable_norm(x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return lib().orc_stable_norm(_d(x), x.size)
+
+
+def inf_norm(X):
+    X = np.asfortranarray(np.atleast_2d(np.asarray(X, dtype=np.float64).T).T)
+    return lib().orc_inf_norm(_d(X), X.shape[0], X.shape[1], X.shape[0])
+
+
+def apply(op: Csr, X):
+    X = np.asfortranarray(np.asarray(X, dtype=np.float64).reshape(op.n, -1))
+    Y = np.empty_like(X, order="F")
+    _check(lib().orc_apply(*op.args(), _d(X), X.shape[1], _d(Y)))
+    return Y
+
+
+# ---------------------------------------------------------------------------
+# parameter selection
+# ---------------------------------------------------------------------------
+@dataclass
+class ScalingShift:
+    s: float = 1.0
+    xi: float = 0.0
+    s0: float = 1.0
+    f_min: float = 0.0
+    m: int = 61
+    r: int = 0
+
+    def c(self):
+        return ScalingShiftC(self.s, self.xi, self.s0, self.f_min, self.m, self.r)
+
+    @staticmethod
+    def from_c(c):
+        return ScalingShift(c.s, c.xi, c.s0, c.f_min, c.m, c.r)
+
+    def astuple(self):
+        return (self.s, self.xi, self.s0, self.f_min, self.m, self.r)
+
+
+class PowerBasis:
+    def __init__(self, op: Csr, m=61, delta=0.8):
+        err = C.c_int32(0)
+        self.op = op
+        self._h = lib().orc_basis_build(*op.args(), m, delta, C.byref(err))
+        _check(err.value)
+        r = C.c_int32()
+        mm = C.c_int32()
+        s0 = C.c_double()
+        lib().orc_basis_info(self._h, C.byref(r), C.byref(mm), C.byref(s0), None, None, None)
+        self.r, self.m, self.s0 = r.value, mm.value, s0.value
+        self.logs = np.empty(max(self.r, 1))
+        self.log_binom = np.empty(self.m + 1)
+        self.columns = np.empty((op.n, self.m + 1), order="F")
+        lib().orc_basis_info(self._h, C.byref(r), C.byref(mm), C.byref(s0), _d(self.logs),
+                             _d(self.columns), _d(self.log_binom))
+        self.logs = self.logs[: self.r]
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().orc_basis_free(self._h)
+            self._h = None
+
+    def objective(self, xi):
+        f = C.c_double()
+        _check(lib().orc_objective(self._h, xi, C.byref(f)))
+        return f.value
+
+    def minimize_shift(self, with_path=False):
+        xi, fm = C.c_double(), C.c_double()
+        if with_path:
+            path = np.empty(4096)
+            ln = C.c_int64()
+            _check(lib().orc_minimize_shift(self._h, C.byref(xi), C.byref(fm), _d(path), 4096,
+                                            C.byref(ln)))
+            return xi.value, fm.value, path[: ln.value].reshape(-1, 2)
+        _check(lib().orc_minimize_shift(self._h, C.byref(xi), C.byref(fm), None, 0, None))
+        return xi.value, fm.value
+
+    def parameters_for_shift(self, xi, tol):
+        out = ScalingShiftC()
+        _check(lib().orc_parameters_for_shift(*self.op.args(), self._h, xi, tol, C.byref(out)))
+        return ScalingShift.from_c(out)
+
+
+def build_power_basis(op, m=61, delta=0.8):
+    return PowerBasis(op, m, delta)
+
+
+def log_shifted_power(op: Csr, v, xi, m):
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().orc_log_shifted_power(*op.args(), _d(v), xi, m, C.byref(out)))
+    return out.value
+
+
+def select_parameters(op: Csr, m=61, tol=-1.0, delta=0.8) -> ScalingShift:
+    out = ScalingShiftC()
+    _check(lib().orc_select_parameters(*op.args(), m, tol, delta, C.byref(out)))
+    return ScalingShift.from_c(out)
+
+
+# ---------------------------------------------------------------------------
+# evaluators
+# ---------------------------------------------------------------------------
+@dataclass
+class RunRecord:
+    s_effective: int
+    series_len_S: int
+    series_lens_F: list
+    matvecs: int
+
+
+def _rec(rec4, lens):
+    return RunRecord(int(rec4[0]), int(rec4[1]), [int(x) for x in lens[: int(rec4[2])]], int(rec4[3]))
+
+
+def phimv_block(op: Csr, t, alpha, V, tol, params: ScalingShift, trace=False, lens_cap=1 << 16):
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+    V = np.asfortranarray(np.asarray(V, dtype=np.float64).reshape(op.n, -1))
+    r = t.size
+    W = np.empty((op.n, r), order="F")
+    rec4 = np.zeros(4, dtype=np.int64)
+    lens = np.zeros(lens_cap, dtype=np.int32)
+    pc = params.c()
+    if trace:
+        cap = 3 * 200000
+        tr = np.empty(cap)
+        tl = C.c_int64()
+        _check(lib().orc_phimv_block(*op.args(), r, _d(t), _d(alpha), V.shape[1] - 1, _d(V),
+                                     op.n, tol, C.byref(pc), _d(W), op.n,
+                                     rec4.ctypes.data_as(i64p), lens.ctypes.data_as(i32p), lens_cap,
+                                     _d(tr), cap, C.byref(tl)))
+        return W, _rec(rec4, lens), tr[: tl.value].reshape(-1, 3)
+    _check(lib().orc_phimv_block(*op.args(), r, _d(t), _d(alpha), V.shape[1] - 1, _d(V), op.n,
+                                 tol, C.byref(pc), _d(W), op.n, rec4.ctypes.data_as(i64p),
+                                 lens.ctypes.data_as(i32p), lens_cap, None, 0, None))
+    return W, _rec(rec4, lens)
+
+
+def phimv(op: Csr, t, alpha, V, tol, params: ScalingShift, lens_cap=1 << 16):
+    V = np.asfortranarray(np.asarray(V, dtype=np.float64).reshape(op.n, -1))
+    w = np.empty(op.n)
+    e0 = np.empty(op.n)
+    tail = np.empty(op.n)
+    rec4 = np.zeros(4, dtype=np.int64)
+    lens = np.zeros(lens_cap, dtype=np.int32)
+    pc = params.c()
+    _check(lib().orc_phimv(*op.args(), float(t), float(alpha), V.shape[1] - 1, _d(V), op.n, tol,
+                           C.byref(pc), _d(w), _d(e0), _d(tail), rec4.ctypes.data_as(i64p),
+                           lens.ctypes.data_as(i32p), lens_cap))
+    return w, e0, tail, _rec(rec4, lens)
+
+
+def reference_w(A, V, t, alpha):
+    A = np.asfortranarray(np.asarray(A, dtype=np.float64))
+    n = A.shape[0]
+    V = np.asfortranarray(np.asarray(V, dtype=np.float64).reshape(n, -1))
+    out = np.empty(n)
+    _check(lib().orc_reference_w(n, _d(A), V.shape[1] - 1, _d(V), t, alpha, _d(out)))
+    return out
+
+
+def dense_phi(M, t, jmax):
+    M = np.asfortranarray(np.asarray(M, dtype=np.float64))
+    d = M.shape[0]
+    out = np.empty((jmax + 1) * d * d)
+    _check(lib().orc_dense_phi(d, _d(M), t, jmax, _d(out)))
+    return [out[k * d * d:(k + 1) * d * d].reshape(d, d, order="F") for k in range(jmax + 1)]
+
+
+def jexp_chain(alpha, s, p):
+    out = np.empty(p + 1)
+    lib().orc_jexp_chain(alpha, s, p, _d(out))
+    return out

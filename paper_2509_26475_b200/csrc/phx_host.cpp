@@ -1,0 +1,1070 @@
+// Host orchestration of the phi-combination engine behind the C ABI in
+// include/phx.h.  Everything numeric that is not a kernel is scalar control
+// (s_eff, mu, coefficient tables, Brent, guard tests, stableNorm block
+// scaling) and runs here on the CPU in the reference's operation order; all
+// n-sized work runs in the sm_100a kernels of phx_kernels.cu.  There is no
+// CPU fallback for n-sized work: without a device every call fails with
+// PHX_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/phx.h"
+#include "phx_kernels.cuh"
+#include "rng.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+phx_status fail(phx_status code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct CudaError {
+  cudaError_t e;
+  const char* what;
+};
+
+#define PHX_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) throw CudaError{e_, #call};   \
+  } while (0)
+
+struct PhxError {
+  phx_status code;
+  std::string msg;
+};
+
+[[noreturn]] void throw_phx(phx_status code, const std::string& msg) { throw PhxError{code, msg}; }
+
+template <class F>
+phx_status guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return PHX_OK;
+  } catch (const PhxError& e) {
+    return fail(e.code, e.msg);
+  } catch (const CudaError& e) {
+    return fail(PHX_ECUDA, std::string("CUDA error ") + cudaGetErrorString(e.e) + " in " + e.what);
+  } catch (const std::bad_alloc&) {
+    return fail(PHX_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(PHX_ECUDA, e.what());
+  }
+}
+
+// grow-only device buffer
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      PHX_CUDA(cudaMalloc(&p, bytes));
+      cap = bytes;
+    }
+    return p;
+  }
+  template <class T>
+  T* as(size_t count) {
+    return static_cast<T*>(get(count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct HostBuf {  // grow-only pinned host buffer
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      PHX_CUDA(cudaMallocHost(&p, bytes));
+      cap = bytes;
+    }
+    return p;
+  }
+  template <class T>
+  T* as(size_t count) {
+    return static_cast<T*>(get(count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+int64_t pow2ceil(int64_t w) {
+  int64_t p = 1;
+  while (p < w) p <<= 1;
+  return p;
+}
+
+// trace configuration (process-wide, for parity debugging)
+std::mutex g_trace_mu;
+int64_t g_trace_cap = 0;
+std::vector<double> g_trace;
+int64_t g_trace_len = 0;
+double g_last_ms = 0.0;
+int64_t g_last_steps = 0;
+
+}  // namespace
+
+struct phx_op_s {
+  int device = 0;
+  int64_t n = 0, nnz = 0;
+  int32_t* d_rp = nullptr;
+  int32_t* d_ci = nullptr;
+  double* d_av = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::mutex mu;
+  // evaluation workspace
+  DevBuf Vw, D0, D1, S, F0, F1, E, W, V, coef, slots, status, lensF, FLo, FRo, trace;
+  // selection workspace
+  DevBuf w0, w1, y, chunkmax, inv, partial, gcoef, spx, spy;
+  HostBuf h_small, h_chunk, h_inv, h_part, h_lens;
+  // fixed-seed start vectors (params.cpp:102-110), cached per operator
+  std::vector<double> start1, start2;
+  bool have_start2 = false;
+};
+
+struct phx_basis_s {
+  phx_op op = nullptr;
+  int m = 0, r = 0;
+  double s0 = 1.0;
+  std::vector<double> logs, log_binom;
+  double* d_cols = nullptr;  // n x (m+1) column-major
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    PHX_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// stableNorm (params.cpp call sites :108,117,124,168,201) on a device vector:
+// chunk maxima on the device, Eigen's sequential block-scale logic here, the
+// scaled chunk sums of squares on the device, the fold here.
+// ---------------------------------------------------------------------------
+double stable_norm_dev(phx_op op, const double* d_x, int64_t n, bool have_chunkmax) {
+  cudaStream_t st = op->stream;
+  if (n == 1) {
+    double* h = op->h_small.as<double>(1);
+    PHX_CUDA(cudaMemcpyAsync(h, d_x, sizeof(double), cudaMemcpyDeviceToHost, st));
+    PHX_CUDA(cudaStreamSynchronize(st));
+    return std::fabs(h[0]);
+  }
+  const int64_t nch = (n + phx::kChunk - 1) / phx::kChunk;
+  auto* d_max = op->chunkmax.as<unsigned long long>(size_t(nch));
+  if (!have_chunkmax) PHX_CUDA(phx::launch_chunkmax(int32_t(n), d_x, d_max, st));
+  auto* h_max = op->h_chunk.as<unsigned long long>(size_t(nch));
+  PHX_CUDA(cudaMemcpyAsync(h_max, d_max, size_t(nch) * 8, cudaMemcpyDeviceToHost, st));
+  PHX_CUDA(cudaStreamSynchronize(st));
+  double* h_inv = op->h_inv.as<double>(size_t(nch));
+  std::vector<double> ratio(static_cast<size_t>(nch));
+  std::vector<char> rescale(static_cast<size_t>(nch)), add(static_cast<size_t>(nch));
+  double scale = 0.0, inv_scale = 1.0;
+  for (int64_t b = 0; b < nch; ++b) {
+    double maxc;
+    std::memcpy(&maxc, &h_max[b], 8);
+    rescale[size_t(b)] = 0;
+    if (maxc > scale) {
+      rescale[size_t(b)] = 1;
+      ratio[size_t(b)] = scale / maxc;
+      const double tmp = 1.0 / maxc;
+      if (tmp > DBL_MAX) {
+        inv_scale = DBL_MAX;
+        scale = 1.0 / inv_scale;
+      } else if (maxc > DBL_MAX) {
+        inv_scale = 1.0;
+        scale = maxc;
+      } else {
+        scale = maxc;
+        inv_scale = tmp;
+      }
+    } else if (maxc != maxc) {
+      scale = maxc;
+    }
+    add[size_t(b)] = scale > 0.0;
+    h_inv[b] = inv_scale;
+  }
+  auto* d_inv = op->inv.as<double>(size_t(nch));
+  auto* d_part = op->partial.as<double>(size_t(nch));
+  PHX_CUDA(cudaMemcpyAsync(d_inv, h_inv, size_t(nch) * 8, cudaMemcpyHostToDevice, st));
+  PHX_CUDA(phx::launch_chunk_ssq(int32_t(n), d_x, d_inv, d_part, st));
+  double* h_part = op->h_part.as<double>(size_t(nch));
+  PHX_CUDA(cudaMemcpyAsync(h_part, d_part, size_t(nch) * 8, cudaMemcpyDeviceToHost, st));
+  PHX_CUDA(cudaStreamSynchronize(st));
+  double ssq = 0.0;
+  for (int64_t b = 0; b < nch; ++b) {
+    if (rescale[size_t(b)]) {
+      const double rt = ratio[size_t(b)];
+      ssq = ssq * (rt * rt);
+    }
+    if (add[size_t(b)]) ssq = ssq + h_part[b];
+  }
+  return scale * std::sqrt(ssq);
+}
+
+bool all_finite_from_chunkmax(phx_op op, int64_t n) {
+  const int64_t nch = (n + phx::kChunk - 1) / phx::kChunk;
+  auto* d_max = op->chunkmax.as<unsigned long long>(size_t(nch));
+  auto* h_max = op->h_chunk.as<unsigned long long>(size_t(nch));
+  PHX_CUDA(cudaMemcpyAsync(h_max, d_max, size_t(nch) * 8, cudaMemcpyDeviceToHost, op->stream));
+  PHX_CUDA(cudaStreamSynchronize(op->stream));
+  for (int64_t b = 0; b < nch; ++b)
+    if (h_max[b] >= 0x7FF0000000000000ull) return false;
+  return true;
+}
+
+void spmv(phx_op op, const double* x, double* y, int mode, double xi, double div, bool chunkmax) {
+  auto* d_max = chunkmax ? op->chunkmax.as<unsigned long long>(size_t((op->n + phx::kChunk - 1) /
+                                                                       phx::kChunk))
+                         : nullptr;
+  PHX_CUDA(phx::launch_spmv(int32_t(op->n), op->d_rp, op->d_ci, op->d_av, x, y, mode, xi, div,
+                            d_max, op->stream));
+}
+
+const std::vector<double>& start_vector(phx_op op, int which) {
+  if (op->start1.empty() || (which == 2 && !op->have_start2)) {
+    phx::Rng rng(0x9e3779b97f4a7c15ull);  // params.cpp:13
+    op->start1 = phx::unit_vector(rng, op->n);
+    if (which == 2) {
+      op->start2 = phx::unit_vector(rng, op->n);
+      op->have_start2 = true;
+    }
+  }
+  return which == 1 ? op->start1 : op->start2;
+}
+
+double log_binomial(int m, int j) {  // params.cpp:15-17
+  return std::lgamma(m + 1.0) - std::lgamma(j + 1.0) - std::lgamma(m - j + 1.0);
+}
+
+// build_power_basis (params.cpp:81-154) with the n-sized work on the device
+phx_basis_s* build_basis(phx_op op, int m, double delta) {
+  if (m < 1) throw_phx(PHX_EINVAL, "build_power_basis: m must be >= 1");
+  if (!(delta > 0.0 && delta <= 1.0))
+    throw_phx(PHX_EINVAL, "build_power_basis: delta must be in (0, 1]");
+  const int64_t n = op->n;
+  cudaStream_t st = op->stream;
+  const double g_max = delta * std::log(std::numeric_limits<double>::max());
+  const double g_min = delta * std::log(std::numeric_limits<double>::min());
+  auto* b = new phx_basis_s();
+  b->op = op;
+  b->m = m;
+  b->log_binom.resize(size_t(m) + 1);
+  double ell_max = 0.0;
+  for (int j = 0; j <= m; ++j) {
+    b->log_binom[size_t(j)] = log_binomial(m, j);
+    ell_max = std::max(ell_max, b->log_binom[size_t(j)]);
+  }
+  try {
+    PHX_CUDA(cudaMalloc(&b->d_cols, size_t(n) * size_t(m + 1) * sizeof(double)));
+    double* col0 = b->d_cols;
+    auto col = [&](int k) { return b->d_cols + size_t(k) * size_t(n); };
+    const std::vector<double>& v1 = start_vector(op, 1);
+    PHX_CUDA(cudaMemcpyAsync(col0, v1.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    spmv(op, col0, col(1), 0, 0.0, 1.0, true);
+    if (!all_finite_from_chunkmax(op, n))
+      throw_phx(PHX_ENUMERIC, "build_power_basis: A*v is not finite; operator rejected");
+    double first_norm = stable_norm_dev(op, col(1), n, true);
+    if (first_norm == 0.0) {
+      const std::vector<double>& v2 = start_vector(op, 2);
+      PHX_CUDA(cudaMemcpyAsync(col0, v2.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+      spmv(op, col0, col(1), 0, 0.0, 1.0, true);
+      if (!all_finite_from_chunkmax(op, n))
+        throw_phx(PHX_ENUMERIC, "build_power_basis: A*v is not finite; operator rejected");
+      first_norm = stable_norm_dev(op, col(1), n, true);
+    }
+    int r = 0;
+    for (int k = 1; k <= m; ++k) {
+      double norm_w;
+      if (k > 1) {
+        spmv(op, col(k - 1), col(k), 0, 0.0, 1.0, true);
+        norm_w = stable_norm_dev(op, col(k), n, true);
+      } else {
+        norm_w = first_norm;
+      }
+      const double L = norm_w > 0.0 ? std::log(norm_w) : -std::numeric_limits<double>::infinity();
+      if (!(L + 0.5 * std::log(k + 1.0) + ell_max <= g_max) || L < g_min) break;
+      b->logs.push_back(L);
+      r = k;
+    }
+    b->r = r;
+    if (r >= 3) {
+      const int j_r = std::max(2, r - 5);
+      b->s0 = std::exp((b->logs[size_t(r - 1)] - b->logs[size_t(j_r - 1)]) / (r - j_r));
+    } else {
+      b->s0 = std::max(first_norm, 1.0);
+    }
+    if (!(b->s0 > 0.0) || !std::isfinite(b->s0)) b->s0 = 1.0;
+    double scale = 1.0;
+    for (int j = 1; j <= r; ++j) {
+      scale /= b->s0;
+      PHX_CUDA(phx::launch_scale(int32_t(n), col(j), scale, 0, st));
+    }
+    for (int k = r + 1; k <= m; ++k) spmv(op, col(k - 1), col(k), 2, 0.0, b->s0, false);
+    PHX_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    if (b->d_cols) cudaFree(b->d_cols);
+    delete b;
+    throw;
+  }
+  return b;
+}
+
+// objective (params.cpp:156-170)
+double objective_dev(phx_basis_s* b, double xi) {
+  if (!std::isfinite(xi)) throw_phx(PHX_EINVAL, "objective: shift must be finite");
+  phx_op op = b->op;
+  const int m = b->m;
+  const double z = -xi / b->s0;
+  double* h = op->h_small.as<double>(size_t(m) + 1);
+  double zp = 1.0;
+  for (int j = m; j >= 0; --j) {
+    h[j] = std::exp(b->log_binom[size_t(j)]) * zp;
+    zp *= z;
+  }
+  double* d_c = op->gcoef.as<double>(size_t(m) + 1);
+  double* d_y = op->y.as<double>(size_t(op->n));
+  const int64_t nch = (op->n + phx::kChunk - 1) / phx::kChunk;
+  auto* d_max = op->chunkmax.as<unsigned long long>(size_t(nch));
+  PHX_CUDA(cudaMemcpyAsync(d_c, h, size_t(m + 1) * 8, cudaMemcpyHostToDevice, op->stream));
+  PHX_CUDA(phx::launch_gemv(int32_t(op->n), m + 1, b->d_cols, d_c, d_y, d_max, op->stream));
+  const double norm = stable_norm_dev(op, d_y, op->n, true);
+  return norm > 0.0 ? std::exp(std::log(norm) / m) : 0.0;
+}
+
+// brent_minimize (params.cpp:21-77), arithmetic order of the reference
+double brent_minimize(const std::function<double(double)>& f, double a, double b, double tol_x,
+                      int max_iter, std::vector<double>* path) {
+  const double golden = 0.3819660112501051;
+  double x = a + golden * (b - a);
+  double w = x, v = x;
+  double fx = f(x), fw = fx, fv = fx;
+  if (path) {
+    path->push_back(x);
+    path->push_back(fx);
+  }
+  double d = 0.0, e = 0.0;
+  for (int it = 0; it < max_iter; ++it) {
+    const double mid = 0.5 * (a + b);
+    const double tol1 = tol_x;
+    const double tol2 = 2.0 * tol1;
+    if (std::fabs(x - mid) <= tol2 - 0.5 * (b - a)) break;
+    bool golden_step = true;
+    if (std::fabs(e) > tol1) {
+      const double rr = (x - w) * (fx - fv);
+      double q = (x - v) * (fx - fw);
+      double p = (x - v) * q - (x - w) * rr;
+      q = 2.0 * (q - rr);
+      if (q > 0.0) p = -p;
+      q = std::fabs(q);
+      const double e_prev = e;
+      e = d;
+      if (std::fabs(p) < std::fabs(0.5 * q * e_prev) && p > q * (a - x) && p < q * (b - x)) {
+        d = p / q;
+        const double u = x + d;
+        if (u - a < tol2 || b - u < tol2) d = (x < mid) ? tol1 : -tol1;
+        golden_step = false;
+      }
+    }
+    if (golden_step) {
+      e = (x < mid) ? b - x : a - x;
+      d = golden * e;
+    }
+    const double u = (std::fabs(d) >= tol1) ? x + d : x + ((d > 0) ? tol1 : -tol1);
+    const double fu = f(u);
+    if (path) {
+      path->push_back(u);
+      path->push_back(fu);
+    }
+    if (fu <= fx) {
+      if (u < x) b = x;
+      else a = x;
+      v = w;
+      fv = fw;
+      w = x;
+      fw = fx;
+      x = u;
+      fx = fu;
+    } else {
+      if (u < x) a = u;
+      else b = u;
+      if (fu <= fw || w == x) {
+        v = w;
+        fv = fw;
+        w = u;
+        fw = fu;
+      } else if (fu <= fv || v == x || v == w) {
+        v = u;
+        fv = fu;
+      }
+    }
+  }
+  return x;
+}
+
+// minimize_shift (params.cpp:172-189)
+std::pair<double, double> minimize_shift_dev(phx_basis_s* b, std::vector<double>* path) {
+  const double n = double(b->op->n);
+  const double half_width = std::sqrt(n) * b->s0;
+  const auto f = [b](double xi) { return objective_dev(b, xi); };
+  const double tol_x = 1e-8 * (1.0 + b->s0);
+  double xi_star = brent_minimize(f, -half_width, half_width, tol_x, 200, path);
+  double f_min = f(xi_star);
+  const double f0 = f(0.0);
+  if (f0 <= f_min) {
+    xi_star = 0.0;
+    f_min = f0;
+  }
+  for (const double edge : {-half_width, half_width}) {
+    const double fe = f(edge);
+    if (fe < f_min) {
+      xi_star = edge;
+      f_min = fe;
+    }
+  }
+  return {xi_star, f_min};
+}
+
+// log_shifted_power (params.cpp:195-209)
+double log_shifted_power_dev(phx_basis_s* b, double xi, int m) {
+  phx_op op = b->op;
+  const int64_t n = op->n;
+  double* w0 = op->w0.as<double>(size_t(n));
+  double* w1 = op->w1.as<double>(size_t(n));
+  PHX_CUDA(cudaMemcpyAsync(w0, b->d_cols, size_t(n) * 8, cudaMemcpyDeviceToDevice, op->stream));
+  double acc = 0.0;
+  for (int k = 0; k < m; ++k) {
+    spmv(op, w0, w1, xi == 0.0 ? 0 : 1, xi, 1.0, true);
+    const double nw = stable_norm_dev(op, w1, n, true);
+    if (!(nw > 0.0) || !std::isfinite(nw))
+      return nw == 0.0 ? -std::numeric_limits<double>::infinity()
+                       : std::numeric_limits<double>::infinity();
+    acc += std::log(nw);
+    PHX_CUDA(phx::launch_scale(int32_t(n), w1, nw, 1, op->stream));
+    std::swap(w0, w1);
+  }
+  return acc;
+}
+
+// parameters_for_shift (params.cpp:213-239)
+phx_scaling_shift params_for_shift_dev(phx_basis_s* b, double xi, double tol) {
+  if (!(tol > 0.0)) throw_phx(PHX_EINVAL, "parameters_for_shift: tol must be positive");
+  const int m = b->m;
+  const double f_basis = objective_dev(b, xi);
+  const double log_nu = log_shifted_power_dev(b, xi, m);
+  const double f_direct = std::isfinite(log_nu) ? std::exp(log_nu / m) / b->s0 : 0.0;
+  const double f_val = std::max(f_basis, f_direct) * (1.0 + 1e-6);
+  phx_scaling_shift out{};
+  out.xi = xi;
+  out.s0 = b->s0;
+  out.f_min = f_val;
+  out.m = m;
+  out.r = b->r;
+  const double denom = std::exp((std::log(tol) + std::lgamma(m + 1.0)) / m);
+  out.s = f_val > 0.0 ? b->s0 * f_val / denom : 0.0;
+  out.s = std::max(out.s, 9.5367431640625e-7);
+  if (!std::isfinite(out.s)) throw_phx(PHX_ENUMERIC, "parameters_for_shift: scaling is not finite");
+  return out;
+}
+
+void destroy_basis(phx_basis_s* b) {
+  if (!b) return;
+  if (b->d_cols) cudaFree(b->d_cols);
+  delete b;
+}
+
+bool finite_all(const double* x, size_t n) {
+  for (size_t q = 0; q < n; ++q)
+    if (!std::isfinite(x[q])) return false;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Block evaluator (phi_block.cpp:48-157) / single evaluator
+// (phi_single.cpp:38-127, r = 1) — host preparation + one persistent launch.
+// ---------------------------------------------------------------------------
+struct EvalIn {
+  int32_t r, p;
+  const double* t;
+  const double* alpha;
+  const double* hV;  // host V (col-major) or nullptr
+  int64_t ldv;
+  const double* dV;  // device V (col-major, ld n) or nullptr
+  double tol;
+  phx_scaling_shift params;
+  double* hW;  // host W or nullptr
+  int64_t ldw;
+  double* dW;  // device W (ld n) or nullptr
+  bool single;
+  double* h_exp_v0;
+  double* h_tail;
+};
+
+void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
+  const char* who = in.single ? "phimv" : "phimv_block";
+  const int64_t n = op->n;
+  const int32_t r = in.r;
+  const int32_t p = in.p;
+  const double tol = in.tol > 0.0 ? in.tol : std::ldexp(1.0, -53);
+  const double xi = in.params.xi;
+  cudaStream_t st = op->stream;
+
+  double tmax = 0.0;
+  for (int32_t i = 0; i < r; ++i) tmax = std::max(tmax, std::fabs(in.t[i]));
+  const double prod = in.single ? std::fabs(in.t[0]) * in.params.s : in.params.s * tmax;
+  const double sc = std::ceil(prod);
+  if (!(sc < 2147483647.0))
+    throw_phx(PHX_EINVAL, std::string(who) + ": s_eff = ceil(s*max|t|) exceeds the supported range");
+  const long s_eff = std::max<long>(1, long(sc));  // :58-59
+
+  std::vector<double> mu(static_cast<size_t>(r)), g(static_cast<size_t>(r));
+  for (int32_t i = 0; i < r; ++i) {
+    mu[size_t(i)] = in.single ? std::exp(in.t[i] * xi / double(s_eff))
+                              : std::exp(xi * in.t[i] / double(s_eff));
+    if (!std::isfinite(mu[size_t(i)]))
+      throw_phx(PHX_ENUMERIC, std::string(who) + ": shift undo factor e^{t xi / s} overflows");
+    g[size_t(i)] = mu[size_t(i)] / double(s_eff);
+  }
+  const int32_t w = (p + 1) * r;
+  const int32_t fcols = p == 0 ? r : 2 * r;
+  // coefficient table: colKd[w] colKa[w] colTos[w] t[r] alpha[r] mu[r] g[r] jc[r*(p+1)]
+  const size_t ncoef = size_t(3 * w + 4 * r + r * (p + 1));
+  std::vector<double> coef(ncoef, 0.0);
+  double* cKd = coef.data();
+  double* cKa = cKd + w;
+  double* cTos = cKa + w;
+  double* ct = cTos + w;
+  double* cal = ct + r;
+  double* cmu = cal + r;
+  double* cg = cmu + r;
+  double* cjc = cg + r;
+  for (int32_t i = 0; i < r; ++i) {
+    // Kiter (nilpotent.cpp:54-71, phi_block.cpp:74); single: Jiter (:269-271)
+    const double kd = in.single ? (0.0 - in.t[i] * xi) / double(s_eff)
+                                : (0.0 - xi * in.t[i]) / double(s_eff);
+    const double ka = (1.0 * in.alpha[i]) / double(s_eff);
+    const double tos = in.t[i] / double(s_eff);
+    for (int32_t j = 0; j <= p; ++j) {
+      const int32_t c = j * r + i;
+      cKd[c] = kd;
+      cKa[c] = j >= 2 ? ka : 0.0;
+      cTos[c] = tos;
+    }
+    ct[i] = in.t[i];
+    cal[i] = in.alpha[i];
+    cmu[i] = mu[size_t(i)];
+    cg[i] = g[size_t(i)];
+    // Jexp chain (nilpotent.cpp:12-21, 38-52)
+    double* cc = cjc + size_t(i) * size_t(p + 1);
+    cc[0] = 1.0;
+    const double kexp = in.alpha[i] / double(s_eff);
+    for (int32_t d = 1; d <= p; ++d) cc[d] = (cc[d - 1] * kexp) / double(d);
+  }
+
+  // layouts
+  const int32_t GS = int32_t(std::min<int64_t>(32, pow2ceil(w)));
+  const int32_t QS = (w + GS - 1) / GS;
+  const int32_t GF = int32_t(std::min<int64_t>(32, pow2ceil(fcols)));
+  const int32_t QF = (fcols + GF - 1) / GF;
+  const int32_t QT = int32_t(pow2ceil(std::max(QS, QF)));
+  if (QT > 8)
+    throw_phx(PHX_EINVAL, std::string(who) + ": block width (p+1)*r above 256 is not supported");
+  const int block = 256;
+  const int32_t tile = block / std::min(GS, GF);
+
+  // workspace
+  const int32_t ldb = w, ldf = fcols;
+  const size_t nb = size_t(n) * size_t(ldb), nf = size_t(n) * size_t(ldf);
+  phx::BlockArgs a{};
+  a.n = int32_t(n);
+  a.rp = op->d_rp;
+  a.ci = op->d_ci;
+  a.av = op->d_av;
+  a.p = p;
+  a.r = r;
+  a.w = w;
+  a.fcols = fcols;
+  a.GS = GS;
+  a.QS = QS;
+  a.GF = GF;
+  a.QF = QF;
+  a.QT = QT;
+  a.tile = tile;
+  a.xi = xi;
+  a.tol = tol;
+  a.s_eff = int32_t(s_eff);
+  a.single_variant = in.single ? 1 : 0;
+  a.t_single = in.t[0];
+  double* d_coef = op->coef.as<double>(ncoef);
+  a.colKd = d_coef;
+  a.colKa = d_coef + w;
+  a.colTos = d_coef + 2 * w;
+  a.t = d_coef + 3 * w;
+  a.alpha = a.t + r;
+  a.mu = a.alpha + r;
+  a.g = a.mu + r;
+  a.jc = a.g + r;
+  a.Vw = op->Vw.as<double>(nb);
+  a.D0 = op->D0.as<double>(nb);
+  a.D1 = op->D1.as<double>(nb);
+  a.S = op->S.as<double>(nb);
+  a.ldb = ldb;
+  a.F0 = op->F0.as<double>(nf);
+  a.F1 = op->F1.as<double>(nf);
+  a.E = op->E.as<double>(nf);
+  a.ldf = ldf;
+  a.W = in.dW ? in.dW : op->W.as<double>(size_t(n) * size_t(r));
+  a.FLo = in.h_exp_v0 ? op->FLo.as<double>(size_t(n) * size_t(r)) : nullptr;
+  a.FRo = in.h_tail ? op->FRo.as<double>(size_t(n) * size_t(r)) : nullptr;
+  a.slots = op->slots.as<unsigned long long>(6);
+  a.status = op->status.as<int32_t>(8);
+  a.lensF = op->lensF.as<int32_t>(size_t(std::max<long>(1, s_eff - 1)));
+  int64_t trace_cap;
+  {
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    trace_cap = g_trace_cap;
+  }
+  a.trace = trace_cap > 0 ? op->trace.as<double>(size_t(trace_cap)) : nullptr;
+  a.trace_cap = int32_t(trace_cap);
+
+  if (in.dV) {
+    a.V = in.dV;
+  } else {
+    double* dV = op->V.as<double>(size_t(n) * size_t(p + 1));
+    if (in.ldv == n)
+      PHX_CUDA(cudaMemcpyAsync(dV, in.hV, size_t(n) * size_t(p + 1) * 8, cudaMemcpyHostToDevice, st));
+    else
+      PHX_CUDA(cudaMemcpy2DAsync(dV, size_t(n) * 8, in.hV, size_t(in.ldv) * 8, size_t(n) * 8,
+                                 size_t(p + 1), cudaMemcpyHostToDevice, st));
+    a.V = dV;
+  }
+  PHX_CUDA(cudaMemcpyAsync(d_coef, coef.data(), ncoef * 8, cudaMemcpyHostToDevice, st));
+  PHX_CUDA(cudaMemsetAsync(a.slots, 0, 6 * sizeof(unsigned long long), st));
+  PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), st));
+
+  int max_blocks = 0;
+  PHX_CUDA(phx::coop_grid_size(QT, block, &max_blocks));
+  const int64_t ntiles = (n + tile - 1) / tile;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(max_blocks, ntiles)));
+  PHX_CUDA(cudaEventRecord(op->ev0, st));
+  PHX_CUDA(phx::launch_phimv_block(a, grid, block, st));
+  PHX_CUDA(cudaEventRecord(op->ev1, st));
+
+  int32_t* h_status = op->h_small.as<int32_t>(8);
+  PHX_CUDA(cudaMemcpyAsync(h_status, a.status, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  const long nsw = s_eff - 1;
+  int32_t* h_lens = op->h_lens.as<int32_t>(size_t(std::max<long>(1, nsw)));
+  if (nsw > 0)
+    PHX_CUDA(cudaMemcpyAsync(h_lens, a.lensF, size_t(nsw) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (in.hW) {
+    if (in.ldw == n)
+      PHX_CUDA(cudaMemcpyAsync(in.hW, a.W, size_t(n) * size_t(r) * 8, cudaMemcpyDeviceToHost, st));
+    else
+      PHX_CUDA(cudaMemcpy2DAsync(in.hW, size_t(in.ldw) * 8, a.W, size_t(n) * 8, size_t(n) * 8,
+                                 size_t(r), cudaMemcpyDeviceToHost, st));
+  }
+  if (in.h_exp_v0)
+    PHX_CUDA(cudaMemcpyAsync(in.h_exp_v0, a.FLo, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
+  if (in.h_tail)
+    PHX_CUDA(cudaMemcpyAsync(in.h_tail, a.FRo, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
+  PHX_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  PHX_CUDA(cudaEventElapsedTime(&ms, op->ev0, op->ev1));
+  {
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    g_last_ms = ms;
+    g_last_steps = h_status[4];
+    if (trace_cap > 0) {
+      g_trace.assign(size_t(trace_cap), 0.0);
+      g_trace_len = h_status[5];
+      PHX_CUDA(cudaMemcpy(g_trace.data(), a.trace, size_t(trace_cap) * 8, cudaMemcpyDeviceToHost));
+    }
+  }
+
+  const int32_t code = h_status[0];
+  const int32_t idx = h_status[1];
+  const int32_t L_S = h_status[2];
+  if (code == phx::kStSeriesCap)
+    throw_phx(PHX_ENUMERIC, std::string(who) + ": series did not converge within 500 terms");
+  if (code == phx::kStSeriesDiverged)
+    throw_phx(PHX_ENUMERIC, std::string(who) + ": series produced a non-finite term at index " +
+                                std::to_string(idx));
+  if (code == phx::kStRecoveryCap)
+    throw_phx(PHX_ENUMERIC, std::string(who) + ": recovery sweep did not converge within 300 terms");
+  if (code == phx::kStRecoveryDiverged)
+    throw_phx(PHX_ENUMERIC, std::string(who) +
+                                ": recovery sweep produced a non-finite term at index " +
+                                std::to_string(idx));
+  if (rec) {
+    rec->s_effective = s_eff;
+    rec->series_len_S = L_S;
+    rec->n_sweeps = int32_t(nsw);
+    int64_t mv = int64_t(L_S - 1) * int64_t(w) + r;  // :100, :117
+    for (long q = 0; q < nsw; ++q) {
+      mv += int64_t(fcols) * int64_t(h_lens[q]);  // :133
+      if (rec->series_lens_F && q < rec->lens_capacity) rec->series_lens_F[q] = h_lens[q];
+    }
+    rec->matvecs = mv;
+  }
+}
+
+void check_block_request(phx_op op, int32_t r, const double* t, const double* alpha, int32_t p,
+                         const double* V, int64_t ldv, bool host_v) {
+  // check_request (phi_block.cpp:15-27)
+  if (r <= 0) throw_phx(PHX_EINVAL, "phimv_block: at least one abscissa required");
+  if (!t || !alpha) throw_phx(PHX_EINVAL, "phimv_block: t and alpha lengths differ");
+  if (p < 0) throw_phx(PHX_EINVAL, "phimv_block: V must have at least one column");
+  if (host_v && ldv < op->n) throw_phx(PHX_EINVAL, "phimv_block: V row count does not match operator");
+  bool fin = finite_all(t, size_t(r)) && finite_all(alpha, size_t(r));
+  if (host_v && fin)
+    for (int32_t j = 0; j <= p && fin; ++j) fin = finite_all(V + size_t(j) * size_t(ldv), size_t(op->n));
+  if (!fin) throw_phx(PHX_EINVAL, "phimv_block: inputs must be finite");
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* phx_last_error(void) { return g_err.c_str(); }
+
+int64_t phx_kernel_launches(void) { return phx::kernel_launch_count(); }
+
+phx_status phx_op_create_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                             const double* vals, int32_t device, phx_op* out) {
+  return guarded([&] {
+    if (!out) throw_phx(PHX_EINVAL, "phx_op_create_csr: out is null");
+    *out = nullptr;
+    if (n < 1) throw_phx(PHX_EINVAL, "phx_op_create_csr: n must be >= 1");
+    if (n >= (int64_t(1) << 31) - 1) throw_phx(PHX_EINVAL, "phx_op_create_csr: n must be < 2^31");
+    if (!row_ptr || row_ptr[0] != 0) throw_phx(PHX_EINVAL, "phx_op_create_csr: row_ptr[0] must be 0");
+    const int64_t nnz = row_ptr[n];
+    if (nnz < 0 || nnz >= (int64_t(1) << 31))
+      throw_phx(PHX_EINVAL, "phx_op_create_csr: nnz must be in [0, 2^31)");
+    for (int64_t i = 0; i < n; ++i)
+      if (row_ptr[i + 1] < row_ptr[i]) throw_phx(PHX_EINVAL, "phx_op_create_csr: row_ptr not monotone");
+    for (int64_t e = 0; e < nnz; ++e) {
+      if (col_idx[e] < 0 || col_idx[e] >= n)
+        throw_phx(PHX_EINVAL, "phx_op_create_csr: column index out of range");
+      if (!std::isfinite(vals[e]))
+        throw_phx(PHX_EINVAL, "dense_operator: matrix has non-finite entries");
+    }
+    int dev = device;
+    if (dev < 0) PHX_CUDA(cudaGetDevice(&dev));
+    DeviceGuard guard(dev);
+    auto* op = new phx_op_s();
+    op->device = dev;
+    op->n = n;
+    op->nnz = nnz;
+    try {
+      PHX_CUDA(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
+      PHX_CUDA(cudaEventCreate(&op->ev0));
+      PHX_CUDA(cudaEventCreate(&op->ev1));
+      std::vector<int32_t> rp32(size_t(n) + 1);
+      for (int64_t i = 0; i <= n; ++i) rp32[size_t(i)] = int32_t(row_ptr[i]);
+      PHX_CUDA(cudaMalloc(&op->d_rp, (size_t(n) + 1) * 4));
+      PHX_CUDA(cudaMalloc(&op->d_ci, std::max<size_t>(1, size_t(nnz)) * 4));
+      PHX_CUDA(cudaMalloc(&op->d_av, std::max<size_t>(1, size_t(nnz)) * 8));
+      PHX_CUDA(cudaMemcpy(op->d_rp, rp32.data(), (size_t(n) + 1) * 4, cudaMemcpyHostToDevice));
+      if (nnz > 0) {
+        PHX_CUDA(cudaMemcpy(op->d_ci, col_idx, size_t(nnz) * 4, cudaMemcpyHostToDevice));
+        PHX_CUDA(cudaMemcpy(op->d_av, vals, size_t(nnz) * 8, cudaMemcpyHostToDevice));
+      }
+    } catch (...) {
+      phx_op_destroy(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
+phx_status phx_op_destroy(phx_op op) {
+  if (!op) return PHX_OK;
+  {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(op->device);
+    if (op->stream) cudaStreamSynchronize(op->stream);
+    for (DevBuf* b : {&op->Vw, &op->D0, &op->D1, &op->S, &op->F0, &op->F1, &op->E, &op->W, &op->V,
+                      &op->coef, &op->slots, &op->status, &op->lensF, &op->FLo, &op->FRo,
+                      &op->trace, &op->w0, &op->w1, &op->y, &op->chunkmax, &op->inv,
+                      &op->partial, &op->gcoef, &op->spx, &op->spy})
+      b->release();
+    for (HostBuf* b : {&op->h_small, &op->h_chunk, &op->h_inv, &op->h_part, &op->h_lens}) b->release();
+    if (op->d_rp) cudaFree(op->d_rp);
+    if (op->d_ci) cudaFree(op->d_ci);
+    if (op->d_av) cudaFree(op->d_av);
+    if (op->ev0) cudaEventDestroy(op->ev0);
+    if (op->ev1) cudaEventDestroy(op->ev1);
+    if (op->stream) cudaStreamDestroy(op->stream);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete op;
+  return PHX_OK;
+}
+
+int64_t phx_op_dim(phx_op op) { return op ? op->n : 0; }
+int64_t phx_op_nnz(phx_op op) { return op ? op->nnz : 0; }
+
+static phx_status apply_impl(phx_op op, int mode, double xi, const double* X, int64_t ldx,
+                             int64_t k, double* Y, int64_t ldy) {
+  return guarded([&] {
+    if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    if (mode == 1 && !std::isfinite(xi)) throw_phx(PHX_EINVAL, "shifted_apply: shift must be finite");
+    if (ldx < op->n || ldy < op->n)
+      throw_phx(PHX_EINVAL, "LinearOperator::apply: block rows do not match the operator dimension");
+    if (k <= 0) return;
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    const int64_t n = op->n;
+    double* dX = op->spx.as<double>(size_t(n) * size_t(k));
+    double* dY = op->spy.as<double>(size_t(n) * size_t(k));
+    PHX_CUDA(cudaMemcpy2DAsync(dX, size_t(n) * 8, X, size_t(ldx) * 8, size_t(n) * 8, size_t(k),
+                               cudaMemcpyHostToDevice, op->stream));
+    PHX_CUDA(phx::launch_spmm_cols(int32_t(n), int32_t(k), op->d_rp, op->d_ci, op->d_av, dX, dY,
+                                   (mode == 1 && xi != 0.0) ? 1 : 0, xi, op->stream));
+    PHX_CUDA(cudaMemcpy2DAsync(Y, size_t(ldy) * 8, dY, size_t(n) * 8, size_t(n) * 8, size_t(k),
+                               cudaMemcpyDeviceToHost, op->stream));
+    PHX_CUDA(cudaStreamSynchronize(op->stream));
+  });
+}
+
+phx_status phx_apply(phx_op op, const double* X, int64_t ldx, int64_t k, double* Y, int64_t ldy) {
+  return apply_impl(op, 0, 0.0, X, ldx, k, Y, ldy);
+}
+phx_status phx_shifted_apply(phx_op op, double xi, const double* X, int64_t ldx, int64_t k,
+                             double* Y, int64_t ldy) {
+  return apply_impl(op, 1, xi, X, ldx, k, Y, ldy);
+}
+
+phx_status phx_basis_build(phx_op op, int32_t m, double delta, phx_basis* out) {
+  return guarded([&] {
+    if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    *out = build_basis(op, m, delta);
+  });
+}
+
+phx_status phx_basis_destroy(phx_basis b) {
+  if (!b) return PHX_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(b->op->device);
+  destroy_basis(b);
+  if (prev >= 0) cudaSetDevice(prev);
+  return PHX_OK;
+}
+
+phx_status phx_basis_info(phx_basis b, int32_t* r, int32_t* m, double* s0, double* logs,
+                          double* log_binom, double* columns) {
+  return guarded([&] {
+    if (r) *r = b->r;
+    if (m) *m = b->m;
+    if (s0) *s0 = b->s0;
+    if (logs) std::copy(b->logs.begin(), b->logs.end(), logs);
+    if (log_binom) std::copy(b->log_binom.begin(), b->log_binom.end(), log_binom);
+    if (columns) {
+      DeviceGuard guard(b->op->device);
+      PHX_CUDA(cudaMemcpy(columns, b->d_cols, size_t(b->op->n) * size_t(b->m + 1) * 8,
+                          cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+phx_status phx_objective(phx_basis b, double xi, double* f) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(b->op->mu);
+    DeviceGuard guard(b->op->device);
+    *f = objective_dev(b, xi);
+  });
+}
+
+phx_status phx_minimize_shift(phx_basis b, double* xi, double* f_min, double* path,
+                              int64_t path_capacity, int64_t* path_len) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(b->op->mu);
+    DeviceGuard guard(b->op->device);
+    std::vector<double> pth;
+    auto res = minimize_shift_dev(b, path ? &pth : nullptr);
+    *xi = res.first;
+    *f_min = res.second;
+    if (path) {
+      if (path_len) *path_len = int64_t(pth.size());
+      for (int64_t q = 0; q < int64_t(pth.size()) && q < path_capacity; ++q) path[q] = pth[size_t(q)];
+    }
+  });
+}
+
+phx_status phx_parameters_for_shift(phx_op op, phx_basis b, double xi, double tol,
+                                    phx_scaling_shift* out) {
+  return guarded([&] {
+    if (!op || op != b->op) throw_phx(PHX_EINVAL, "parameters_for_shift: basis belongs to another operator");
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    *out = params_for_shift_dev(b, xi, tol);
+  });
+}
+
+phx_status phx_select_parameters(phx_op op, int32_t m, double tol, double delta,
+                                 phx_scaling_shift* out) {
+  return guarded([&] {
+    if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    if (tol <= 0.0) tol = std::ldexp(1.0, -53);  // params.cpp:243
+    phx_basis_s* b = build_basis(op, m, delta);
+    try {
+      const double xi_star = minimize_shift_dev(b, nullptr).first;
+      *out = params_for_shift_dev(b, xi_star, tol);
+    } catch (...) {
+      destroy_basis(b);
+      throw;
+    }
+    destroy_basis(b);
+  });
+}
+
+phx_status phx_phimv_block(phx_op op, int32_t r, const double* t, const double* alpha, int32_t p,
+                           const double* V, int64_t ldv, double tol,
+                           const phx_scaling_shift* params, double* W, int64_t ldw,
+                           phx_run_record* rec) {
+  return guarded([&] {
+    if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    check_block_request(op, r, t, alpha, p, V, ldv, true);
+    if (!params) throw_phx(PHX_EINVAL, "phimv_block: params is null");
+    if (ldw < op->n) throw_phx(PHX_EINVAL, "phimv_block: W leading dimension below n");
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    EvalIn in{};
+    in.r = r;
+    in.p = p;
+    in.t = t;
+    in.alpha = alpha;
+    in.hV = V;
+    in.ldv = ldv;
+    in.tol = tol;
+    in.params = *params;
+    in.hW = W;
+    in.ldw = ldw;
+    evaluate(op, in, rec);
+  });
+}
+
+phx_status phx_phimv_block_device(phx_op op, int32_t r, const double* t, const double* alpha,
+                                  int32_t p, const double* d_V, double tol,
+                                  const phx_scaling_shift* params, double* d_W,
+                                  phx_run_record* rec) {
+  return guarded([&] {
+    if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    check_block_request(op, r, t, alpha, p, nullptr, op->n, false);
+    if (!params || !d_V || !d_W) throw_phx(PHX_EINVAL, "phimv_block: null argument");
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    EvalIn in{};
+    in.r = r;
+    in.p = p;
+    in.t = t;
+    in.alpha = alpha;
+    in.dV = d_V;
+    in.tol = tol;
+    in.params = *params;
+    in.dW = d_W;
+    evaluate(op, in, rec);
+  });
+}
+
+phx_status phx_phimv(phx_op op, double t, double alpha, int32_t p, const double* V, int64_t ldv,
+                     double tol, const phx_scaling_shift* params, double* w, double* exp_v0,
+                     double* tail, phx_run_record* rec) {
+  return guarded([&] {
+    if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    // check_request (phi_single.cpp:15-24)
+    if (p < 0) throw_phx(PHX_EINVAL, "phimv: V must have at least one column");
+    if (ldv < op->n) throw_phx(PHX_EINVAL, "phimv: V row count does not match operator");
+    for (int32_t j = 0; j <= p; ++j)
+      if (!finite_all(V + size_t(j) * size_t(ldv), size_t(op->n)))
+        throw_phx(PHX_EINVAL, "phimv: V has non-finite entries");
+    if (!std::isfinite(t) || !std::isfinite(alpha))
+      throw_phx(PHX_EINVAL, "phimv: t and alpha must be finite");
+    if (!params) throw_phx(PHX_EINVAL, "phimv: params is null");
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    EvalIn in{};
+    in.r = 1;
+    in.p = p;
+    in.t = &t;
+    in.alpha = &alpha;
+    in.hV = V;
+    in.ldv = ldv;
+    in.tol = tol;
+    in.params = *params;
+    in.hW = w;
+    in.ldw = op->n;
+    in.single = true;
+    in.h_exp_v0 = exp_v0;
+    in.h_tail = tail;
+    evaluate(op, in, rec);
+  });
+}
+
+phx_status phx_last_eval_stats(double* kernel_ms, int64_t* steps) {
+  std::lock_guard<std::mutex> lk(g_trace_mu);
+  if (kernel_ms) *kernel_ms = g_last_ms;
+  if (steps) *steps = g_last_steps;
+  return PHX_OK;
+}
+
+phx_status phx_set_trace(int64_t capacity) {
+  std::lock_guard<std::mutex> lk(g_trace_mu);
+  g_trace_cap = capacity < 0 ? 0 : capacity;
+  g_trace.clear();
+  return PHX_OK;
+}
+
+phx_status phx_get_trace(double* out, int64_t capacity, int64_t* len) {
+  std::lock_guard<std::mutex> lk(g_trace_mu);
+  const int64_t used = std::min<int64_t>(g_trace_len, int64_t(g_trace.size()));
+  if (len) *len = used;
+  for (int64_t q = 0; q < used && q < capacity; ++q) out[q] = g_trace[size_t(q)];
+  return PHX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// Shared declarations between the host orchestration (phx_host.cpp) and the
+// sm_100a kernels (phx_kernels.cu).  No torch, no Eigen: plain device
+// pointers.
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace phx {
+
+constexpr int kChunk = 4096;       // stableNorm block (Eigen blocking)
+constexpr int kNormThreads = 256;  // canonical lane count of a chunk
+
+// Per-call parameters of the persistent phimv_block kernel.
+struct BlockArgs {
+  // operator (CSR, int32 indices)
+  int32_t n;
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* av;
+  // shape
+  int32_t p, r, w, fcols;
+  int32_t GS, QS;  // S-layout: lanes per row (pow2 <= 32), columns per lane
+  int32_t GF, QF;  // F-layout
+  int32_t QT;      // template width: pow2 >= max(QS, QF), in {1,2,4,8}
+  int32_t tile;    // rows per tile (row -> CTA mapping, independent of layout)
+  // scalars
+  double xi, tol;
+  int32_t s_eff;
+  int32_t single_variant;  // recovery op order of phi_single.cpp:106
+  double t_single;         // t (single variant only)
+  // per-column / per-abscissa coefficients (device)
+  const double* colKd;   // [w]   Kiter diagonal
+  const double* colKa;   // [w]   Kiter superdiagonal (0 for blocks 0,1)
+  const double* colTos;  // [w]   t_i / s
+  const double* t;       // [r]
+  const double* alpha;   // [r]
+  const double* mu;      // [r]
+  const double* g;       // [r]   mu_i / s
+  const double* jc;      // [r*(p+1)] Jexp chain c_d per abscissa
+  // buffers (row-interleaved blocks, row stride ldb / ldf doubles)
+  const double* V;  // n x (p+1) column-major, ld n
+  double* Vw;
+  double* D0;
+  double* D1;
+  double* S;
+  int32_t ldb;
+  double* F0;
+  double* F1;
+  double* E;
+  int32_t ldf;
+  double* W;    // n x r column-major, ld n
+  double* FLo;  // optional n x r exp_v0 (single variant), ld n
+  double* FRo;  // optional n x r tail, ld n
+  // control
+  unsigned long long* slots;  // [3][2] ring of per-step row-sum maxima
+  int32_t* status;            // [8]: code, index, L_S, sweeps done, steps
+  int32_t* lensF;             // [s_eff-1]
+  double* trace;              // optional (kind, a, b) triples
+  int32_t trace_cap;
+};
+
+// status codes written by the kernel
+enum : int32_t {
+  kStOk = 0,
+  kStSeriesCap = 1,
+  kStSeriesDiverged = 2,
+  kStRecoveryCap = 3,
+  kStRecoveryDiverged = 4,
+};
+
+// launch wrappers (phx_kernels.cu)
+cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st);
+cudaError_t coop_grid_size(int QT, int block, int* max_blocks);
+
+// y = f(A x) with mode 0: A x, 1: A x - fl(xi x), 2: (A x) / div ; fused
+// per-chunk max|y| into chunkmax (bit patterns) when chunkmax != nullptr
+cudaError_t launch_spmv(int32_t n, const int32_t* rp, const int32_t* ci, const double* av,
+                        const double* x, double* y, int mode, double xi, double div,
+                        unsigned long long* chunkmax, cudaStream_t st);
+// y = B c (B column-major n x ncol, ld n), canonical sequential order; fused
+// chunk max
+cudaError_t launch_gemv(int32_t n, int32_t ncol, const double* B, const double* c, double* y,
+                        unsigned long long* chunkmax, cudaStream_t st);
+cudaError_t launch_chunkmax(int32_t n, const double* x, unsigned long long* chunkmax,
+                            cudaStream_t st);
+// partial[b] = canonical sum over chunk b of fl(fl(x*inv[b])^2)
+cudaError_t launch_chunk_ssq(int32_t n, const double* x, const double* inv, double* partial,
+                             cudaStream_t st);
+// x = x * s (mode 0) or x / s (mode 1)
+cudaError_t launch_scale(int32_t n, double* x, double s, int mode, cudaStream_t st);
+// host col-major block (device copy, ld n) <-> nothing else needed; apply on
+// k columns: Y = A X (mode 0) or (A - xi I) X (mode 1), column-major, ld n
+cudaError_t launch_spmm_cols(int32_t n, int32_t k, const int32_t* rp, const int32_t* ci,
+                             const double* av, const double* X, double* Y, int mode, double xi,
+                             cudaStream_t st);
+
+int64_t kernel_launch_count();
+
+}  // namespace phx
