@@ -87,6 +87,9 @@ phx_status phx_op_create_csr(int64_t n, const int64_t* row_ptr, const int32_t* c
 phx_status phx_op_destroy(phx_op op);
 int64_t phx_op_dim(phx_op op);
 int64_t phx_op_nnz(phx_op op);
+/* The CUDA stream (cudaStream_t) every call on this operator runs on; lets a
+ * caller bracket calls with its own CUDA events. */
+void* phx_op_stream(phx_op op);
 
 /* Y = A*X (LinearOperator::apply, linop.cpp:10-24) and (A - xi I) X
  * (shifted_apply, linop.cpp:40-49) on host column-major blocks of k columns

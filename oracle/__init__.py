@@ -78,6 +78,9 @@ def lib():
         L.orc_phimv_block.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int64, dp, dp, C.c_int32, dp,
                                       C.c_int64, C.c_double, C.POINTER(ScalingShiftC), dp,
                                       C.c_int64, i64p, i32p, C.c_int64, dp, C.c_int64, i64p]
+        L.orc_phimv_block_prefix.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int64, dp, dp,
+                                             C.c_int32, dp, C.c_int64, C.c_double,
+                                             C.POINTER(ScalingShiftC), C.c_int32, i32p]
         L.orc_phimv.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, C.c_double, C.c_int32, dp,
                                 C.c_int64, C.c_double, C.POINTER(ScalingShiftC), dp, dp, dp, i64p,
                                 i32p, C.c_int64]
@@ -315,6 +318,19 @@ def phimv_block(op: Csr, t, alpha, V, tol, params: ScalingShift, trace=False, le
                                  tol, C.byref(pc), _d(W), op.n, rec4.ctypes.data_as(i64p),
                                  lens.ctypes.data_as(i32p), lens_cap, None, 0, None))
     return W, _rec(rec4, lens)
+
+
+def phimv_block_prefix(op: Csr, t, alpha, V, tol, params: ScalingShift, max_s_terms: int):
+    """Timing sample: the evaluation stopped after max_s_terms S terms."""
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+    V = np.asfortranarray(np.asarray(V, dtype=np.float64).reshape(op.n, -1))
+    done = C.c_int32()
+    pc = params.c()
+    _check(lib().orc_phimv_block_prefix(*op.args(), t.size, _d(t), _d(alpha), V.shape[1] - 1,
+                                        _d(V), op.n, tol, C.byref(pc), int(max_s_terms),
+                                        C.byref(done)))
+    return done.value
 
 
 def phimv(op: Csr, t, alpha, V, tol, params: ScalingShift, lens_cap=1 << 16):

@@ -563,7 +563,8 @@ struct BlockResult {
 };
 
 static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, const Mat& V,
-                               double req_tol, const ScalingShift& params, Trace tr) {
+                               double req_tol, const ScalingShift& params, Trace tr,
+                               int max_s_terms = 0) {
   // check_request (phi_block.cpp:15-27)
   if (t.empty()) throw std::invalid_argument("phimv_block: at least one abscissa required");
   if (alpha.size() != t.size()) throw std::invalid_argument("phimv_block: t and alpha lengths differ");
@@ -626,6 +627,13 @@ static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, con
   tr.add(0, c2, nS);
   Mat Vn(n, w);
   while (c1 + c2 > tol * nS) {  // :93
+    if (max_s_terms > 0 && k - 1 >= max_s_terms) {
+      // timing sample only (bench.py reference arm): stop after a prefix
+      rec.series_len_S = k;
+      BlockResult early;
+      early.rec = std::move(rec);
+      return early;
+    }
     if (k >= kSeriesCap) no_convergence("phimv_block", "series", kSeriesCap);
     ++k;
     c1 = c2;
@@ -1175,6 +1183,23 @@ int orc_phimv_block(int64_t n, const int64_t* rp, const int32_t* ci, const doubl
       *trace_len = int64_t(tr.size());
       for (int64_t q = 0; q < int64_t(tr.size()) && q < trace_cap; ++q) trace[q] = tr[size_t(q)];
     }
+  });
+}
+
+// Timing sample for the CPU reference arm: the same evaluation, stopped after
+// max_s_terms S-series terms (no promotion/recovery).  Returns the terms done.
+int orc_phimv_block_prefix(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                           int64_t r, const double* t, const double* alpha, int32_t p,
+                           const double* V, int64_t ldv, double tol,
+                           const orc_scaling_shift* params, int32_t max_s_terms,
+                           int32_t* terms_done) {
+  return guarded([&] {
+    orc::Vec tv(t, t + r), av(alpha, alpha + r);
+    orc::Mat Vm = wrap(V, n, p + 1, ldv);
+    orc::Trace trc;
+    orc::BlockResult res =
+        orc::phimv_block(make_op(n, rp, ci, v), tv, av, Vm, tol, *params, trc, max_s_terms);
+    *terms_done = res.rec.series_len_S - 1;
   });
 }
 

@@ -69,7 +69,7 @@ _WL = None
 
 # every exported symbol of include/phx.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = (
-    "phx_op_create_csr", "phx_op_destroy", "phx_op_dim", "phx_op_nnz", "phx_apply",
+    "phx_op_create_csr", "phx_op_destroy", "phx_op_dim", "phx_op_nnz", "phx_op_stream", "phx_apply",
     "phx_shifted_apply", "phx_select_parameters", "phx_basis_build", "phx_basis_destroy",
     "phx_basis_info", "phx_objective", "phx_minimize_shift", "phx_parameters_for_shift",
     "phx_phimv_block", "phx_phimv_block_device", "phx_phimv", "phx_last_error",
@@ -100,6 +100,8 @@ def lib():
     L.phx_op_nnz.argtypes = [C.c_void_p]
     L.phx_op_create_csr.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int32, C.POINTER(C.c_void_p)]
     L.phx_op_destroy.argtypes = [C.c_void_p]
+    L.phx_op_stream.restype = C.c_void_p
+    L.phx_op_stream.argtypes = [C.c_void_p]
     L.phx_apply.argtypes = [C.c_void_p, dp, C.c_int64, C.c_int64, dp, C.c_int64]
     L.phx_shifted_apply.argtypes = [C.c_void_p, C.c_double, dp, C.c_int64, C.c_int64, dp, C.c_int64]
     L.phx_select_parameters.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_double,
@@ -238,6 +240,10 @@ class CsrOperator:
 
     def dim(self):
         return self.n
+
+    def stream_ptr(self) -> int:
+        """cudaStream_t of this operator (for torch.cuda.ExternalStream)."""
+        return int(lib().phx_op_stream(self._h) or 0)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -842,6 +842,7 @@ phx_status phx_op_destroy(phx_op op) {
 
 int64_t phx_op_dim(phx_op op) { return op ? op->n : 0; }
 int64_t phx_op_nnz(phx_op op) { return op ? op->nnz : 0; }
+void* phx_op_stream(phx_op op) { return op ? static_cast<void*>(op->stream) : nullptr; }
 
 static phx_status apply_impl(phx_op op, int mode, double xi, const double* X, int64_t ldx,
                              int64_t k, double* Y, int64_t ldy) {
