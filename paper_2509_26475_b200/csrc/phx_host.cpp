@@ -605,7 +605,9 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   if (QT > 8)
     throw_phx(PHX_EINVAL, std::string(who) + ": block width (p+1)*r above 256 is not supported");
   const int block = 256;
-  const int32_t tile = block / std::min(GS, GF);
+  // rows per CTA tile: 8 warps x the larger warp tile (kernel: (32/G) * R rows,
+  // R = 2 rows per lane group when QT == 1)
+  const int32_t tile = 8 * (32 / std::min(GS, GF)) * (QT == 1 ? 2 : 1);
 
   // workspace
   const int32_t ldb = w, ldf = fcols;

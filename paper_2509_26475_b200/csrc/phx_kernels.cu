@@ -93,104 +93,136 @@ __device__ __forceinline__ void publish2(unsigned long long a, unsigned long lon
   __syncthreads();
 }
 
-// Gather-accumulate for one row: acc[q] = sum_e av[e] * X[ci[e]*ld + c_q]
-// in CSR storage order, sequentially from +0 (the oracle's ApplyFn order).
-// The row's (col, val) pairs are loaded cooperatively by the group (one
-// coalesced load) and broadcast by shuffle; the loop trip count is made
-// warp-uniform so the shuffles are convergent.
-template <int Q, int B>
-__device__ __forceinline__ void gather_row(const int32_t* __restrict__ ci,
-                                           const double* __restrict__ av, int e0, int cnt,
-                                           const double* X, int ld, const int (&cq)[Q],
-                                           const bool (&vq)[Q], int G, int lg,
-                                           double (&acc)[Q]) {
-  int wmax = cnt;
-  for (int m = 16; m >= 1; m >>= 1) wmax = max(wmax, __shfl_xor_sync(kFull, wmax, m));
-  for (int base = 0; base < wmax; base += G) {
-    const int idx = base + lg;
-    int mycol = 0;
-    double mya = 0.0;
-    if (idx < cnt) {
-      mycol = __ldg(ci + e0 + idx);
-      mya = __ldg(av + e0 + idx);
+// ---------------------------------------------------------------------------
+// Warp tiles.  A warp processes RW = (32/G)*R consecutive rows at a time:
+// lane group g = lane/G (G lanes per row, Q columns per lane), R rows per
+// group (row = base + rr*(32/G) + g, so for each rr the warp's groups cover
+// consecutive rows and every block-row load is one contiguous segment).  The
+// warp tile's CSR slice is staged once in warp-private shared memory with
+// coalesced loads (row_ptr, then the contiguous entry range); tiles whose
+// slice exceeds the staging capacity read the entries from global memory.
+// ---------------------------------------------------------------------------
+constexpr int kWarps = kBlock / 32;
+constexpr int kWCap = 256;   // staged CSR entries per warp
+constexpr int kMaxRW = 64;   // rows per warp tile
+
+struct WarpStage {
+  int rp[kMaxRW + 1];
+  int ci[kWCap];
+  double av[kWCap];
+};
+
+struct TileCsr {
+  const int* ci;
+  const double* av;
+  int e_lo;
+};
+
+// Stage the CSR slice of rows [base, base+RW) (rows past n are empty).
+__device__ __forceinline__ TileCsr stage_csr(const BlockArgs& a, int base, int RW,
+                                             WarpStage& st, int lane) {
+  __syncwarp();  // every lane is done with the previous tile's slice
+  for (int l = lane; l <= RW; l += 32) st.rp[l] = __ldg(a.rp + min(base + l, a.n));
+  __syncwarp();
+  TileCsr tc;
+  tc.e_lo = st.rp[0];
+  const int E = st.rp[RW] - tc.e_lo;
+  if (E <= kWCap) {
+    for (int e = lane; e < E; e += 32) {
+      st.ci[e] = __ldg(a.ci + tc.e_lo + e);
+      st.av[e] = __ldg(a.av + tc.e_lo + e);
     }
-    const int lim = min(G, wmax - base);
-    for (int u0 = 0; u0 < lim; u0 += B) {
-      double xv[B][Q];
-      double aa[B];
-      bool ok[B];
+    tc.ci = st.ci;
+    tc.av = st.av;
+  } else {
+    tc.ci = a.ci + tc.e_lo;
+    tc.av = a.av + tc.e_lo;
+  }
+  __syncwarp();
+  return tc;
+}
+
+// acc[rr][q] = sum over row rr's entries, in storage order from +0, of
+// av[e] * X[ci[e]*ld + c_q].  Gathers are plain (L1-cached) loads: X was
+// written before the last grid.sync(), which invalidates L1 (CCTL.IVALL).
+template <int Q, int R, int B>
+__device__ __forceinline__ void gather_tile(const TileCsr& tc, const int (&rs)[R],
+                                            const int (&cnt)[R], const double* X, int ld,
+                                            const int (&cq)[Q], const bool (&vq)[Q],
+                                            double (&acc)[R][Q]) {
+  int maxc = 0;
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int src = u0 + u;
-        const int col = __shfl_sync(kFull, mycol, src & (G - 1), G);
-        aa[u] = __shfl_sync(kFull, mya, src & (G - 1), G);
-        ok[u] = (src < lim) && (base + src < cnt);
+  for (int rr = 0; rr < R; ++rr) maxc = max(maxc, cnt[rr]);
+  for (int u0 = 0; u0 < maxc; u0 += B) {
+    double xv[B][R][Q];
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const bool ok = u0 + u < cnt[rr];
+        const int col = ok ? tc.ci[rs[rr] + u0 + u] : 0;
 #pragma unroll
         for (int q = 0; q < Q; ++q)
-          xv[u][q] = (ok[u] && vq[q]) ? ldcg(X + size_t(col) * size_t(ld) + cq[q]) : 0.0;
+          xv[u][rr][q] = (ok && vq[q]) ? X[size_t(col) * size_t(ld) + cq[q]] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < B; ++u)
-        if (ok[u]) {
+    for (int u = 0; u < B; ++u)
 #pragma unroll
-          for (int q = 0; q < Q; ++q) acc[q] = acc[q] + aa[u] * xv[u][q];
+      for (int rr = 0; rr < R; ++rr)
+        if (u0 + u < cnt[rr]) {
+          const double av = tc.av[rs[rr] + u0 + u];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[rr][q] = acc[rr][q] + av * xv[u][rr][q];
         }
-    }
   }
 }
 
 template <int Q>
-struct Batch {
-  static constexpr int value = Q == 1 ? 8 : (Q == 2 ? 4 : 2);
+struct Tr {  // rows per group per warp tile, gather batch
+  static constexpr int R = Q == 1 ? 2 : 1;
+  static constexpr int B = Q == 1 ? 4 : (Q == 2 ? 4 : 2);
 };
+
+struct Layout {
+  int G, gpw, g, lg, RW, qn, qp, width;
+};
+
+__device__ __forceinline__ Layout make_layout(int G, int qn, int width, int R) {
+  Layout L;
+  const int lane = threadIdx.x & 31;
+  L.G = G;
+  L.gpw = 32 / G;
+  L.g = lane / G;
+  L.lg = lane % G;
+  L.RW = L.gpw * R;
+  L.qn = qn;
+  L.width = width;
+  // power-of-two count of 32-column chunks (1 when the row fits in G lanes)
+  int chunks = (width + 31) / 32;
+  int qp = 1;
+  while (qp < chunks) qp <<= 1;
+  L.qp = width > 32 ? qp : 1;
+  return L;
+}
 
 // Persistent evaluator.  See the file header.
 template <int Q>
-__global__ void __launch_bounds__(kBlock) k_phimv_block(BlockArgs a) {
+__global__ void __launch_bounds__(kBlock, 3) k_phimv_block(BlockArgs a) {
+  constexpr int R = Tr<Q>::R;
+  constexpr int B = Tr<Q>::B;
   cg::grid_group grid = cg::this_grid();
-  __shared__ unsigned long long red[2][kBlock / 32];
-  constexpr int B = Batch<Q>::value;
+  __shared__ unsigned long long red[2][kWarps];
+  __shared__ WarpStage stage[kWarps];
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpStage& st = stage[warp];
 
-  const int ntiles = (a.n + a.tile - 1) / a.tile;
+  const int n = a.n, r = a.r, p = a.p, ldb = a.ldb, ldf = a.ldf;
+  const int ntiles = (n + a.tile - 1) / a.tile;
   const bool has_xi = a.xi != 0.0;
   const bool master = blockIdx.x == 0 && threadIdx.x == 0;
-
-  // ---- S layout constants (row-invariant per lane) ----
-  const int GS = a.GS, gpcS = blockDim.x / GS, gidS = threadIdx.x / GS, lgS = threadIdx.x % GS;
-  int cS[Q], jS[Q], iS[Q];
-  bool vS[Q];
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    cS[q] = lgS + GS * q;
-    vS[q] = (q < a.QS) && (cS[q] < a.w);
-    jS[q] = vS[q] ? cS[q] / a.r : 0;
-    iS[q] = vS[q] ? cS[q] % a.r : 0;
-  }
-  const int qpS = a.w > 32 ? ((a.w + 31) / 32 <= 1 ? 1 : (1 << (32 - __clz((a.w + 31) / 32 - 1)))) : 1;
-  // ---- F layout constants ----
-  const int GF = a.GF, gpcF = blockDim.x / GF, gidF = threadIdx.x / GF, lgF = threadIdx.x % GF;
-  int cF[Q], iF[Q];
-  bool vF[Q];
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    cF[q] = lgF + GF * q;
-    vF[q] = (q < a.QF) && (cF[q] < a.fcols);
-    iF[q] = vF[q] ? (cF[q] < a.r ? cF[q] : cF[q] - a.r) : 0;
-  }
-  const int qpF =
-      a.fcols > 32 ? ((a.fcols + 31) / 32 <= 1 ? 1 : (1 << (32 - __clz((a.fcols + 31) / 32 - 1)))) : 1;
-
-  double kd[Q], ka[Q], tos[Q];
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    kd[q] = vS[q] ? __ldg(a.colKd + cS[q]) : 0.0;
-    ka[q] = vS[q] ? __ldg(a.colKa + cS[q]) : 0.0;
-    tos[q] = vS[q] ? __ldg(a.colTos + cS[q]) : 0.0;
-  }
-  double tosF[Q];
-#pragma unroll
-  for (int q = 0; q < Q; ++q) tosF[q] = vF[q] ? __ldg(a.colTos + iF[q]) : 0.0;
+  const Layout LS = make_layout(a.GS, a.QS, a.w, R);
+  const Layout LF = make_layout(a.GF, a.QF, a.fcols, R);
 
   int step = 0;
   int tr_len = 0;
@@ -203,7 +235,7 @@ __global__ void __launch_bounds__(kBlock) k_phimv_block(BlockArgs a) {
     tr_len += 3;
   };
   // publish this CTA's maxima for the current step, zero the slot of the next
-  // step (safe: its last readers finished before the previous grid sync),
+  // step (its last readers finished before the previous grid sync),
   // grid-sync, read the global maxima.
   auto sync_step = [&](unsigned long long ma, unsigned long long mb, double& ra, double& rb) {
     unsigned long long* slot = a.slots + 2 * (step % 3);
@@ -218,190 +250,239 @@ __global__ void __launch_bounds__(kBlock) k_phimv_block(BlockArgs a) {
     rb = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot + 1)));
     ++step;
   };
+  auto finish = [&](int err, int idx, int L_S, int extra_steps) {
+    if (master) {
+      a.status[0] = err;
+      a.status[1] = idx;
+      a.status[2] = L_S;
+      a.status[3] = 0;
+      a.status[4] = step + extra_steps;
+      a.status[5] = min(tr_len, a.trace_cap);
+    }
+  };
 
-  const int ldb = a.ldb, ldf = a.ldf, n = a.n, r = a.r, p = a.p;
+  // per-lane column bookkeeping of a layout (recomputed per phase)
+  auto cols = [&](const Layout& L, int (&c)[Q], bool (&v)[Q]) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      c[q] = L.lg + L.G * q;
+      v[q] = (q < L.qn) && (c[q] < L.width);
+    }
+  };
 
   // ================= init: Vw = V[src]*g, D = S = Vw (phi_block.cpp:76-92)
+  unsigned long long m0 = 0;
   {
-    unsigned long long m0 = 0;
+    int c[Q];
+    bool v[Q];
+    cols(LS, c, v);
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
-      for (int ro = gidS; ro < a.tile; ro += gpcS) {
-        const int row = t * a.tile + ro;
-        const bool rv = row < n;
-        double v[Q];
+      for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+        const int base = t * a.tile + wt * LS.RW;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          v[q] = 0.0;
-          if (rv && vS[q]) {
-            const int src = jS[q] == 0 ? 0 : p + 1 - jS[q];
-            v[q] = __ldg(a.V + size_t(src) * size_t(n) + row) * __ldg(a.g + iS[q]);
-            const size_t o = size_t(row) * size_t(ldb) + cS[q];
-            a.Vw[o] = v[q];
-            a.D0[o] = v[q];
-            a.S[o] = v[q];
-          }
-        }
-        double av_[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) av_[q] = fabs(v[q]);
-        const double rs = group_rowsum<Q>(av_, GS, qpS);
-        if (rv) m0 = umax64(m0, abs_bits(rs));
-      }
-    double mD, mSn;
-    sync_step(m0, m0, mD, mSn);
-    // c2 = inf_norm(D), ||S|| at k = 1
-    double c1 = INF, c2 = mD, nS = mSn;
-    trace(0.0, c2, nS);
-
-    // ================= S series (phi_block.cpp:93-106)
-    int k = 1;
-    double sigma = 1.0;
-    double* Dc = a.D0;
-    double* Dn = a.D1;
-    int err = kStOk, err_idx = 0;
-    while (c1 + c2 > a.tol * nS) {
-      if (k >= 500) {
-        err = kStSeriesCap;
-        err_idx = 500;
-        break;
-      }
-      ++k;
-      c1 = c2;
-      sigma *= k;
-      unsigned long long mdb = 0, msb = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
-        for (int ro = gidS; ro < a.tile; ro += gpcS) {
-          const int row = t * a.tile + ro;
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = base + rr * LS.gpw + LS.g;
           const bool rv = row < n;
-          int e0 = 0, cnt = 0;
-          if (rv) {
-            e0 = __ldg(a.rp + row);
-            cnt = __ldg(a.rp + row + 1) - e0;
-          }
-          bool vq[Q];
-          double vw[Q], vwl[Q], so[Q], ds[Q], acc[Q];
+          double x[Q];
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
-            vq[q] = rv && vS[q];
-            const size_t o = size_t(row) * size_t(ldb) + cS[q];
-            vw[q] = vq[q] ? ldcg(a.Vw + o) : 0.0;
-            vwl[q] = (vq[q] && jS[q] >= 2) ? ldcg(a.Vw + o - r) : 0.0;
-            so[q] = vq[q] ? ldcg(a.S + o) : 0.0;
-            ds[q] = (vq[q] && has_xi) ? ldcg(Dc + o) : 0.0;
-            acc[q] = 0.0;
+            x[q] = 0.0;
+            if (rv && v[q]) {
+              const int j = c[q] / r, i = c[q] - j * r;
+              const int src = j == 0 ? 0 : p + 1 - j;
+              x[q] = __ldg(a.V + size_t(src) * size_t(n) + row) * __ldg(a.g + i);
+              const size_t o = size_t(row) * size_t(ldb) + c[q];
+              a.Vw[o] = x[q];
+              a.D0[o] = x[q];
+              a.S[o] = x[q];
+            }
+            x[q] = fabs(x[q]);
           }
-          gather_row<Q, B>(a.ci, a.av, e0, cnt, Dc, ldb, cS, vq, GS, lgS, acc);
-          double vn[Q], dn[Q], sn[Q];
+          const double rsum = group_rowsum<Q>(x, LS.G, LS.qp);
+          if (rv) m0 = umax64(m0, abs_bits(rsum));
+        }
+      }
+  }
+  double mD, mSn;
+  sync_step(m0, m0, mD, mSn);
+  double c1 = INF, c2 = mD, nS = mSn;  // c2 = inf_norm(D), ||S|| at k = 1
+  trace(0.0, c2, nS);
+
+  // ================= S series (phi_block.cpp:93-106)
+  int k = 1;
+  double sigma = 1.0;
+  double* Dc = a.D0;
+  double* Dn = a.D1;
+  int err = kStOk, err_idx = 0;
+  while (c1 + c2 > a.tol * nS) {
+    if (k >= 500) {
+      err = kStSeriesCap;
+      err_idx = 500;
+      break;
+    }
+    ++k;
+    c1 = c2;
+    sigma *= k;
+    unsigned long long mdb = 0, msb = 0;
+    {
+      int c[Q], jj[Q];
+      bool v[Q];
+      double kd[Q], ka[Q], tos[Q];
+      cols(LS, c, v);
 #pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            // Vw = Vw * Kiter: ascending source column from +0 (:98)
-            double g2 = 0.0;
-            if (jS[q] >= 2) g2 = g2 + vwl[q] * ka[q];
-            g2 = g2 + vw[q] * kd[q];
-            vn[q] = g2;
-            // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
-            double y = acc[q];
-            if (has_xi) y = y - a.xi * ds[q];
-            y = y * tos[q];
-            dn[q] = y + vn[q];
-            sn[q] = so[q] + dn[q] / sigma;  // S += D/sigma (:105)
+      for (int q = 0; q < Q; ++q) {
+        jj[q] = v[q] ? c[q] / r : 0;
+        kd[q] = v[q] ? __ldg(a.colKd + c[q]) : 0.0;
+        ka[q] = v[q] ? __ldg(a.colKa + c[q]) : 0.0;
+        tos[q] = v[q] ? __ldg(a.colTos + c[q]) : 0.0;
+      }
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+          const int base = t * a.tile + wt * LS.RW;
+          // row-local streams first (independent of the CSR slice)
+          double vw[R][Q], vwl[R][Q], so[R][Q], ds[R][Q], acc[R][Q];
+          bool vq[R][Q];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              vq[rr][q] = row < n && v[q];
+              const size_t o = size_t(row) * size_t(ldb) + c[q];
+              vw[rr][q] = vq[rr][q] ? a.Vw[o] : 0.0;
+              vwl[rr][q] = (vq[rr][q] && jj[q] >= 2) ? a.Vw[o - r] : 0.0;
+              so[rr][q] = vq[rr][q] ? a.S[o] : 0.0;
+              ds[rr][q] = (vq[rr][q] && has_xi) ? Dc[o] : 0.0;
+              acc[rr][q] = 0.0;
+            }
           }
+          const TileCsr tc = stage_csr(a, base, LS.RW, st, lane);
+          int rs[R], cnt[R];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int li = rr * LS.gpw + LS.g;
+            rs[rr] = st.rp[li] - tc.e_lo;
+            cnt[rr] = st.rp[li + 1] - st.rp[li];
+          }
+          gather_tile<Q, R, B>(tc, rs, cnt, Dc, ldb, c, v, acc);
+          double vn[R][Q], dn[R][Q], sn[R][Q];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              // Vw = Vw * Kiter: ascending source column from +0 (:98)
+              double g2 = 0.0;
+              if (jj[q] >= 2) g2 = g2 + vwl[rr][q] * ka[q];
+              g2 = g2 + vw[rr][q] * kd[q];
+              vn[rr][q] = g2;
+              // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
+              double y = acc[rr][q];
+              if (has_xi) y = y - a.xi * ds[rr][q];
+              y = y * tos[q];
+              dn[rr][q] = y + g2;
+              sn[rr][q] = so[rr][q] + dn[rr][q] / sigma;  // S += D/sigma (:105)
+            }
           __syncwarp();
 #pragma unroll
-          for (int q = 0; q < Q; ++q)
-            if (vq[q]) {
-              const size_t o = size_t(row) * size_t(ldb) + cS[q];
-              a.Vw[o] = vn[q];
-              Dn[o] = dn[q];
-              a.S[o] = sn[q];
-            }
-          double ad[Q], as[Q];
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
+            double ad[Q], as[Q];
 #pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            ad[q] = vq[q] ? fabs(dn[q]) : 0.0;
-            as[q] = vq[q] ? fabs(sn[q]) : 0.0;
-          }
-          const double rd = group_rowsum<Q>(ad, GS, qpS);
-          const double rs = group_rowsum<Q>(as, GS, qpS);
-          if (rv) {
-            mdb = umax64(mdb, abs_bits(rd));
-            msb = umax64(msb, abs_bits(rs));
+            for (int q = 0; q < Q; ++q) {
+              if (vq[rr][q]) {
+                const size_t o = size_t(row) * size_t(ldb) + c[q];
+                a.Vw[o] = vn[rr][q];
+                Dn[o] = dn[rr][q];
+                a.S[o] = sn[rr][q];
+              }
+              ad[q] = vq[rr][q] ? fabs(dn[rr][q]) : 0.0;
+              as[q] = vq[rr][q] ? fabs(sn[rr][q]) : 0.0;
+            }
+            const double rd = group_rowsum<Q>(ad, LS.G, LS.qp);
+            const double rsm = group_rowsum<Q>(as, LS.G, LS.qp);
+            if (row < n) {
+              mdb = umax64(mdb, abs_bits(rd));
+              msb = umax64(msb, abs_bits(rsm));
+            }
           }
         }
-      double maxD, maxS;
-      sync_step(mdb, msb, maxD, maxS);
-      c2 = maxD / sigma;  // :103
-      if (!isfinite(c2)) {
-        err = kStSeriesDiverged;
-        err_idx = k;
-        break;
-      }
-      nS = maxS;
-      trace(1.0, c2, nS);
-      double* tmp = Dc;
-      Dc = Dn;
-      Dn = tmp;
     }
-    const int L_S = k;
-    if (err != kStOk) {
-      if (master) {
-        a.status[0] = err;
-        a.status[1] = err_idx;
-        a.status[2] = L_S;
-        a.status[3] = 0;
-        a.status[4] = step;
-        a.status[5] = min(tr_len, a.trace_cap);
-      }
-      return;
+    double maxD, maxS;
+    sync_step(mdb, msb, maxD, maxS);
+    c2 = maxD / sigma;  // :103
+    if (!isfinite(c2)) {
+      err = kStSeriesDiverged;
+      err_idx = k;
+      break;
     }
+    nS = maxS;
+    trace(1.0, c2, nS);
+    double* tmp = Dc;
+    Dc = Dn;
+    Dn = tmp;
+  }
+  const int L_S = k;
+  if (err != kStOk) {
+    finish(err, err_idx, L_S, 0);
+    return;
+  }
 
-    // ================= promotion (phi_block.cpp:109-120)
-    // F_L = fl(fl(A S_L * t_i) + v0) (unshifted A), F_R = S block p.
-    double* Fc = a.F0;
-    double* Fn = a.F1;
-    const bool sweeps = a.s_eff > 1;
-    {
-      unsigned long long mf = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
-        for (int ro = gidF; ro < a.tile; ro += gpcF) {
-          const int row = t * a.tile + ro;
-          const bool rv = row < n;
-          int e0 = 0, cnt = 0;
-          if (rv) {
-            e0 = __ldg(a.rp + row);
-            cnt = __ldg(a.rp + row + 1) - e0;
-          }
-          bool vl[Q];
-          double acc[Q];
-          int cl[Q];
+  // ================= promotion (phi_block.cpp:109-120)
+  // F_L = fl(fl(A S_L * t_i) + v0) (unshifted A), F_R = S block p.
+  double* Fc = a.F0;
+  double* Fn = a.F1;
+  const bool sweeps = a.s_eff > 1;
+  unsigned long long mf = 0;
+  {
+    int c[Q];
+    bool v[Q], vl[Q];
+    cols(LF, c, v);
 #pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            vl[q] = rv && vF[q] && cF[q] < r;
-            cl[q] = cF[q];
-            acc[q] = 0.0;
-          }
-          gather_row<Q, B>(a.ci, a.av, e0, cnt, a.S, ldb, cl, vl, GF, lgF, acc);
+    for (int q = 0; q < Q; ++q) vl[q] = v[q] && c[q] < r;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
+        const int base = t * a.tile + wt * LF.RW;
+        double acc[R][Q];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[rr][q] = 0.0;
+        const TileCsr tc = stage_csr(a, base, LF.RW, st, lane);
+        int rs[R], cnt[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int li = rr * LF.gpw + LF.g;
+          rs[rr] = st.rp[li] - tc.e_lo;
+          cnt[rr] = st.rp[li + 1] - st.rp[li];
+        }
+        gather_tile<Q, R, B>(tc, rs, cnt, a.S, ldb, c, vl, acc);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = base + rr * LF.gpw + LF.g;
+          const bool rv = row < n;
           double f[Q];
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
             f[q] = 0.0;
-            if (rv && vF[q]) {
-              if (cF[q] < r) {
-                const double sc = acc[q] * __ldg(a.t + iF[q]);
+            if (rv && v[q]) {
+              const int i = c[q] < r ? c[q] : c[q] - r;
+              const size_t srow = size_t(row) * size_t(ldb) + size_t(p) * size_t(r);
+              if (c[q] < r) {
+                const double sc = acc[rr][q] * __ldg(a.t + i);
                 f[q] = sc + __ldg(a.V + row);
               } else {
-                f[q] = ldcg(a.S + size_t(row) * size_t(ldb) + size_t(p) * size_t(r) + iF[q]);
+                f[q] = a.S[srow + i];
               }
-              const size_t o = size_t(row) * size_t(ldf) + cF[q];
-              Fc[o] = f[q];
-              if (sweeps) a.E[o] = f[q];
-              if (!sweeps && cF[q] < r) {
+              const size_t o = size_t(row) * size_t(ldf) + c[q];
+              if (sweeps) {
+                Fc[o] = f[q];
+                a.E[o] = f[q];
+              } else if (c[q] < r) {
                 // assembly W = F_L + fl(F_R * alpha) (:148-154)
-                const int i = cF[q];
                 double wv = f[q];
                 double fr = 0.0;
                 if (p > 0) {
-                  fr = ldcg(a.S + size_t(row) * size_t(ldb) + size_t(p) * size_t(r) + i);
+                  fr = a.S[srow + i];
                   wv = wv + fr * __ldg(a.alpha + i);
                 }
                 a.W[size_t(i) * size_t(n) + row] = wv;
@@ -409,166 +490,189 @@ __global__ void __launch_bounds__(kBlock) k_phimv_block(BlockArgs a) {
                 if (a.FRo) a.FRo[size_t(i) * size_t(n) + row] = fr;
               }
             }
+            f[q] = fabs(f[q]);
           }
           if (sweeps) {
-            double af[Q];
-#pragma unroll
-            for (int q = 0; q < Q; ++q) af[q] = (rv && vF[q]) ? fabs(f[q]) : 0.0;
-            const double rf = group_rowsum<Q>(af, GF, qpF);
+            const double rf = group_rowsum<Q>(f, LF.G, LF.qp);
             if (rv) mf = umax64(mf, abs_bits(rf));
           }
         }
-      if (!sweeps) {
-        if (master) {
-          a.status[0] = kStOk;
-          a.status[1] = 0;
-          a.status[2] = L_S;
-          a.status[3] = 0;
-          a.status[4] = step + 1;
-          a.status[5] = min(tr_len, a.trace_cap);
-        }
-        return;
       }
-      double maxF, dummy;
-      sync_step(mf, mf, maxF, dummy);
+  }
+  if (!sweeps) {
+    finish(kStOk, 0, L_S, 1);
+    return;
+  }
+  double fnorm, dummy;
+  sync_step(mf, mf, fnorm, dummy);
 
-      // ================= recovery sweeps (phi_block.cpp:122-146)
-      double fnorm = maxF;
-      for (int sweep = 1; sweep < a.s_eff; ++sweep) {
-        int kk = 0;
-        double d1 = INF, d2 = fnorm, nE = fnorm;  // E = F
-        trace(2.0, d2, nE);
-        while (d1 + d2 > a.tol * nE) {
-          if (kk >= 300) {
-            err = kStRecoveryCap;
-            err_idx = 300;
-            break;
-          }
-          ++kk;
-          d1 = d2;
-          const double fac = a.single_variant ? a.t_single / (double(a.s_eff) * kk) : 0.0;
-          unsigned long long mfb = 0, meb = 0;
-          for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
-            for (int ro = gidF; ro < a.tile; ro += gpcF) {
-              const int row = t * a.tile + ro;
-              const bool rv = row < n;
-              int e0 = 0, cnt = 0;
-              if (rv) {
-                e0 = __ldg(a.rp + row);
-                cnt = __ldg(a.rp + row + 1) - e0;
-              }
-              bool vq[Q];
-              double eo[Q], fs[Q], acc[Q];
+  // ================= recovery sweeps (phi_block.cpp:122-146)
+  for (int sweep = 1; sweep < a.s_eff; ++sweep) {
+    int kk = 0;
+    double d1 = INF, d2 = fnorm, nE = fnorm;  // E = F
+    trace(2.0, d2, nE);
+    while (d1 + d2 > a.tol * nE) {
+      if (kk >= 300) {
+        err = kStRecoveryCap;
+        err_idx = 300;
+        break;
+      }
+      ++kk;
+      d1 = d2;
+      const double fac = a.single_variant ? a.t_single / (double(a.s_eff) * kk) : 0.0;
+      unsigned long long mfb = 0, meb = 0;
+      {
+        int c[Q];
+        bool v[Q];
+        double tosF[Q];
+        cols(LF, c, v);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int i = c[q] < r ? c[q] : c[q] - r;
+          tosF[q] = v[q] ? __ldg(a.colTos + i) : 0.0;
+        }
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+          for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
+            const int base = t * a.tile + wt * LF.RW;
+            double eo[R][Q], fs[R][Q], acc[R][Q];
+            bool vq[R][Q];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              const int row = base + rr * LF.gpw + LF.g;
 #pragma unroll
               for (int q = 0; q < Q; ++q) {
-                vq[q] = rv && vF[q];
-                const size_t o = size_t(row) * size_t(ldf) + cF[q];
-                eo[q] = vq[q] ? ldcg(a.E + o) : 0.0;
-                fs[q] = (vq[q] && has_xi) ? ldcg(Fc + o) : 0.0;
-                acc[q] = 0.0;
+                vq[rr][q] = row < n && v[q];
+                const size_t o = size_t(row) * size_t(ldf) + c[q];
+                eo[rr][q] = vq[rr][q] ? a.E[o] : 0.0;
+                fs[rr][q] = (vq[rr][q] && has_xi) ? Fc[o] : 0.0;
+                acc[rr][q] = 0.0;
               }
-              gather_row<Q, B>(a.ci, a.av, e0, cnt, Fc, ldf, cF, vq, GF, lgF, acc);
-              double y[Q], en[Q];
+            }
+            const TileCsr tc = stage_csr(a, base, LF.RW, st, lane);
+            int rs[R], cnt[R];
 #pragma unroll
-              for (int q = 0; q < Q; ++q) {
-                double v = acc[q];
-                if (has_xi) v = v - a.xi * fs[q];
-                if (a.single_variant) {
-                  v = fac * v;  // phi_single.cpp:106
-                } else {
-                  v = v / double(kk);  // phi_block.cpp:132
-                  v = v * tosF[q];     // :134-135
-                }
-                y[q] = v;
-                en[q] = eo[q] + v;  // E += F (:138)
-                if (vq[q]) {
-                  const size_t o = size_t(row) * size_t(ldf) + cF[q];
-                  Fn[o] = y[q];
-                  a.E[o] = en[q];
-                }
-              }
+            for (int rr = 0; rr < R; ++rr) {
+              const int li = rr * LF.gpw + LF.g;
+              rs[rr] = st.rp[li] - tc.e_lo;
+              cnt[rr] = st.rp[li + 1] - st.rp[li];
+            }
+            gather_tile<Q, R, B>(tc, rs, cnt, Fc, ldf, c, v, acc);
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              const int row = base + rr * LF.gpw + LF.g;
               double ay[Q], ae[Q];
 #pragma unroll
               for (int q = 0; q < Q; ++q) {
-                ay[q] = vq[q] ? fabs(y[q]) : 0.0;
-                ae[q] = vq[q] ? fabs(en[q]) : 0.0;
+                double y = acc[rr][q];
+                if (has_xi) y = y - a.xi * fs[rr][q];
+                if (a.single_variant) {
+                  y = fac * y;  // phi_single.cpp:106
+                } else {
+                  y = y / double(kk);  // phi_block.cpp:132
+                  y = y * tosF[q];     // :134-135
+                }
+                const double en = eo[rr][q] + y;  // E += F (:138)
+                if (vq[rr][q]) {
+                  const size_t o = size_t(row) * size_t(ldf) + c[q];
+                  Fn[o] = y;
+                  a.E[o] = en;
+                }
+                ay[q] = vq[rr][q] ? fabs(y) : 0.0;
+                ae[q] = vq[rr][q] ? fabs(en) : 0.0;
               }
-              const double ry = group_rowsum<Q>(ay, GF, qpF);
-              const double re = group_rowsum<Q>(ae, GF, qpF);
-              if (rv) {
+              const double ry = group_rowsum<Q>(ay, LF.G, LF.qp);
+              const double re = group_rowsum<Q>(ae, LF.G, LF.qp);
+              if (row < n) {
                 mfb = umax64(mfb, abs_bits(ry));
                 meb = umax64(meb, abs_bits(re));
               }
             }
-          double maxF2, maxE;
-          sync_step(mfb, meb, maxF2, maxE);
-          d2 = maxF2;
-          if (!isfinite(d2)) {
-            err = kStRecoveryDiverged;
-            err_idx = kk;
-            break;
           }
-          nE = maxE;
-          trace(3.0, d2, nE);
-          double* tmp = Fc;
-          Fc = Fn;
-          Fn = tmp;
-        }
-        if (err != kStOk) break;
-        if (master && sweep - 1 < a.s_eff - 1) a.lensF[sweep - 1] = kk;
+      }
+      double maxF2, maxE;
+      sync_step(mfb, meb, maxF2, maxE);
+      d2 = maxF2;
+      if (!isfinite(d2)) {
+        err = kStRecoveryDiverged;
+        err_idx = kk;
+        break;
+      }
+      nE = maxE;
+      trace(3.0, d2, nE);
+      double* tmp = Fc;
+      Fc = Fn;
+      Fn = tmp;
+    }
+    if (err != kStOk) break;
+    if (master) a.lensF[sweep - 1] = kk;
 
-        // ---- sweep end (:141-145): E *= mu; Sadv = Sadv*Jexp; F refresh
-        // phase A (S layout): Sadv blocks 1..p, in place, ascending source
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
-          for (int ro = gidS; ro < a.tile; ro += gpcS) {
-            const int row = t * a.tile + ro;
-            const bool rv = row < n;
+    // ---- sweep end (:141-145): E *= mu; Sadv = Sadv*Jexp; F refresh
+    // phase A (S layout): Sadv blocks 1..p in place, ascending source column
+    {
+      int c[Q];
+      bool v[Q];
+      cols(LS, c, v);
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+          const int base = t * a.tile + wt * LS.RW;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
             double nv[Q];
             bool wq[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
-              wq[q] = rv && vS[q] && jS[q] >= 1;
+              const int j = v[q] ? c[q] / r : 0, i = c[q] - j * r;
+              wq[q] = row < n && v[q] && j >= 1;
               nv[q] = 0.0;
               if (wq[q]) {
                 const double* srow = a.S + size_t(row) * size_t(ldb);
-                const double* cc = a.jc + size_t(iS[q]) * size_t(p + 1);
+                const double* cc = a.jc + size_t(i) * size_t(p + 1);
                 double accv = 0.0;
-                for (int l = 1; l <= jS[q]; ++l)
-                  accv = accv + ldcg(srow + l * r + iS[q]) * __ldg(cc + (jS[q] - l));
+                for (int l = 1; l <= j; ++l) accv = accv + srow[l * r + i] * __ldg(cc + (j - l));
                 nv[q] = accv;
               }
             }
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < Q; ++q)
-              if (wq[q]) a.S[size_t(row) * size_t(ldb) + cS[q]] = nv[q];
+              if (wq[q]) a.S[size_t(row) * size_t(ldb) + c[q]] = nv[q];
           }
-        __syncthreads();
-        // phase B (F layout): F_L = E_L*mu, F_R = E_R*mu + Sadv_p; E = F
-        const bool last = sweep == a.s_eff - 1;
-        unsigned long long mfe = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
-          for (int ro = gidF; ro < a.tile; ro += gpcF) {
-            const int row = t * a.tile + ro;
+        }
+    }
+    __syncthreads();
+    // phase B (F layout): F_L = E_L*mu, F_R = E_R*mu + Sadv_p; E = F
+    const bool last = sweep == a.s_eff - 1;
+    unsigned long long mfe = 0;
+    {
+      int c[Q];
+      bool v[Q];
+      cols(LF, c, v);
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
+          const int base = t * a.tile + wt * LF.RW;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LF.gpw + LF.g;
             const bool rv = row < n;
             double f[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
               f[q] = 0.0;
-              if (rv && vF[q]) {
-                const size_t o = size_t(row) * size_t(ldf) + cF[q];
-                const double en = ldcg(a.E + o) * __ldg(a.mu + iF[q]);
+              if (rv && v[q]) {
+                const int i = c[q] < r ? c[q] : c[q] - r;
+                const size_t o = size_t(row) * size_t(ldf) + c[q];
+                const size_t srow = size_t(row) * size_t(ldb) + size_t(p) * size_t(r);
+                const double en = a.E[o] * __ldg(a.mu + i);
                 double fv = en;
-                if (cF[q] >= r)
-                  fv = en + ldcg(a.S + size_t(row) * size_t(ldb) + size_t(p) * size_t(r) + iF[q]);
+                if (c[q] >= r) fv = en + a.S[srow + i];
                 f[q] = fv;
-                if (last && cF[q] < r) {
-                  const int i = cF[q];
+                if (last && c[q] < r) {
                   double wv = fv;
                   double fr = 0.0;
                   if (p > 0) {
-                    const double er = ldcg(a.E + size_t(row) * size_t(ldf) + r + i) * __ldg(a.mu + i);
-                    fr = er + ldcg(a.S + size_t(row) * size_t(ldb) + size_t(p) * size_t(r) + i);
+                    const double er = a.E[size_t(row) * size_t(ldf) + r + i] * __ldg(a.mu + i);
+                    fr = er + a.S[srow + i];
                     wv = wv + (a.single_variant ? __ldg(a.alpha + i) * fr : fr * __ldg(a.alpha + i));
                   }
                   a.W[size_t(i) * size_t(n) + row] = wv;
@@ -579,36 +683,28 @@ __global__ void __launch_bounds__(kBlock) k_phimv_block(BlockArgs a) {
             }
             if (!last) {
               __syncwarp();
+              double af[Q];
 #pragma unroll
-              for (int q = 0; q < Q; ++q)
-                if (rv && vF[q]) {
-                  const size_t o = size_t(row) * size_t(ldf) + cF[q];
+              for (int q = 0; q < Q; ++q) {
+                if (rv && v[q]) {
+                  const size_t o = size_t(row) * size_t(ldf) + c[q];
                   Fc[o] = f[q];
                   a.E[o] = f[q];
                 }
-              double af[Q];
-#pragma unroll
-              for (int q = 0; q < Q; ++q) af[q] = (rv && vF[q]) ? fabs(f[q]) : 0.0;
-              const double rf = group_rowsum<Q>(af, GF, qpF);
+                af[q] = (rv && v[q]) ? fabs(f[q]) : 0.0;
+              }
+              const double rf = group_rowsum<Q>(af, LF.G, LF.qp);
               if (rv) mfe = umax64(mfe, abs_bits(rf));
             }
           }
-        if (!last) {
-          double mxf, dmy;
-          sync_step(mfe, mfe, mxf, dmy);
-          fnorm = mxf;
         }
-      }
-      if (master) {
-        a.status[0] = err;
-        a.status[1] = err_idx;
-        a.status[2] = L_S;
-        a.status[3] = 0;
-        a.status[4] = step;
-        a.status[5] = min(tr_len, a.trace_cap);
-      }
+    }
+    if (!last) {
+      double dmy;
+      sync_step(mfe, mfe, fnorm, dmy);
     }
   }
+  finish(err, err_idx, L_S, 0);
 }
 
 // ---------------------------------------------------------------------------
