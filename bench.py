@@ -121,6 +121,17 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def max_over_ranks(x: float, dist=None, device="cpu") -> float:
+    """Max of a per-rank timing over all ranks (the contract's max-over-ranks
+    clock); identity without a process group."""
+    if dist is None:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def algorithmic_bytes(wl, rec):
     """Algorithmic HBM bytes of one k_phimv_block launch:
     init 8n(p+1) + 24wn; each S term B_S = CSR + 48wn; promotion+assembly
@@ -283,10 +294,7 @@ def main():
     launches = P.kernel_launches() - launches0
     elapsed = ev0.elapsed_time(ev1) / 1e3
     barrier()
-    t = torch.tensor([elapsed], dtype=torch.float64, device=f"cuda:{local}")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_max = float(t.item())
+    elapsed_max = max_over_ranks(elapsed, dist, f"cuda:{local}")
     value = args.steps * world / elapsed_max
 
     # ---- e2e through the C-ABI host-buffer call: pinned V in, W out ----
@@ -319,10 +327,7 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_el = e0.elapsed_time(e1) / 1e3
-    t = torch.tensor([e2e_el], dtype=torch.float64, device=f"cuda:{local}")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_value = e2e_steps * world / float(t.item())
+    e2e_value = e2e_steps * world / max_over_ranks(e2e_el, dist, f"cuda:{local}")
 
     # ---- roofline of the dominant (only) kernel, k_phimv_block ----
     peak, peak_src = measured_peak()

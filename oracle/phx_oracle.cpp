@@ -43,6 +43,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -889,17 +890,30 @@ struct LMat {
   LD operator()(long i, long j) const { return a[size_t(i) + size_t(j) * size_t(n)]; }
 };
 
+// C = A B; output columns are split across host threads (each column is
+// computed by one thread in a fixed order, so the result is thread-count
+// independent).
 static LMat lmul(const LMat& A, const LMat& B) {
   const long n = A.n;
   LMat C(n);
-  for (long j = 0; j < n; ++j)
-    for (long k = 0; k < n; ++k) {
-      const LD b = B(k, j);
-      if (b == 0.0L) continue;
-      const LD* ak = &A.a[size_t(k) * size_t(n)];
-      LD* cj = &C.a[size_t(j) * size_t(n)];
-      for (long i = 0; i < n; ++i) cj[i] += ak[i] * b;
-    }
+  auto cols = [&](long j0, long j1) {
+    for (long j = j0; j < j1; ++j)
+      for (long k = 0; k < n; ++k) {
+        const LD b = B(k, j);
+        if (b == 0.0L) continue;
+        const LD* ak = &A.a[size_t(k) * size_t(n)];
+        LD* cj = &C.a[size_t(j) * size_t(n)];
+        for (long i = 0; i < n; ++i) cj[i] += ak[i] * b;
+      }
+  };
+  const long nt = n >= 128 ? std::max(1u, std::thread::hardware_concurrency()) : 1;
+  if (nt <= 1) {
+    cols(0, n);
+    return C;
+  }
+  std::vector<std::thread> ts;
+  for (long q = 0; q < nt; ++q) ts.emplace_back(cols, n * q / nt, n * (q + 1) / nt);
+  for (auto& t : ts) t.join();
   return C;
 }
 

@@ -1,0 +1,94 @@
+"""The oracle against its committed golden fixtures (tests/golden/, made by
+tests/golden/make_golden.py): bitwise reproduction of ScalingShift,
+RunRecord, W and the stopping-test trace on seeded BASELINE workloads, and
+agreement with the long-double augmented-matrix reference (reference_w,
+oracle.cpp:53-91 restated) within the user tolerance where n + p <= 2000."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2509_26475_b200 as P
+
+SMALL = ["cfg1_s200", "cfg2_s64", "cfg3_s12", "cfg4_s1024", "cfg5_s2000", "cfg1_s1000"]
+
+
+def load(golden_dir, name):
+    with open(os.path.join(golden_dir, name + ".json")) as f:
+        meta = json.load(f)
+    arr = np.load(os.path.join(golden_dir, name + ".npz"))
+    return meta, arr
+
+
+def sha(a):
+    return hashlib.sha256(np.asfortranarray(a, dtype=np.float64).tobytes(order="F")).hexdigest()
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_oracle_reproduces_fixture(golden_dir, name):
+    meta, arr = load(golden_dir, name)
+    wl = P.workload(meta["cfg"], meta["size"])
+    op = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    ss = O.select_parameters(op, 61, wl.tol)
+    assert list(ss.astuple()) == meta["params"]
+    W, rec, tr = O.phimv_block(op, wl.t, wl.alpha, wl.V, wl.tol, ss, trace=True)
+    assert rec.s_effective == meta["s_effective"]
+    assert rec.series_len_S == meta["series_len_S"]
+    assert rec.series_lens_F == meta["series_lens_F"]
+    assert rec.matvecs == meta["matvecs"]
+    assert np.array_equal(W, arr["W"])
+    assert sha(W) == meta["W_sha256"]
+    assert np.array_equal(tr, arr["trace"])
+
+
+HP = [("cfg1_s1000", 1, 0), ("cfg2_s44", 2, 44), ("cfg3_s12", 3, 12), ("cfg4_s1024", 4, 1024),
+      ("cfg5_s1990", 5, 1990)]
+
+
+@pytest.mark.parametrize("name,cfg,size", HP)
+def test_high_precision(golden_dir, name, cfg, size):
+    """W within the user tolerance of the long-double reference (per column,
+    normwise relative)."""
+    path = os.path.join(golden_dir, f"hp_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip("high-precision fixture not generated")
+    ref = np.load(path)["W_ref"]
+    wl = P.workload(cfg, size)
+    op = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    ss = O.select_parameters(op, 61, wl.tol)
+    W, rec = O.phimv_block(op, wl.t, wl.alpha, wl.V, wl.tol, ss)
+    for i in range(wl.r):
+        scale = np.abs(ref[:, i]).max()
+        err = np.linalg.norm((W[:, i] - ref[:, i]) / scale) / np.linalg.norm(ref[:, i] / scale)
+        # the user tolerance, with the reference tests' 10x slack (test_phi_block.cpp:38)
+        # and a floor at rounding level (sum of ~n*L_S rounded terms)
+        bound = max(10.0 * wl.tol, 1e-12)
+        assert err <= bound, (i, err, bound)
+
+
+def test_workload_generators():
+    """Structure and sizes of the five configs (csrc/workloads.cpp)."""
+    expect = {1: (1000, 2998), 2: (4096, 5 * 4096 - 4 * 64), 3: (1728, 7 * 1728 - 6 * 144),
+              4: (1024, 17 * 1024), 5: (2000, 3999)}
+    sizes = {1: 0, 2: 64, 3: 12, 4: 1024, 5: 2000}
+    for cfg, (n, nnz) in expect.items():
+        wl = P.workload(cfg, sizes[cfg])
+        assert (wl.n, wl.nnz) == (n, nnz)
+        assert wl.rp[0] == 0 and wl.rp[-1] == nnz and np.all(np.diff(wl.rp) >= 0)
+        for i in range(0, wl.n, max(1, wl.n // 50)):
+            cols = wl.ci[wl.rp[i]:wl.rp[i + 1]]
+            assert np.all(np.diff(cols) > 0)  # sorted, distinct
+            assert i in cols
+        assert np.all(np.isfinite(wl.V))
+    wl = P.workload(1, 0)
+    assert wl.av[0] == -2.0 * 1001.0 ** 2 and wl.av[1] == 1001.0 ** 2
+    # C4: diagonally dominant negative diagonal
+    wl = P.workload(4, 1024)
+    for i in range(0, 1024, 97):
+        s, e = wl.rp[i], wl.rp[i + 1]
+        d = wl.av[s:e][wl.ci[s:e] == i][0]
+        off = np.abs(wl.av[s:e][wl.ci[s:e] != i]).sum()
+        assert d < -off - 1.0 + 1e-9
