@@ -1,0 +1,832 @@
+// The persistent phimv_block kernel (phi_block.cpp:48-157, Alg. 3), sm_100a.
+//
+// ONE cooperative launch per evaluation.  Every Taylor term is a grid step:
+// the CTAs sweep their row tiles, each lane group (G lanes of a warp, V = 1
+// or 2 adjacent columns per lane, Q column chunks) gathers the CSR row's
+// block rows (row-interleaved layout, one coalesced vector load per gathered
+// row), fuses the shift, scaling, J-term and accumulator updates with both
+// |.| row sums, and publishes a per-CTA max with one atomicMax; after
+// grid.sync() every CTA reads the two maxima and takes the same stopping
+// decision, so loop control never leaves the device.
+//
+// Compiled with --fmad=false (no FMA): bit-for-bit the oracle's operation
+// order (oracle/phx_oracle.cpp).  Row sums use the canonical
+// pairwise tree over pow2-padded natural column order: with V = 2 the
+// lane-local pair is the tree's first level, the butterfly the next ones.
+#include <cooperative_groups.h>
+
+#include "phx_kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace phx {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int kWCap = 256;  // staged CSR entries per warp tile
+constexpr int kMaxRW = 64;  // rows per warp tile
+
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ double from_bits(unsigned long long b) {
+  return __longlong_as_double(static_cast<long long>(b));
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+
+template <int V>
+struct Vio;
+template <>
+struct Vio<1> {
+  __device__ __forceinline__ static void ld(const double* p, double (&x)[1]) { x[0] = *p; }
+  __device__ __forceinline__ static void st(double* p, const double (&x)[1]) { *p = x[0]; }
+};
+template <>
+struct Vio<2> {
+  __device__ __forceinline__ static void ld(const double* p, double (&x)[2]) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    x[0] = t.x;
+    x[1] = t.y;
+  }
+  __device__ __forceinline__ static void st(double* p, const double (&x)[2]) {
+    *reinterpret_cast<double2*>(p) = make_double2(x[0], x[1]);
+  }
+};
+
+template <int Q, int V>
+struct Cfg {
+  static constexpr int R = (Q == 1 && V == 1) ? 2 : 1;  // rows per lane group per warp tile
+  static constexpr int B = (Q * V <= 2) ? 4 : 2;        // gather batch (entries in flight)
+};
+
+// Lane-group layout of one phase (S width or F width).
+struct Layout {
+  int G, gpw, g, lg, RW, qn, qp, width;
+};
+
+__device__ __forceinline__ Layout make_layout(int G, int qn, int width, int R, int V) {
+  Layout L;
+  const int lane = threadIdx.x & 31;
+  L.G = G;
+  L.gpw = 32 / G;
+  L.g = lane / G;
+  L.lg = lane % G;
+  L.RW = L.gpw * R;
+  L.qn = qn;
+  L.width = width;
+  const int chunk = 32 * V;  // columns per chunk q
+  int chunks = (width + chunk - 1) / chunk;
+  int qp = 1;
+  while (qp < chunks) qp <<= 1;
+  L.qp = width > chunk ? qp : 1;
+  return L;
+}
+
+// Canonical row sum of the group's |values| (pairwise tree over pow2-padded
+// natural column order; invalid lanes hold 0).
+template <int Q, int V>
+__device__ __forceinline__ double group_rowsum(const double (&v)[Q][V], int G, int qp) {
+  double T[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    double x = v[q][0];
+    if (V == 2) x = x + v[q][V - 1];
+    for (int m = 1; m < G; m <<= 1) x = x + __shfl_xor_sync(kFull, x, m);
+    T[q] = x;
+  }
+#pragma unroll
+  for (int h = 1; h < Q; h <<= 1) {
+    if (h < qp) {
+#pragma unroll
+      for (int q = 0; q + h < Q; q += 2 * h) T[q] = T[q] + T[q + h];
+    }
+  }
+  return T[0];
+}
+
+// CTA max of two bit patterns -> one atomicMax each into the step's slot.
+__device__ __forceinline__ void publish2(unsigned long long a, unsigned long long b,
+                                         unsigned long long* slot,
+                                         unsigned long long (*red)[kWarps]) {
+  for (int m = 16; m >= 1; m >>= 1) {
+    a = umax64(a, __shfl_xor_sync(kFull, a, m));
+    b = umax64(b, __shfl_xor_sync(kFull, b, m));
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = a;
+    red[1][warp] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ma = 0, mb = 0;
+    for (int q = 0; q < kWarps; ++q) {
+      ma = umax64(ma, red[0][q]);
+      mb = umax64(mb, red[1][q]);
+    }
+    atomicMax(slot, ma);
+    atomicMax(slot + 1, mb);
+  }
+  __syncthreads();
+}
+
+// Warp-private staging of one warp tile's CSR slice: row_ptr, then the
+// contiguous entry range as (element offset col*ld, value) pairs.
+struct WarpStage {
+  int rp[kMaxRW + 1];
+  unsigned off[kWCap];
+  double av[kWCap];
+};
+
+__device__ __forceinline__ bool stage_csr(const BlockArgs& a, int base, int RW, unsigned ld,
+                                          WarpStage& st, int lane, int& e_lo) {
+  __syncwarp();  // every lane is done with the previous tile's slice
+  for (int l = lane; l <= RW; l += 32) st.rp[l] = __ldg(a.rp + min(base + l, a.n));
+  __syncwarp();
+  e_lo = st.rp[0];
+  const int E = st.rp[RW] - e_lo;
+  const bool fits = E <= kWCap;
+  if (fits) {
+    for (int e = lane; e < E; e += 32) {
+      st.off[e] = unsigned(__ldg(a.ci + e_lo + e)) * ld;
+      st.av[e] = __ldg(a.av + e_lo + e);
+    }
+  }
+  __syncwarp();
+  return fits;
+}
+
+// acc[rr][q][e] = sum over row rr's entries (storage order, from +0) of
+// av * X[col*ld + c].  X was written before the last grid.sync(), which
+// invalidates L1 (CCTL.IVALL), so plain cached loads are coherent.
+template <int Q, int V, int R, int B, bool SMEM>
+__device__ __forceinline__ void gather(const BlockArgs& a, const WarpStage& st, int e_lo,
+                                       unsigned ld, const int (&rs)[R], const int (&cnt)[R],
+                                       const double* X, const unsigned (&cq)[Q],
+                                       const bool (&vq)[Q], double (&acc)[R][Q][V]) {
+  int maxc = 0;
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) maxc = max(maxc, cnt[rr]);
+  for (int u0 = 0; u0 < maxc; u0 += B) {
+    double xv[B][R][Q][V];
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const bool ok = u0 + u < cnt[rr];
+        unsigned off = 0;
+        if (ok) {
+          const int e = rs[rr] + u0 + u;
+          off = SMEM ? st.off[e] : unsigned(__ldg(a.ci + e_lo + e)) * ld;
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          if (ok && vq[q]) {
+            Vio<V>::ld(X + (off + cq[q]), xv[u][rr][q]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) xv[u][rr][q][e] = 0.0;
+          }
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr)
+        if (u0 + u < cnt[rr]) {
+          const int e = rs[rr] + u0 + u;
+          const double av = SMEM ? st.av[e] : __ldg(a.av + e_lo + e);
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[rr][q][v] = acc[rr][q][v] + av * xv[u][rr][q][v];
+        }
+  }
+}
+
+template <int Q, int V, int R, int B>
+__device__ __forceinline__ void gather_tile(const BlockArgs& a, const WarpStage& st, bool fits,
+                                            int e_lo, unsigned ld, const int (&rs)[R],
+                                            const int (&cnt)[R], const double* X,
+                                            const unsigned (&cq)[Q], const bool (&vq)[Q],
+                                            double (&acc)[R][Q][V]) {
+  if (fits)
+    gather<Q, V, R, B, true>(a, st, e_lo, ld, rs, cnt, X, cq, vq, acc);
+  else
+    gather<Q, V, R, B, false>(a, st, e_lo, ld, rs, cnt, X, cq, vq, acc);
+}
+
+template <int Q, int V>
+__global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 : 1))
+    k_phimv_block(BlockArgs a) {
+  constexpr int R = Cfg<Q, V>::R;
+  constexpr int B = Cfg<Q, V>::B;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long red[2][kWarps];
+  __shared__ WarpStage stage[kWarps];
+  const double INF = __longlong_as_double(0x7FF0000000000000ll);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpStage& st = stage[warp];
+
+  const int n = a.n, r = a.r, p = a.p;
+  const unsigned ldb = unsigned(a.ldb), ldf = unsigned(a.ldf);
+  const int ntiles = (n + a.tile - 1) / a.tile;
+  const bool has_xi = a.xi != 0.0;
+  const bool master = blockIdx.x == 0 && threadIdx.x == 0;
+  const Layout LS = make_layout(a.GS, a.QS, a.w, R, V);
+  const Layout LF = make_layout(a.GF, a.QF, a.fcols, R, V);
+
+  int step = 0;
+  int tr_len = 0;
+  auto trace = [&](double kind, double x, double y) {
+    if (master && a.trace != nullptr && tr_len + 3 <= a.trace_cap) {
+      a.trace[tr_len] = kind;
+      a.trace[tr_len + 1] = x;
+      a.trace[tr_len + 2] = y;
+    }
+    tr_len += 3;
+  };
+  // publish this CTA's maxima, zero the next step's slot (its last readers
+  // finished before the previous grid sync), grid-sync, read the maxima
+  auto sync_step = [&](unsigned long long ma, unsigned long long mb, double& ra, double& rb) {
+    unsigned long long* slot = a.slots + 2 * (step % 3);
+    publish2(ma, mb, slot, red);
+    if (master) {
+      unsigned long long* nxt = a.slots + 2 * ((step + 1) % 3);
+      nxt[0] = 0ull;
+      nxt[1] = 0ull;
+    }
+    grid.sync();
+    ra = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot)));
+    rb = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot + 1)));
+    ++step;
+  };
+  auto finish = [&](int err, int idx, int L_S, int extra_steps) {
+    if (master) {
+      a.status[0] = err;
+      a.status[1] = idx;
+      a.status[2] = L_S;
+      a.status[3] = 0;
+      a.status[4] = step + extra_steps;
+      a.status[5] = min(tr_len, a.trace_cap);
+    }
+  };
+  // lane column offsets (first column of each chunk) and chunk validity
+  auto cols = [&](const Layout& L, unsigned (&c)[Q], bool (&v)[Q]) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      c[q] = unsigned(V * (L.lg + L.G * q));
+      v[q] = (q < L.qn) && (int(c[q]) < L.width);
+    }
+  };
+
+  // ================= init: Vw = V[src]*g, D = S = Vw (phi_block.cpp:76-92)
+  unsigned long long m0 = 0;
+  {
+    unsigned c[Q];
+    bool v[Q];
+    cols(LS, c, v);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+        const int base = t * a.tile + wt * LS.RW;
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = base + rr * LS.gpw + LS.g;
+          const bool rv = row < n;
+          double x[Q][V], ax[Q][V];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+              x[q][e] = 0.0;
+              if (rv && v[q]) {
+                const int cc = int(c[q]) + e;
+                const int j = cc / r, i = cc - j * r;
+                const int src = j == 0 ? 0 : p + 1 - j;
+                x[q][e] = __ldg(a.V + size_t(src) * size_t(n) + row) * __ldg(a.g + i);
+              }
+              ax[q][e] = fabs(x[q][e]);
+            }
+            if (rv && v[q]) {
+              const unsigned o = unsigned(row) * ldb + c[q];
+              Vio<V>::st(a.Vw + o, x[q]);
+              Vio<V>::st(a.D0 + o, x[q]);
+              Vio<V>::st(a.S + o, x[q]);
+            }
+          }
+          const double rsum = group_rowsum<Q, V>(ax, LS.G, LS.qp);
+          if (rv) m0 = umax64(m0, abs_bits(rsum));
+        }
+      }
+  }
+  double mD, mSn;
+  sync_step(m0, m0, mD, mSn);
+  double c1 = INF, c2 = mD, nS = mSn;  // c2 = inf_norm(D), ||S|| at k = 1
+  trace(0.0, c2, nS);
+
+  // ================= S series (phi_block.cpp:93-106)
+  int k = 1;
+  double sigma = 1.0;
+  double* Dc = a.D0;
+  double* Dn = a.D1;
+  int err = kStOk, err_idx = 0;
+  const bool vwl_vec = V == 2 && (r % 2) == 0;
+  while (c1 + c2 > a.tol * nS) {
+    if (k >= 500) {
+      err = kStSeriesCap;
+      err_idx = 500;
+      break;
+    }
+    ++k;
+    c1 = c2;
+    sigma *= k;
+    unsigned long long mdb = 0, msb = 0;
+    {
+      unsigned c[Q];
+      bool v[Q];
+      cols(LS, c, v);
+      int jj[Q][V];
+      double kd[Q][V], ka[Q][V], tos[Q][V];
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const int cc = int(c[q]) + e;
+          jj[q][e] = v[q] ? cc / r : 0;
+          kd[q][e] = v[q] ? __ldg(a.colKd + cc) : 0.0;
+          ka[q][e] = v[q] ? __ldg(a.colKa + cc) : 0.0;
+          tos[q][e] = v[q] ? __ldg(a.colTos + cc) : 0.0;
+        }
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+          const int base = t * a.tile + wt * LS.RW;
+          // row-local streams first (independent of the CSR slice)
+          double vw[R][Q][V], vwl[R][Q][V], so[R][Q][V], ds[R][Q][V], acc[R][Q][V];
+          bool vq[R][Q];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              vq[rr][q] = row < n && v[q];
+              const unsigned o = unsigned(row) * ldb + c[q];
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                vw[rr][q][e] = vwl[rr][q][e] = so[rr][q][e] = ds[rr][q][e] = 0.0;
+                acc[rr][q][e] = 0.0;
+              }
+              if (vq[rr][q]) {
+                Vio<V>::ld(a.Vw + o, vw[rr][q]);
+                Vio<V>::ld(a.S + o, so[rr][q]);
+                if (has_xi) Vio<V>::ld(Dc + o, ds[rr][q]);
+                if (vwl_vec) {
+                  if (jj[q][0] >= 2) Vio<V>::ld(a.Vw + (o - unsigned(r)), vwl[rr][q]);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < V; ++e)
+                    if (jj[q][e] >= 2) vwl[rr][q][e] = a.Vw[o + e - unsigned(r)];
+                }
+              }
+            }
+          }
+          int e_lo;
+          const bool fits = stage_csr(a, base, LS.RW, ldb, st, lane, e_lo);
+          int rs[R], cnt[R];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int li = rr * LS.gpw + LS.g;
+            rs[rr] = st.rp[li] - e_lo;
+            cnt[rr] = st.rp[li + 1] - st.rp[li];
+          }
+          gather_tile<Q, V, R, B>(a, st, fits, e_lo, ldb, rs, cnt, Dc, c, v, acc);
+          double vn[R][Q][V], dn[R][Q][V], sn[R][Q][V];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                // Vw = Vw * Kiter: ascending source column from +0 (:98)
+                double g2 = 0.0;
+                if (jj[q][e] >= 2) g2 = g2 + vwl[rr][q][e] * ka[q][e];
+                g2 = g2 + vw[rr][q][e] * kd[q][e];
+                vn[rr][q][e] = g2;
+                // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
+                double y = acc[rr][q][e];
+                if (has_xi) y = y - a.xi * ds[rr][q][e];
+                y = y * tos[q][e];
+                dn[rr][q][e] = y + g2;
+                sn[rr][q][e] = so[rr][q][e] + dn[rr][q][e] / sigma;  // S += D/sigma (:105)
+              }
+          __syncwarp();  // every lane has read its Vw[c - r] before any lane writes Vw
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
+            double ad[Q][V], as[Q][V];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              if (vq[rr][q]) {
+                const unsigned o = unsigned(row) * ldb + c[q];
+                Vio<V>::st(a.Vw + o, vn[rr][q]);
+                Vio<V>::st(Dn + o, dn[rr][q]);
+                Vio<V>::st(a.S + o, sn[rr][q]);
+              }
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                ad[q][e] = vq[rr][q] ? fabs(dn[rr][q][e]) : 0.0;
+                as[q][e] = vq[rr][q] ? fabs(sn[rr][q][e]) : 0.0;
+              }
+            }
+            const double rd = group_rowsum<Q, V>(ad, LS.G, LS.qp);
+            const double rsm = group_rowsum<Q, V>(as, LS.G, LS.qp);
+            if (row < n) {
+              mdb = umax64(mdb, abs_bits(rd));
+              msb = umax64(msb, abs_bits(rsm));
+            }
+          }
+        }
+    }
+    double maxD, maxS;
+    sync_step(mdb, msb, maxD, maxS);
+    c2 = maxD / sigma;  // :103
+    if (!isfinite(c2)) {
+      err = kStSeriesDiverged;
+      err_idx = k;
+      break;
+    }
+    nS = maxS;
+    trace(1.0, c2, nS);
+    double* tmp = Dc;
+    Dc = Dn;
+    Dn = tmp;
+  }
+  const int L_S = k;
+  if (err != kStOk) {
+    finish(err, err_idx, L_S, 0);
+    return;
+  }
+
+  // ================= promotion (phi_block.cpp:109-120)
+  // F_L = fl(fl(A S_L * t_i) + v0) (unshifted A), F_R = S block p.
+  double* Fc = a.F0;
+  double* Fn = a.F1;
+  const bool sweeps = a.s_eff > 1;
+  unsigned long long mf = 0;
+  {
+    unsigned c[Q];
+    bool v[Q], vl[Q];
+    cols(LF, c, v);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) vl[q] = v[q] && int(c[q]) < r;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
+        const int base = t * a.tile + wt * LF.RW;
+        double acc[R][Q][V];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[rr][q][e] = 0.0;
+        int e_lo;
+        const bool fits = stage_csr(a, base, LF.RW, ldb, st, lane, e_lo);
+        int rs[R], cnt[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int li = rr * LF.gpw + LF.g;
+          rs[rr] = st.rp[li] - e_lo;
+          cnt[rr] = st.rp[li + 1] - st.rp[li];
+        }
+        // gathers S block-0 columns (left F columns live at the same column
+        // index in S); a pair straddling the left/right split gathers one
+        // extra column, unused
+        gather_tile<Q, V, R, B>(a, st, fits, e_lo, ldb, rs, cnt, a.S, c, vl, acc);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = base + rr * LF.gpw + LF.g;
+          const bool rv = row < n;
+          double f[Q][V], af[Q][V];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+              f[q][e] = 0.0;
+              const int cc = int(c[q]) + e;
+              if (rv && v[q]) {
+                const int i = cc < r ? cc : cc - r;
+                const size_t srow = size_t(row) * ldb + size_t(p) * size_t(r);
+                if (cc < r) {
+                  const double sc = acc[rr][q][e] * __ldg(a.t + i);
+                  f[q][e] = sc + __ldg(a.V + row);
+                } else {
+                  f[q][e] = a.S[srow + i];
+                }
+                if (!sweeps && cc < r) {
+                  // assembly W = F_L + fl(F_R * alpha) (:148-154)
+                  double wv = f[q][e];
+                  double fr = 0.0;
+                  if (p > 0) {
+                    fr = a.S[srow + i];
+                    wv = wv + fr * __ldg(a.alpha + i);
+                  }
+                  a.W[size_t(i) * size_t(n) + row] = wv;
+                  if (a.FLo) a.FLo[size_t(i) * size_t(n) + row] = f[q][e];
+                  if (a.FRo) a.FRo[size_t(i) * size_t(n) + row] = fr;
+                }
+              }
+              af[q][e] = fabs(f[q][e]);
+            }
+            if (sweeps && rv && v[q]) {
+              const unsigned o = unsigned(row) * ldf + c[q];
+              Vio<V>::st(Fc + o, f[q]);
+              Vio<V>::st(a.E + o, f[q]);
+            }
+          }
+          if (sweeps) {
+            const double rf = group_rowsum<Q, V>(af, LF.G, LF.qp);
+            if (rv) mf = umax64(mf, abs_bits(rf));
+          }
+        }
+      }
+  }
+  if (!sweeps) {
+    finish(kStOk, 0, L_S, 1);
+    return;
+  }
+  double fnorm, dummy;
+  sync_step(mf, mf, fnorm, dummy);
+
+  // ================= recovery sweeps (phi_block.cpp:122-146)
+  for (int sweep = 1; sweep < a.s_eff; ++sweep) {
+    int kk = 0;
+    double d1 = INF, d2 = fnorm, nE = fnorm;  // E = F
+    trace(2.0, d2, nE);
+    while (d1 + d2 > a.tol * nE) {
+      if (kk >= 300) {
+        err = kStRecoveryCap;
+        err_idx = 300;
+        break;
+      }
+      ++kk;
+      d1 = d2;
+      const double fac = a.single_variant ? a.t_single / (double(a.s_eff) * kk) : 0.0;
+      unsigned long long mfb = 0, meb = 0;
+      {
+        unsigned c[Q];
+        bool v[Q];
+        double tosF[Q][V];
+        cols(LF, c, v);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            const int cc = int(c[q]) + e;
+            const int i = cc < r ? cc : cc - r;
+            tosF[q][e] = v[q] ? __ldg(a.colTos + i) : 0.0;
+          }
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+          for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
+            const int base = t * a.tile + wt * LF.RW;
+            double eo[R][Q][V], fs[R][Q][V], acc[R][Q][V];
+            bool vq[R][Q];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              const int row = base + rr * LF.gpw + LF.g;
+#pragma unroll
+              for (int q = 0; q < Q; ++q) {
+                vq[rr][q] = row < n && v[q];
+                const unsigned o = unsigned(row) * ldf + c[q];
+#pragma unroll
+                for (int e = 0; e < V; ++e) eo[rr][q][e] = fs[rr][q][e] = acc[rr][q][e] = 0.0;
+                if (vq[rr][q]) {
+                  Vio<V>::ld(a.E + o, eo[rr][q]);
+                  if (has_xi) Vio<V>::ld(Fc + o, fs[rr][q]);
+                }
+              }
+            }
+            int e_lo;
+            const bool fits = stage_csr(a, base, LF.RW, ldf, st, lane, e_lo);
+            int rs[R], cnt[R];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              const int li = rr * LF.gpw + LF.g;
+              rs[rr] = st.rp[li] - e_lo;
+              cnt[rr] = st.rp[li + 1] - st.rp[li];
+            }
+            gather_tile<Q, V, R, B>(a, st, fits, e_lo, ldf, rs, cnt, Fc, c, v, acc);
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              const int row = base + rr * LF.gpw + LF.g;
+              double y[Q][V], en[Q][V], ay[Q][V], ae[Q][V];
+#pragma unroll
+              for (int q = 0; q < Q; ++q) {
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                  double yv = acc[rr][q][e];
+                  if (has_xi) yv = yv - a.xi * fs[rr][q][e];
+                  if (a.single_variant) {
+                    yv = fac * yv;  // phi_single.cpp:106
+                  } else {
+                    yv = yv / double(kk);  // phi_block.cpp:132
+                    yv = yv * tosF[q][e];  // :134-135
+                  }
+                  y[q][e] = yv;
+                  en[q][e] = eo[rr][q][e] + yv;  // E += F (:138)
+                  ay[q][e] = vq[rr][q] ? fabs(yv) : 0.0;
+                  ae[q][e] = vq[rr][q] ? fabs(en[q][e]) : 0.0;
+                }
+                if (vq[rr][q]) {
+                  const unsigned o = unsigned(row) * ldf + c[q];
+                  Vio<V>::st(Fn + o, y[q]);
+                  Vio<V>::st(a.E + o, en[q]);
+                }
+              }
+              const double ry = group_rowsum<Q, V>(ay, LF.G, LF.qp);
+              const double re = group_rowsum<Q, V>(ae, LF.G, LF.qp);
+              if (row < n) {
+                mfb = umax64(mfb, abs_bits(ry));
+                meb = umax64(meb, abs_bits(re));
+              }
+            }
+          }
+      }
+      double maxF2, maxE;
+      sync_step(mfb, meb, maxF2, maxE);
+      d2 = maxF2;
+      if (!isfinite(d2)) {
+        err = kStRecoveryDiverged;
+        err_idx = kk;
+        break;
+      }
+      nE = maxE;
+      trace(3.0, d2, nE);
+      double* tmp = Fc;
+      Fc = Fn;
+      Fn = tmp;
+    }
+    if (err != kStOk) break;
+    if (master) a.lensF[sweep - 1] = kk;
+
+    // ---- sweep end (:141-145): E *= mu; Sadv = Sadv*Jexp; F refresh
+    // phase A (S layout): Sadv blocks 1..p in place, ascending source column
+    {
+      unsigned c[Q];
+      bool v[Q];
+      cols(LS, c, v);
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+          const int base = t * a.tile + wt * LS.RW;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
+            double nv[Q][V];
+            bool wq[Q][V];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                const int cc = int(c[q]) + e;
+                const int j = v[q] ? cc / r : 0, i = cc - j * r;
+                wq[q][e] = row < n && v[q] && j >= 1;
+                nv[q][e] = 0.0;
+                if (wq[q][e]) {
+                  const double* srow = a.S + size_t(row) * ldb;
+                  const double* cj = a.jc + size_t(i) * size_t(p + 1);
+                  double accv = 0.0;
+                  for (int l = 1; l <= j; ++l) accv = accv + srow[l * r + i] * __ldg(cj + (j - l));
+                  nv[q][e] = accv;
+                }
+              }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e)
+                if (wq[q][e]) a.S[size_t(row) * ldb + c[q] + e] = nv[q][e];
+          }
+        }
+    }
+    __syncthreads();
+    // phase B (F layout): F_L = E_L*mu, F_R = E_R*mu + Sadv_p; E = F
+    const bool last = sweep == a.s_eff - 1;
+    unsigned long long mfe = 0;
+    {
+      unsigned c[Q];
+      bool v[Q];
+      cols(LF, c, v);
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
+          const int base = t * a.tile + wt * LF.RW;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LF.gpw + LF.g;
+            const bool rv = row < n;
+            double f[Q][V], af[Q][V];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                f[q][e] = 0.0;
+                const int cc = int(c[q]) + e;
+                if (rv && v[q]) {
+                  const int i = cc < r ? cc : cc - r;
+                  const size_t srow = size_t(row) * ldb + size_t(p) * size_t(r);
+                  const double en = a.E[size_t(row) * ldf + cc] * __ldg(a.mu + i);
+                  double fv = en;
+                  if (cc >= r) fv = en + a.S[srow + i];
+                  f[q][e] = fv;
+                  if (last && cc < r) {
+                    double wv = fv;
+                    double fr = 0.0;
+                    if (p > 0) {
+                      const double er = a.E[size_t(row) * ldf + r + i] * __ldg(a.mu + i);
+                      fr = er + a.S[srow + i];
+                      wv = wv + (a.single_variant ? __ldg(a.alpha + i) * fr : fr * __ldg(a.alpha + i));
+                    }
+                    a.W[size_t(i) * size_t(n) + row] = wv;
+                    if (a.FLo) a.FLo[size_t(i) * size_t(n) + row] = fv;
+                    if (a.FRo) a.FRo[size_t(i) * size_t(n) + row] = fr;
+                  }
+                }
+                af[q][e] = (rv && v[q]) ? fabs(f[q][e]) : 0.0;
+              }
+            if (!last) {
+              __syncwarp();
+#pragma unroll
+              for (int q = 0; q < Q; ++q)
+                if (rv && v[q]) {
+                  const unsigned o = unsigned(row) * ldf + c[q];
+                  Vio<V>::st(Fc + o, f[q]);
+                  Vio<V>::st(a.E + o, f[q]);
+                }
+              const double rf = group_rowsum<Q, V>(af, LF.G, LF.qp);
+              if (rv) mfe = umax64(mfe, abs_bits(rf));
+            }
+          }
+        }
+    }
+    if (!last) {
+      double dmy;
+      sync_step(mfe, mfe, fnorm, dmy);
+    }
+  }
+  finish(err, err_idx, L_S, 0);
+}
+
+template <int Q, int V>
+cudaError_t occupancy(int block, int* per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_phimv_block<Q, V>, block, 0);
+}
+
+}  // namespace
+
+cudaError_t coop_grid_size(int QT, int V, int block, int* max_blocks) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  const int key = QT * 10 + V;
+  switch (key) {
+    case 11: e = occupancy<1, 1>(block, &per_sm); break;
+    case 12: e = occupancy<1, 2>(block, &per_sm); break;
+    case 21: e = occupancy<2, 1>(block, &per_sm); break;
+    case 22: e = occupancy<2, 2>(block, &per_sm); break;
+    case 41: e = occupancy<4, 1>(block, &per_sm); break;
+    case 42: e = occupancy<4, 2>(block, &per_sm); break;
+    case 81: e = occupancy<8, 1>(block, &per_sm); break;
+    case 82: e = occupancy<8, 2>(block, &per_sm); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  *max_blocks = per_sm * sms;
+  return cudaSuccess;
+}
+
+cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st) {
+  BlockArgs copy = a;
+  void* args[] = {&copy};
+  count_launch();
+  const int key = a.QT * 10 + a.vec;
+  const void* fn = nullptr;
+  switch (key) {
+    case 11: fn = (const void*)k_phimv_block<1, 1>; break;
+    case 12: fn = (const void*)k_phimv_block<1, 2>; break;
+    case 21: fn = (const void*)k_phimv_block<2, 1>; break;
+    case 22: fn = (const void*)k_phimv_block<2, 2>; break;
+    case 41: fn = (const void*)k_phimv_block<4, 1>; break;
+    case 42: fn = (const void*)k_phimv_block<4, 2>; break;
+    case 81: fn = (const void*)k_phimv_block<8, 1>; break;
+    case 82: fn = (const void*)k_phimv_block<8, 2>; break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
+}
+
+}  // namespace phx

@@ -596,21 +596,26 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
     for (int32_t d = 1; d <= p; ++d) cc[d] = (cc[d - 1] * kexp) / double(d);
   }
 
-  // layouts
-  const int32_t GS = int32_t(std::min<int64_t>(32, pow2ceil(w)));
-  const int32_t QS = (w + GS - 1) / GS;
-  const int32_t GF = int32_t(std::min<int64_t>(32, pow2ceil(fcols)));
-  const int32_t QF = (fcols + GF - 1) / GF;
+  // layouts: V adjacent columns per lane (double2 when both widths are even),
+  // G = lanes per row (pow2 <= 32), Q = column chunks per lane
+  const int32_t V = (w % 2 == 0 && fcols % 2 == 0) ? 2 : 1;
+  const int32_t GS = int32_t(std::min<int64_t>(32, pow2ceil((w + V - 1) / V)));
+  const int32_t QS = (w + V * GS - 1) / (V * GS);
+  const int32_t GF = int32_t(std::min<int64_t>(32, pow2ceil((fcols + V - 1) / V)));
+  const int32_t QF = (fcols + V * GF - 1) / (V * GF);
   const int32_t QT = int32_t(pow2ceil(std::max(QS, QF)));
   if (QT > 8)
-    throw_phx(PHX_EINVAL, std::string(who) + ": block width (p+1)*r above 256 is not supported");
+    throw_phx(PHX_EINVAL, std::string(who) + ": block width (p+1)*r above " +
+                              std::to_string(256 * V) + " is not supported");
   const int block = 256;
   // rows per CTA tile: 8 warps x the larger warp tile (kernel: (32/G) * R rows,
-  // R = 2 rows per lane group when QT == 1)
-  const int32_t tile = 8 * (32 / std::min(GS, GF)) * (QT == 1 ? 2 : 1);
+  // R = 2 rows per lane group when QT == 1 and V == 1)
+  const int32_t tile = 8 * (32 / std::min(GS, GF)) * ((QT == 1 && V == 1) ? 2 : 1);
 
   // workspace
   const int32_t ldb = w, ldf = fcols;
+  if (uint64_t(n) * uint64_t(ldb) >= (uint64_t(1) << 32))
+    throw_phx(PHX_EINVAL, std::string(who) + ": n*(p+1)*r >= 2^32 block entries exceeds one device");
   const size_t nb = size_t(n) * size_t(ldb), nf = size_t(n) * size_t(ldf);
   phx::BlockArgs a{};
   a.n = int32_t(n);
@@ -626,6 +631,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.GF = GF;
   a.QF = QF;
   a.QT = QT;
+  a.vec = V;
   a.tile = tile;
   a.xi = xi;
   a.tol = tol;
@@ -680,7 +686,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), st));
 
   int max_blocks = 0;
-  PHX_CUDA(phx::coop_grid_size(QT, block, &max_blocks));
+  PHX_CUDA(phx::coop_grid_size(QT, V, block, &max_blocks));
   const int64_t ntiles = (n + tile - 1) / tile;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(max_blocks, ntiles)));
   PHX_CUDA(cudaEventRecord(op->ev0, st));
