@@ -25,7 +25,6 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int kWCap = 256;  // staged CSR entries per warp tile
 constexpr int kMaxRW = 64;  // rows per warp tile
 
 __device__ __forceinline__ unsigned long long abs_bits(double x) {
@@ -40,10 +39,15 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsig
 
 template <int V>
 struct Vio;
+// ld/st: default caching (gather sources and their producers);
+// ldcs/stcs: evict-first streaming hints for the read-once / write-once
+// accumulator streams (Vw, S, E), so L2 keeps the gather targets
 template <>
 struct Vio<1> {
   __device__ __forceinline__ static void ld(const double* p, double (&x)[1]) { x[0] = *p; }
   __device__ __forceinline__ static void st(double* p, const double (&x)[1]) { *p = x[0]; }
+  __device__ __forceinline__ static void ldcs(const double* p, double (&x)[1]) { x[0] = __ldcs(p); }
+  __device__ __forceinline__ static void stcs(double* p, const double (&x)[1]) { __stcs(p, x[0]); }
 };
 template <>
 struct Vio<2> {
@@ -54,6 +58,14 @@ struct Vio<2> {
   }
   __device__ __forceinline__ static void st(double* p, const double (&x)[2]) {
     *reinterpret_cast<double2*>(p) = make_double2(x[0], x[1]);
+  }
+  __device__ __forceinline__ static void ldcs(const double* p, double (&x)[2]) {
+    const double2 t = __ldcs(reinterpret_cast<const double2*>(p));
+    x[0] = t.x;
+    x[1] = t.y;
+  }
+  __device__ __forceinline__ static void stcs(double* p, const double (&x)[2]) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(x[0], x[1]));
   }
 };
 
@@ -95,7 +107,9 @@ __device__ __forceinline__ double group_rowsum(const double (&v)[Q][V], int G, i
   for (int q = 0; q < Q; ++q) {
     double x = v[q][0];
     if (V == 2) x = x + v[q][V - 1];
-    for (int m = 1; m < G; m <<= 1) x = x + __shfl_xor_sync(kFull, x, m);
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1)
+      if (m < G) x = x + __shfl_xor_sync(kFull, x, m);  // G is warp-uniform
     T[q] = x;
   }
 #pragma unroll
@@ -134,40 +148,109 @@ __device__ __forceinline__ void publish2(unsigned long long a, unsigned long lon
   __syncthreads();
 }
 
-// Warp-private staging of one warp tile's CSR slice: row_ptr, then the
-// contiguous entry range as (element offset col*ld, value) pairs.
-struct WarpStage {
-  int rp[kMaxRW + 1];
-  unsigned off[kWCap];
-  double av[kWCap];
+// ---------------------------------------------------------------------------
+// Per-warp cp.async pipeline over the warp's sequence of row tiles.  While
+// tile s is computed, the CSR entries of tile s+1 and the row_ptr slice of
+// tile s+2 are in flight into warp-private shared memory (LDGSTS, no
+// registers held), so the row_ptr -> entries -> gather dependency chain costs
+// one round trip per tile instead of three.
+// ---------------------------------------------------------------------------
+constexpr int kEC = 160;  // staged CSR entries per warp tile
+
+struct WarpPipe {
+  int rp[3][kMaxRW + 1];
+  int ci[2][kEC];
+  double av[2][kEC];
 };
 
-__device__ __forceinline__ bool stage_csr(const BlockArgs& a, int base, int RW, unsigned ld,
-                                          WarpStage& st, int lane, int& e_lo) {
-  __syncwarp();  // every lane is done with the previous tile's slice
-  for (int l = lane; l <= RW; l += 32) st.rp[l] = __ldg(a.rp + min(base + l, a.n));
-  __syncwarp();
-  e_lo = st.rp[0];
-  const int E = st.rp[RW] - e_lo;
-  const bool fits = E <= kWCap;
-  if (fits) {
-    for (int e = lane; e < E; e += 32) {
-      st.off[e] = unsigned(__ldg(a.ci + e_lo + e)) * ld;
-      st.av[e] = __ldg(a.av + e_lo + e);
-    }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// The warp's tiles: within every CTA tile the warp owns warp tiles
+// wt = warp, warp + 8, ... (m of them); CTA tiles t = blockIdx.x + k*grid.
+struct TileSeq {
+  int m, ntiles, tile, RW, warp;
+  __device__ __forceinline__ int base(int s) const {
+    const int t = int(blockIdx.x) + (s / m) * int(gridDim.x);
+    return t < ntiles ? t * tile + (warp + (s % m) * kWarps) * RW : -1;
   }
+};
+
+__device__ __forceinline__ TileSeq make_seq(const BlockArgs& a, const Layout& L, int ntiles,
+                                            int warp) {
+  TileSeq ts;
+  ts.m = a.tile / (L.RW * kWarps);
+  ts.ntiles = ntiles;
+  ts.tile = a.tile;
+  ts.RW = L.RW;
+  ts.warp = warp;
+  return ts;
+}
+
+__device__ __forceinline__ void issue_rp(const BlockArgs& a, int* dst, int base, int RW, int lane) {
+  for (int l = lane; l <= RW; l += 32) cp_async4(dst + l, a.rp + min(base + l, a.n));
+}
+
+__device__ __forceinline__ void issue_entries(const BlockArgs& a, const int* rp, int RW, int* ci,
+                                              double* av, int lane) {
+  const int e_lo = rp[0], E = rp[RW] - e_lo;
+  if (E <= kEC)
+    for (int e = lane; e < E; e += 32) {
+      cp_async4(ci + e, a.ci + e_lo + e);
+      cp_async8(av + e, a.av + e_lo + e);
+    }
+}
+
+// body(base, rp, ci, av): rp = row_ptr[base .. base+RW] (clamped at n); when
+// rp[RW] - rp[0] <= kEC, ci/av hold the tile's entries from index 0.
+template <class Body>
+__device__ __forceinline__ void pipelined(const BlockArgs& a, const TileSeq& ts, WarpPipe& pp,
+                                          int lane, Body&& body) {
+  const int b0 = ts.base(0);
+  if (b0 < 0) return;  // warp-uniform
   __syncwarp();
-  return fits;
+  issue_rp(a, pp.rp[0], b0, ts.RW, lane);
+  cp_commit();
+  cp_wait_all();
+  __syncwarp();
+  issue_entries(a, pp.rp[0], ts.RW, pp.ci[0], pp.av[0], lane);
+  const int b1 = ts.base(1);
+  if (b1 >= 0) issue_rp(a, pp.rp[1], b1, ts.RW, lane);
+  cp_commit();
+  int base = b0;
+  for (int s = 0; base >= 0; ++s) {
+    cp_wait_all();
+    __syncwarp();  // tile s's entries and tile s+1's row_ptr have landed
+    const int nb = ts.base(s + 1);
+    if (nb >= 0) {
+      issue_entries(a, pp.rp[(s + 1) % 3], ts.RW, pp.ci[(s + 1) & 1], pp.av[(s + 1) & 1], lane);
+      const int nnb = ts.base(s + 2);
+      if (nnb >= 0) issue_rp(a, pp.rp[(s + 2) % 3], nnb, ts.RW, lane);
+    }
+    cp_commit();
+    body(base, pp.rp[s % 3], pp.ci[s & 1], pp.av[s & 1]);
+    __syncwarp();  // done with slot s before it is refilled
+    base = nb;
+  }
 }
 
 // acc[rr][q][e] = sum over row rr's entries (storage order, from +0) of
 // av * X[col*ld + c].  X was written before the last grid.sync(), which
 // invalidates L1 (CCTL.IVALL), so plain cached loads are coherent.
 template <int Q, int V, int R, int B, bool SMEM>
-__device__ __forceinline__ void gather(const BlockArgs& a, const WarpStage& st, int e_lo,
-                                       unsigned ld, const int (&rs)[R], const int (&cnt)[R],
-                                       const double* X, const unsigned (&cq)[Q],
-                                       const bool (&vq)[Q], double (&acc)[R][Q][V]) {
+__device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const double* av_s,
+                                       int e_lo, unsigned ld, const int (&rs)[R],
+                                       const int (&cnt)[R], const double* X,
+                                       const unsigned (&cq)[Q], const bool (&vq)[Q],
+                                       double (&acc)[R][Q][V]) {
   int maxc = 0;
 #pragma unroll
   for (int rr = 0; rr < R; ++rr) maxc = max(maxc, cnt[rr]);
@@ -181,7 +264,7 @@ __device__ __forceinline__ void gather(const BlockArgs& a, const WarpStage& st, 
         unsigned off = 0;
         if (ok) {
           const int e = rs[rr] + u0 + u;
-          off = SMEM ? st.off[e] : unsigned(__ldg(a.ci + e_lo + e)) * ld;
+          off = unsigned(SMEM ? ci[e] : __ldg(a.ci + e_lo + e)) * ld;
         }
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -199,7 +282,7 @@ __device__ __forceinline__ void gather(const BlockArgs& a, const WarpStage& st, 
       for (int rr = 0; rr < R; ++rr)
         if (u0 + u < cnt[rr]) {
           const int e = rs[rr] + u0 + u;
-          const double av = SMEM ? st.av[e] : __ldg(a.av + e_lo + e);
+          const double av = SMEM ? av_s[e] : __ldg(a.av + e_lo + e);
 #pragma unroll
           for (int q = 0; q < Q; ++q)
 #pragma unroll
@@ -209,15 +292,22 @@ __device__ __forceinline__ void gather(const BlockArgs& a, const WarpStage& st, 
 }
 
 template <int Q, int V, int R, int B>
-__device__ __forceinline__ void gather_tile(const BlockArgs& a, const WarpStage& st, bool fits,
-                                            int e_lo, unsigned ld, const int (&rs)[R],
-                                            const int (&cnt)[R], const double* X,
-                                            const unsigned (&cq)[Q], const bool (&vq)[Q],
-                                            double (&acc)[R][Q][V]) {
-  if (fits)
-    gather<Q, V, R, B, true>(a, st, e_lo, ld, rs, cnt, X, cq, vq, acc);
+__device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L, const int* rp,
+                                            const int* ci, const double* av, unsigned ld,
+                                            const double* X, const unsigned (&cq)[Q],
+                                            const bool (&vq)[Q], double (&acc)[R][Q][V]) {
+  const int e_lo = rp[0];
+  int rs[R], cnt[R];
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) {
+    const int li = rr * L.gpw + L.g;
+    rs[rr] = rp[li] - e_lo;
+    cnt[rr] = rp[li + 1] - rp[li];
+  }
+  if (rp[L.RW] - e_lo <= kEC)
+    gather<Q, V, R, B, true>(a, ci, av, e_lo, ld, rs, cnt, X, cq, vq, acc);
   else
-    gather<Q, V, R, B, false>(a, st, e_lo, ld, rs, cnt, X, cq, vq, acc);
+    gather<Q, V, R, B, false>(a, ci, av, e_lo, ld, rs, cnt, X, cq, vq, acc);
 }
 
 template <int Q, int V>
@@ -227,10 +317,10 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
   constexpr int B = Cfg<Q, V>::B;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long red[2][kWarps];
-  __shared__ WarpStage stage[kWarps];
+  __shared__ WarpPipe pipe[kWarps];
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpStage& st = stage[warp];
+  WarpPipe& pp = pipe[warp];
 
   const int n = a.n, r = a.r, p = a.p;
   const unsigned ldb = unsigned(a.ldb), ldf = unsigned(a.ldf);
@@ -361,9 +451,8 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
           ka[q][e] = v[q] ? __ldg(a.colKa + cc) : 0.0;
           tos[q][e] = v[q] ? __ldg(a.colTos + cc) : 0.0;
         }
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
-        for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
-          const int base = t * a.tile + wt * LS.RW;
+      pipelined(a, make_seq(a, LS, ntiles, warp), pp, lane,
+                [&](int base, const int* rp, const int* ci, const double* avs) {
           // row-local streams first (independent of the CSR slice)
           double vw[R][Q][V], vwl[R][Q][V], so[R][Q][V], ds[R][Q][V], acc[R][Q][V];
           bool vq[R][Q];
@@ -380,8 +469,8 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
                 acc[rr][q][e] = 0.0;
               }
               if (vq[rr][q]) {
-                Vio<V>::ld(a.Vw + o, vw[rr][q]);
-                Vio<V>::ld(a.S + o, so[rr][q]);
+                Vio<V>::ldcs(a.Vw + o, vw[rr][q]);
+                Vio<V>::ldcs(a.S + o, so[rr][q]);
                 if (has_xi) Vio<V>::ld(Dc + o, ds[rr][q]);
                 if (vwl_vec) {
                   if (jj[q][0] >= 2) Vio<V>::ld(a.Vw + (o - unsigned(r)), vwl[rr][q]);
@@ -393,16 +482,7 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
               }
             }
           }
-          int e_lo;
-          const bool fits = stage_csr(a, base, LS.RW, ldb, st, lane, e_lo);
-          int rs[R], cnt[R];
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr) {
-            const int li = rr * LS.gpw + LS.g;
-            rs[rr] = st.rp[li] - e_lo;
-            cnt[rr] = st.rp[li + 1] - st.rp[li];
-          }
-          gather_tile<Q, V, R, B>(a, st, fits, e_lo, ldb, rs, cnt, Dc, c, v, acc);
+          gather_tile<Q, V, R, B>(a, LS, rp, ci, avs, ldb, Dc, c, v, acc);
           double vn[R][Q][V], dn[R][Q][V], sn[R][Q][V];
 #pragma unroll
           for (int rr = 0; rr < R; ++rr)
@@ -431,9 +511,9 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
             for (int q = 0; q < Q; ++q) {
               if (vq[rr][q]) {
                 const unsigned o = unsigned(row) * ldb + c[q];
-                Vio<V>::st(a.Vw + o, vn[rr][q]);
+                Vio<V>::stcs(a.Vw + o, vn[rr][q]);
                 Vio<V>::st(Dn + o, dn[rr][q]);
-                Vio<V>::st(a.S + o, sn[rr][q]);
+                Vio<V>::stcs(a.S + o, sn[rr][q]);
               }
 #pragma unroll
               for (int e = 0; e < V; ++e) {
@@ -448,7 +528,7 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
               msb = umax64(msb, abs_bits(rsm));
             }
           }
-        }
+                });
     }
     double maxD, maxS;
     sync_step(mdb, msb, maxD, maxS);
@@ -482,9 +562,8 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
     cols(LF, c, v);
 #pragma unroll
     for (int q = 0; q < Q; ++q) vl[q] = v[q] && int(c[q]) < r;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
-      for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
-        const int base = t * a.tile + wt * LF.RW;
+    pipelined(a, make_seq(a, LF, ntiles, warp), pp, lane,
+              [&](int base, const int* rp, const int* ci, const double* avs) {
         double acc[R][Q][V];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr)
@@ -492,19 +571,10 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
           for (int q = 0; q < Q; ++q)
 #pragma unroll
             for (int e = 0; e < V; ++e) acc[rr][q][e] = 0.0;
-        int e_lo;
-        const bool fits = stage_csr(a, base, LF.RW, ldb, st, lane, e_lo);
-        int rs[R], cnt[R];
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) {
-          const int li = rr * LF.gpw + LF.g;
-          rs[rr] = st.rp[li] - e_lo;
-          cnt[rr] = st.rp[li + 1] - st.rp[li];
-        }
         // gathers S block-0 columns (left F columns live at the same column
         // index in S); a pair straddling the left/right split gathers one
         // extra column, unused
-        gather_tile<Q, V, R, B>(a, st, fits, e_lo, ldb, rs, cnt, a.S, c, vl, acc);
+        gather_tile<Q, V, R, B>(a, LF, rp, ci, avs, ldb, a.S, c, vl, acc);
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
           const int row = base + rr * LF.gpw + LF.g;
@@ -551,7 +621,7 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
             if (rv) mf = umax64(mf, abs_bits(rf));
           }
         }
-      }
+              });
   }
   if (!sweeps) {
     finish(kStOk, 0, L_S, 1);
@@ -588,9 +658,8 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
             const int i = cc < r ? cc : cc - r;
             tosF[q][e] = v[q] ? __ldg(a.colTos + i) : 0.0;
           }
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
-          for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
-            const int base = t * a.tile + wt * LF.RW;
+        pipelined(a, make_seq(a, LF, ntiles, warp), pp, lane,
+                  [&](int base, const int* rp, const int* ci, const double* avs) {
             double eo[R][Q][V], fs[R][Q][V], acc[R][Q][V];
             bool vq[R][Q];
 #pragma unroll
@@ -603,21 +672,12 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
 #pragma unroll
                 for (int e = 0; e < V; ++e) eo[rr][q][e] = fs[rr][q][e] = acc[rr][q][e] = 0.0;
                 if (vq[rr][q]) {
-                  Vio<V>::ld(a.E + o, eo[rr][q]);
+                  Vio<V>::ldcs(a.E + o, eo[rr][q]);
                   if (has_xi) Vio<V>::ld(Fc + o, fs[rr][q]);
                 }
               }
             }
-            int e_lo;
-            const bool fits = stage_csr(a, base, LF.RW, ldf, st, lane, e_lo);
-            int rs[R], cnt[R];
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-              const int li = rr * LF.gpw + LF.g;
-              rs[rr] = st.rp[li] - e_lo;
-              cnt[rr] = st.rp[li + 1] - st.rp[li];
-            }
-            gather_tile<Q, V, R, B>(a, st, fits, e_lo, ldf, rs, cnt, Fc, c, v, acc);
+            gather_tile<Q, V, R, B>(a, LF, rp, ci, avs, ldf, Fc, c, v, acc);
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
               const int row = base + rr * LF.gpw + LF.g;
@@ -642,7 +702,7 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
                 if (vq[rr][q]) {
                   const unsigned o = unsigned(row) * ldf + c[q];
                   Vio<V>::st(Fn + o, y[q]);
-                  Vio<V>::st(a.E + o, en[q]);
+                  Vio<V>::stcs(a.E + o, en[q]);
                 }
               }
               const double ry = group_rowsum<Q, V>(ay, LF.G, LF.qp);
@@ -652,7 +712,7 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
                 meb = umax64(meb, abs_bits(re));
               }
             }
-          }
+                  });
       }
       double maxF2, maxE;
       sync_step(mfb, meb, maxF2, maxE);
