@@ -72,7 +72,7 @@ struct Vio<2> {
 template <int Q, int V>
 struct Cfg {
   static constexpr int R = (Q == 1 && V == 1) ? 2 : 1;  // rows per lane group per warp tile
-  static constexpr int B = (Q * V <= 2) ? 4 : 2;        // gather batch (entries in flight)
+  static constexpr int B = (Q == 1 && V == 2) ? 8 : ((Q * V <= 2) ? 4 : 2);  // gather batch
 };
 
 // Lane-group layout of one phase (S width or F width).
