@@ -1,0 +1,247 @@
+// phx/phiact.hpp — the reference's C++ interface for the hot path, restored
+// on top of the C ABI of libphx.so (include/phx.h).
+//
+// A caller of the reference (arXiv 2509.26475 "phiact", proj/include/phiact)
+// switches by including this header instead of phiact/params.hpp +
+// phiact/phi_block.hpp + phiact/phi_single.hpp and linking libphx.so:
+//
+//   reference                                  here
+//   phiact::LinearOperator (linop.hpp:19-37)   phiact::LinearOperator built by
+//                                              phiact::csr_operator(...)
+//   phiact::ScalingShift (params.hpp:34-41)    same fields
+//   phiact::select_parameters (params.hpp:75)  same signature
+//   phiact::BlockPhiRequest / BlockPhiResult   same fields (Matrix/Vector are
+//     (phi_block.hpp:14-25)                    the small column-major types below)
+//   phiact::phimv_block (phi_block.hpp:30)     same signature
+//   phiact::PhiRequest/PhiResult/phimv         same
+//   phiact::RunRecord (phi_single.hpp:16-21)   same fields
+//   exceptions std::invalid_argument / std::runtime_error / std::logic_error
+//
+// Differences: the operator is a CSR matrix held on the device (the
+// reference's ApplyFn is an opaque host callback that cannot run on a GPU);
+// Matrix/Vector are minimal column-major containers instead of Eigen types
+// (Eigen is not required).  Header-only.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <initializer_list>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../phx.h"
+
+namespace phiact {
+
+using Index = std::int64_t;
+
+// Column-major dense block (the reference's Eigen::MatrixXd layout).
+class Matrix {
+ public:
+  Matrix() = default;
+  Matrix(Index rows, Index cols) : rows_(rows), cols_(cols), a_(size_t(rows * cols), 0.0) {}
+  Index rows() const { return rows_; }
+  Index cols() const { return cols_; }
+  double& operator()(Index i, Index j) { return a_[size_t(i + j * rows_)]; }
+  double operator()(Index i, Index j) const { return a_[size_t(i + j * rows_)]; }
+  double* data() { return a_.data(); }
+  const double* data() const { return a_.data(); }
+  double* col(Index j) { return a_.data() + j * rows_; }
+  const double* col(Index j) const { return a_.data() + j * rows_; }
+
+ private:
+  Index rows_ = 0, cols_ = 0;
+  std::vector<double> a_;
+};
+
+class Vector {
+ public:
+  Vector() = default;
+  explicit Vector(Index n, double v = 0.0) : a_(size_t(n), v) {}
+  Vector(std::initializer_list<double> l) : a_(l) {}
+  Index size() const { return Index(a_.size()); }
+  double& operator()(Index i) { return a_[size_t(i)]; }
+  double operator()(Index i) const { return a_[size_t(i)]; }
+  double* data() { return a_.data(); }
+  const double* data() const { return a_.data(); }
+
+ private:
+  std::vector<double> a_;
+};
+
+inline constexpr int kDefaultDegree = 61;               // params.hpp:12
+inline constexpr double kDefaultGuardFraction = 0.8;    // params.hpp:13
+inline constexpr double kScalingFloor = 9.5367431640625e-7;  // params.hpp:14
+
+namespace detail {
+[[noreturn]] inline void raise(phx_status st) {
+  const std::string msg = phx_last_error();
+  switch (st) {
+    case PHX_EINVAL: throw std::invalid_argument(msg);
+    case PHX_ENUMERIC: throw std::runtime_error(msg);
+    case PHX_ELOGIC: throw std::logic_error(msg);
+    default: throw std::runtime_error("phx device error: " + msg);
+  }
+}
+inline void check(phx_status st) {
+  if (st != PHX_OK) raise(st);
+}
+}  // namespace detail
+
+// LinearOperator (linop.hpp:19-37) for a device-resident CSR matrix.
+// Immutable after construction; copies share the device handle.
+class LinearOperator {
+ public:
+  LinearOperator() = default;
+  Index dim() const { return h_ ? phx_op_dim(h_.get()) : 0; }
+  const std::string& label() const { return label_; }
+  // A*X (linop.cpp:10-24)
+  Matrix apply(const Matrix& X) const {
+    if (!h_) throw std::logic_error("LinearOperator::apply: operator is empty");
+    if (X.rows() != dim())
+      throw std::invalid_argument("LinearOperator::apply: block has " + std::to_string(X.rows()) +
+                                  " rows, operator dimension is " + std::to_string(dim()));
+    Matrix Y(X.rows(), X.cols());
+    detail::check(phx_apply(h_.get(), X.data(), X.rows(), X.cols(), Y.data(), Y.rows()));
+    return Y;
+  }
+  phx_op handle() const { return h_.get(); }
+
+ private:
+  friend LinearOperator csr_operator(Index, const std::vector<std::int64_t>&,
+                                     const std::vector<std::int32_t>&, const std::vector<double>&,
+                                     std::string, int);
+  std::shared_ptr<phx_op_s> h_;
+  std::string label_;
+};
+
+// CSR factory (the reference's dense_operator analogue, linop.cpp:26-38).
+inline LinearOperator csr_operator(Index n, const std::vector<std::int64_t>& row_ptr,
+                                   const std::vector<std::int32_t>& col_idx,
+                                   const std::vector<double>& vals, std::string label = {},
+                                   int device = -1) {
+  if (Index(row_ptr.size()) != n + 1) throw std::invalid_argument("csr_operator: row_ptr size");
+  phx_op h = nullptr;
+  detail::check(phx_op_create_csr(n, row_ptr.data(), col_idx.data(), vals.data(), device, &h));
+  LinearOperator op;
+  op.h_ = std::shared_ptr<phx_op_s>(h, [](phx_op p) { phx_op_destroy(p); });
+  op.label_ = std::move(label);
+  return op;
+}
+
+// (A - xi I) X (linop.cpp:40-49)
+inline Matrix shifted_apply(const LinearOperator& op, double xi, const Matrix& X) {
+  Matrix Y(X.rows(), X.cols());
+  detail::check(phx_shifted_apply(op.handle(), xi, X.data(), X.rows(), X.cols(), Y.data(), Y.rows()));
+  return Y;
+}
+
+struct ScalingShift {  // params.hpp:34-41
+  double s = 1.0;
+  double xi = 0.0;
+  double s0 = 1.0;
+  double f_min = 0.0;
+  int m = kDefaultDegree;
+  int r = 0;
+};
+
+struct RunRecord {  // phi_single.hpp:16-21
+  long s_effective = 1;
+  int series_len_S = 0;
+  std::vector<int> series_lens_F;
+  long matvecs = 0;
+};
+
+namespace detail {
+inline phx_scaling_shift to_c(const ScalingShift& s) {
+  return phx_scaling_shift{s.s, s.xi, s.s0, s.f_min, s.m, s.r};
+}
+inline ScalingShift from_c(const phx_scaling_shift& c) {
+  return ScalingShift{c.s, c.xi, c.s0, c.f_min, c.m, c.r};
+}
+}  // namespace detail
+
+// select_parameters (params.hpp:75-77)
+inline ScalingShift select_parameters(const LinearOperator& op, int m = kDefaultDegree,
+                                      double tol = -1.0,
+                                      double delta = kDefaultGuardFraction) {
+  phx_scaling_shift out{};
+  detail::check(phx_select_parameters(op.handle(), m, tol, delta, &out));
+  return detail::from_c(out);
+}
+
+struct BlockPhiRequest {  // phi_block.hpp:14-20
+  Vector t;
+  Vector alpha;
+  Matrix V;
+  double tol = -1.0;
+  ScalingShift params;
+};
+
+struct BlockPhiResult {  // phi_block.hpp:22-25
+  Matrix W;
+  RunRecord stats;
+};
+
+// phimv_block (phi_block.hpp:30-31)
+inline BlockPhiResult phimv_block(const LinearOperator& op, const BlockPhiRequest& req) {
+  if (req.t.size() == 0) throw std::invalid_argument("phimv_block: at least one abscissa required");
+  if (req.alpha.size() != req.t.size())
+    throw std::invalid_argument("phimv_block: t and alpha lengths differ");
+  if (req.V.cols() < 1) throw std::invalid_argument("phimv_block: V must have at least one column");
+  if (req.V.rows() != op.dim())
+    throw std::invalid_argument("phimv_block: V row count does not match operator");
+  BlockPhiResult out;
+  out.W = Matrix(req.V.rows(), req.t.size());
+  const phx_scaling_shift ss = detail::to_c(req.params);
+  std::vector<int32_t> lens(1 << 20);
+  phx_run_record rec{0, 0, 0, lens.data(), int64_t(lens.size()), 0};
+  detail::check(phx_phimv_block(op.handle(), int32_t(req.t.size()), req.t.data(), req.alpha.data(),
+                                int32_t(req.V.cols() - 1), req.V.data(), req.V.rows(), req.tol, &ss,
+                                out.W.data(), out.W.rows(), &rec));
+  out.stats.s_effective = rec.s_effective;
+  out.stats.series_len_S = rec.series_len_S;
+  out.stats.series_lens_F.assign(lens.begin(), lens.begin() + std::min<int64_t>(rec.n_sweeps, int64_t(lens.size())));
+  out.stats.matvecs = rec.matvecs;
+  return out;
+}
+
+struct PhiRequest {  // phi_single.hpp:26-32
+  double t = 1.0;
+  double alpha = 1.0;
+  Matrix V;
+  double tol = -1.0;
+  ScalingShift params;
+};
+
+struct PhiResult {  // phi_single.hpp:34-39
+  Vector w;
+  Vector exp_v0;
+  Vector tail;
+  RunRecord stats;
+};
+
+// phimv (phi_single.hpp:44)
+inline PhiResult phimv(const LinearOperator& op, const PhiRequest& req) {
+  const Index n = op.dim();
+  PhiResult out;
+  out.w = Vector(n);
+  out.exp_v0 = Vector(n);
+  out.tail = Vector(n);
+  const phx_scaling_shift ss = detail::to_c(req.params);
+  std::vector<int32_t> lens(1 << 20);
+  phx_run_record rec{0, 0, 0, lens.data(), int64_t(lens.size()), 0};
+  detail::check(phx_phimv(op.handle(), req.t, req.alpha, int32_t(req.V.cols() - 1), req.V.data(),
+                          req.V.rows(), req.tol, &ss, out.w.data(), out.exp_v0.data(),
+                          out.tail.data(), &rec));
+  out.stats.s_effective = rec.s_effective;
+  out.stats.series_len_S = rec.series_len_S;
+  out.stats.series_lens_F.assign(lens.begin(), lens.begin() + std::min<int64_t>(rec.n_sweeps, int64_t(lens.size())));
+  out.stats.matvecs = rec.matvecs;
+  return out;
+}
+
+}  // namespace phiact

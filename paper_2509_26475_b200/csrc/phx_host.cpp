@@ -659,7 +659,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.W = in.dW ? in.dW : op->W.as<double>(size_t(n) * size_t(r));
   a.FLo = in.h_exp_v0 ? op->FLo.as<double>(size_t(n) * size_t(r)) : nullptr;
   a.FRo = in.h_tail ? op->FRo.as<double>(size_t(n) * size_t(r)) : nullptr;
-  a.slots = op->slots.as<unsigned long long>(6);
+  a.slots = op->slots.as<unsigned long long>(6);  // [3][maxA, maxB]
   a.status = op->status.as<int32_t>(8);
   a.lensF = op->lensF.as<int32_t>(size_t(std::max<long>(1, s_eff - 1)));
   int64_t trace_cap;

@@ -1,0 +1,31 @@
+"""The C++ drop-in header (include/phx/phiact.hpp): a reference-style C++
+program compiles against it and libphx.so (CPU), and runs on the GPU."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "cpp", "test_phiact_api.cpp")
+LIBDIR = os.path.join(ROOT, "paper_2509_26475_b200", "lib")
+
+
+def build(tmp_path):
+    exe = str(tmp_path / "test_phiact_api")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+                    SRC, "-L", LIBDIR, "-lphx", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+    return exe
+
+
+def test_cpp_header_compiles_and_links(tmp_path):
+    assert os.path.exists(build(tmp_path))
+
+
+@pytest.mark.gpu
+def test_cpp_api_runs(tmp_path):
+    exe = build(tmp_path)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "invalid_argument: phimv_block: at least one abscissa required" in out.stdout
+    assert "runtime_error: phimv_block: shift undo factor" in out.stdout
