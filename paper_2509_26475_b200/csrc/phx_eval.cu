@@ -26,6 +26,7 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kMaxRW = 64;  // rows per warp tile
+constexpr double DBL_MAX_D = 1.7976931348623157e308;
 
 __device__ __forceinline__ unsigned long long abs_bits(double x) {
   return static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFull;
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
   };
 
   // ================= init: Vw = V[src]*g, D = S = Vw (phi_block.cpp:76-92)
-  unsigned long long m0 = 0;
+  unsigned long long m0 = 0, mv = 0;  // max |Vw| row sum; max |V| entry (finiteness)
   {
     unsigned c[Q];
     bool v[Q];
@@ -397,7 +398,9 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
                 const int cc = int(c[q]) + e;
                 const int j = cc / r, i = cc - j * r;
                 const int src = j == 0 ? 0 : p + 1 - j;
-                x[q][e] = __ldg(a.V + size_t(src) * size_t(n) + row) * __ldg(a.g + i);
+                const double vraw = __ldg(a.V + size_t(src) * size_t(n) + row);
+                mv = umax64(mv, abs_bits(vraw));
+                x[q][e] = vraw * __ldg(a.g + i);
               }
               ax[q][e] = fabs(x[q][e]);
             }
@@ -414,8 +417,12 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
       }
   }
   double mD, mSn;
-  sync_step(m0, m0, mD, mSn);
-  double c1 = INF, c2 = mD, nS = mSn;  // c2 = inf_norm(D), ||S|| at k = 1
+  sync_step(m0, mv, mD, mSn);
+  if (!(mSn <= DBL_MAX_D)) {  // a non-finite entry of V (check_request, phi_block.cpp:25-26)
+    finish(kStInputNonFinite, 0, 1, 0);
+    return;
+  }
+  double c1 = INF, c2 = mD, nS = mD;  // c2 = inf_norm(D) = ||S|| at k = 1 (S = D = Vw)
   trace(0.0, c2, nS);
 
   // ================= S series (phi_block.cpp:93-106)

@@ -548,16 +548,29 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   for (int32_t i = 0; i < r; ++i) tmax = std::max(tmax, std::fabs(in.t[i]));
   const double prod = in.single ? std::fabs(in.t[0]) * in.params.s : in.params.s * tmax;
   const double sc = std::ceil(prod);
-  if (!(sc < 2147483647.0))
+  // check_request runs before these errors in the reference: a host V is
+  // re-checked here (error path only) to keep that precedence
+  auto v_first = [&]() {
+    if (!in.hV) return;
+    for (int32_t j = 0; j <= p; ++j)
+      if (!finite_all(in.hV + size_t(j) * size_t(in.ldv), size_t(n)))
+        throw_phx(PHX_EINVAL, in.single ? "phimv: V has non-finite entries"
+                                        : "phimv_block: inputs must be finite");
+  };
+  if (!(sc < 2147483647.0)) {
+    v_first();
     throw_phx(PHX_EINVAL, std::string(who) + ": s_eff = ceil(s*max|t|) exceeds the supported range");
+  }
   const long s_eff = std::max<long>(1, long(sc));  // :58-59
 
   std::vector<double> mu(static_cast<size_t>(r)), g(static_cast<size_t>(r));
   for (int32_t i = 0; i < r; ++i) {
     mu[size_t(i)] = in.single ? std::exp(in.t[i] * xi / double(s_eff))
                               : std::exp(xi * in.t[i] / double(s_eff));
-    if (!std::isfinite(mu[size_t(i)]))
+    if (!std::isfinite(mu[size_t(i)])) {
+      v_first();
       throw_phx(PHX_ENUMERIC, std::string(who) + ": shift undo factor e^{t xi / s} overflows");
+    }
     g[size_t(i)] = mu[size_t(i)] / double(s_eff);
   }
   const int32_t w = (p + 1) * r;
@@ -727,6 +740,9 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   const int32_t code = h_status[0];
   const int32_t idx = h_status[1];
   const int32_t L_S = h_status[2];
+  if (code == phx::kStInputNonFinite)
+    throw_phx(PHX_EINVAL, in.single ? "phimv: V has non-finite entries"
+                                    : "phimv_block: inputs must be finite");
   if (code == phx::kStSeriesCap)
     throw_phx(PHX_ENUMERIC, std::string(who) + ": series did not converge within 500 terms");
   if (code == phx::kStSeriesDiverged)
@@ -758,10 +774,11 @@ void check_block_request(phx_op op, int32_t r, const double* t, const double* al
   if (!t || !alpha) throw_phx(PHX_EINVAL, "phimv_block: t and alpha lengths differ");
   if (p < 0) throw_phx(PHX_EINVAL, "phimv_block: V must have at least one column");
   if (host_v && ldv < op->n) throw_phx(PHX_EINVAL, "phimv_block: V row count does not match operator");
-  bool fin = finite_all(t, size_t(r)) && finite_all(alpha, size_t(r));
-  if (host_v && fin)
-    for (int32_t j = 0; j <= p && fin; ++j) fin = finite_all(V + size_t(j) * size_t(ldv), size_t(op->n));
-  if (!fin) throw_phx(PHX_EINVAL, "phimv_block: inputs must be finite");
+  // V's finiteness is checked on the device, in the evaluator's first pass
+  // over V (kStInputNonFinite); t and alpha here
+  (void)V;
+  if (!(finite_all(t, size_t(r)) && finite_all(alpha, size_t(r))))
+    throw_phx(PHX_EINVAL, "phimv_block: inputs must be finite");
 }
 
 }  // namespace

@@ -68,6 +68,7 @@ enum : int32_t {
   kStSeriesDiverged = 2,
   kStRecoveryCap = 3,
   kStRecoveryDiverged = 4,
+  kStInputNonFinite = 5,  // V has a non-finite entry (detected in the init pass)
 };
 
 // launch wrappers (phx_kernels.cu)
