@@ -70,10 +70,13 @@ struct Vio<2> {
   }
 };
 
-template <int Q, int V>
+template <int Q, int V, int R_>
 struct Cfg {
-  static constexpr int R = (Q == 1 && V == 1) ? 2 : 1;  // rows per lane group per warp tile
-  static constexpr int B = (Q == 1 && V == 2) ? 8 : ((Q * V <= 2) ? 4 : 2);  // gather batch
+  static constexpr int R = R_;  // rows per lane group per warp tile
+  // gather batch: entries in flight per lane group
+  static constexpr int B = (Q == 1 && V == 2 && R_ == 1) ? 8 : ((Q * V * R_ <= 4) ? 4 : 2);
+  // resident CTAs per SM the register budget is sized for
+  static constexpr int MINB = (Q * V * R_ <= 2) ? 4 : ((Q * V * R_ <= 4) ? 3 : ((Q * V <= 4) ? 2 : 1));
 };
 
 // Lane-group layout of one phase (S width or F width).
@@ -311,11 +314,10 @@ __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L,
     gather<Q, V, R, B, false>(a, ci, av, e_lo, ld, rs, cnt, X, cq, vq, acc);
 }
 
-template <int Q, int V>
-__global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 : 1))
-    k_phimv_block(BlockArgs a) {
-  constexpr int R = Cfg<Q, V>::R;
-  constexpr int B = Cfg<Q, V>::B;
+template <int Q, int V, int RR>
+__global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs a) {
+  constexpr int R = Cfg<Q, V, RR>::R;
+  constexpr int B = Cfg<Q, V, RR>::B;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long red[2][kWarps];
   __shared__ WarpPipe pipe[kWarps];
@@ -844,33 +846,53 @@ __global__ void __launch_bounds__(kBlock, (Q * V <= 2) ? 4 : ((Q * V <= 4) ? 2 :
   finish(err, err_idx, L_S, 0);
 }
 
-template <int Q, int V>
+template <int Q, int V, int R>
 cudaError_t occupancy(int block, int* per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_phimv_block<Q, V>, block, 0);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_phimv_block<Q, V, R>, block, 0);
+}
+
+template <int Q, int V, int R>
+const void* kernel_ptr() {
+  return reinterpret_cast<const void*>(k_phimv_block<Q, V, R>);
+}
+
+// instantiated variants: (Q, V, R) with R = 2 only for single-chunk rows
+const void* select_kernel(int QT, int V, int R, cudaError_t (**occ)(int, int*)) {
+  const int key = QT * 100 + V * 10 + R;
+  switch (key) {
+#define PHX_CASE(q, v, r)          \
+  case q * 100 + v * 10 + r:       \
+    *occ = occupancy<q, v, r>;     \
+    return kernel_ptr<q, v, r>();
+    PHX_CASE(1, 1, 1)
+    PHX_CASE(1, 1, 2)
+    PHX_CASE(1, 2, 1)
+    PHX_CASE(1, 2, 2)
+    PHX_CASE(2, 1, 1)
+    PHX_CASE(2, 2, 1)
+    PHX_CASE(4, 1, 1)
+    PHX_CASE(4, 2, 1)
+    PHX_CASE(8, 1, 1)
+    PHX_CASE(8, 2, 1)
+#undef PHX_CASE
+    default:
+      return nullptr;
+  }
 }
 
 }  // namespace
 
-cudaError_t coop_grid_size(int QT, int V, int block, int* max_blocks) {
+cudaError_t coop_grid_size(int QT, int V, int R, int block, int* max_blocks) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   int sms = 0;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
+  cudaError_t (*occ)(int, int*) = nullptr;
+  if (!select_kernel(QT, V, R, &occ)) return cudaErrorInvalidValue;
   int per_sm = 0;
-  const int key = QT * 10 + V;
-  switch (key) {
-    case 11: e = occupancy<1, 1>(block, &per_sm); break;
-    case 12: e = occupancy<1, 2>(block, &per_sm); break;
-    case 21: e = occupancy<2, 1>(block, &per_sm); break;
-    case 22: e = occupancy<2, 2>(block, &per_sm); break;
-    case 41: e = occupancy<4, 1>(block, &per_sm); break;
-    case 42: e = occupancy<4, 2>(block, &per_sm); break;
-    case 81: e = occupancy<8, 1>(block, &per_sm); break;
-    case 82: e = occupancy<8, 2>(block, &per_sm); break;
-    default: return cudaErrorInvalidValue;
-  }
+  e = occ(block, &per_sm);
   if (e != cudaSuccess) return e;
   *max_blocks = per_sm * sms;
   return cudaSuccess;
@@ -879,20 +901,10 @@ cudaError_t coop_grid_size(int QT, int V, int block, int* max_blocks) {
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st) {
   BlockArgs copy = a;
   void* args[] = {&copy};
+  cudaError_t (*occ)(int, int*) = nullptr;
+  const void* fn = select_kernel(a.QT, a.vec, a.R, &occ);
+  if (!fn) return cudaErrorInvalidValue;
   count_launch();
-  const int key = a.QT * 10 + a.vec;
-  const void* fn = nullptr;
-  switch (key) {
-    case 11: fn = (const void*)k_phimv_block<1, 1>; break;
-    case 12: fn = (const void*)k_phimv_block<1, 2>; break;
-    case 21: fn = (const void*)k_phimv_block<2, 1>; break;
-    case 22: fn = (const void*)k_phimv_block<2, 2>; break;
-    case 41: fn = (const void*)k_phimv_block<4, 1>; break;
-    case 42: fn = (const void*)k_phimv_block<4, 2>; break;
-    case 81: fn = (const void*)k_phimv_block<8, 1>; break;
-    case 82: fn = (const void*)k_phimv_block<8, 2>; break;
-    default: return cudaErrorInvalidValue;
-  }
   return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
 }
 

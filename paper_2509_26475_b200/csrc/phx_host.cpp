@@ -623,7 +623,11 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   const int block = 256;
   // rows per CTA tile: 8 warps x the larger warp tile (kernel: (32/G) * R rows,
   // R = 2 rows per lane group when QT == 1 and V == 1)
-  const int32_t tile = 8 * (32 / std::min(GS, GF)) * ((QT == 1 && V == 1) ? 2 : 1);
+  // R rows per lane group: 2 for short rows (the per-tile pipeline overhead
+  // dominates) or scalar lanes, else 1 (more resident warps)
+  const double avg_nnz = double(op->nnz) / double(n);
+  const int32_t R = (QT == 1 && (V == 1 || avg_nnz < 2.5)) ? 2 : 1;
+  const int32_t tile = 8 * (32 / std::min(GS, GF)) * R;
 
   // workspace
   const int32_t ldb = w, ldf = fcols;
@@ -645,6 +649,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.QF = QF;
   a.QT = QT;
   a.vec = V;
+  a.R = R;
   a.tile = tile;
   a.xi = xi;
   a.tol = tol;
@@ -699,7 +704,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), st));
 
   int max_blocks = 0;
-  PHX_CUDA(phx::coop_grid_size(QT, V, block, &max_blocks));
+  PHX_CUDA(phx::coop_grid_size(QT, V, R, block, &max_blocks));
   const int64_t ntiles = (n + tile - 1) / tile;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(max_blocks, ntiles)));
   PHX_CUDA(cudaEventRecord(op->ev0, st));

@@ -24,6 +24,7 @@ struct BlockArgs {
   int32_t GF, QF;  // F-layout
   int32_t QT;      // template width: pow2 >= max(QS, QF), in {1,2,4,8}
   int32_t vec;     // adjacent columns per lane (2 when both widths are even)
+  int32_t R;       // rows per lane group per warp tile (1 or 2; 2 only when QT == 1)
   int32_t tile;    // rows per tile (row -> CTA mapping, independent of layout)
   // scalars
   double xi, tol;
@@ -73,7 +74,7 @@ enum : int32_t {
 
 // launch wrappers (phx_kernels.cu)
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st);
-cudaError_t coop_grid_size(int QT, int V, int block, int* max_blocks);
+cudaError_t coop_grid_size(int QT, int V, int R, int block, int* max_blocks);
 
 // y = f(A x) with mode 0: A x, 1: A x - fl(xi x), 2: (A x) / div ; fused
 // per-chunk max|y| into chunkmax (bit patterns) when chunkmax != nullptr
