@@ -192,3 +192,55 @@ def test_kernel_actually_runs():
     assert p.kernel_launches() > before
     ms, steps = p.last_eval_stats()
     assert ms > 0 and steps >= 2
+
+
+def _random_sparse(n, k, seed):
+    """n x n CSR with k off-diagonal entries per row + a dominant diagonal."""
+    rng = np.random.default_rng(seed)
+    rp = [0]
+    ci, av = [], []
+    for i in range(n):
+        cols = sorted(set(rng.integers(0, n, size=k).tolist()) | {i})
+        vals = rng.standard_normal(len(cols))
+        vals[cols.index(i)] = -(np.abs(vals).sum() + 2.0)
+        ci += cols
+        av += vals.tolist()
+        rp.append(len(ci))
+    return n, np.array(rp, dtype=np.int64), np.array(ci, dtype=np.int32), np.array(av)
+
+
+@pytest.mark.parametrize("p,r", [(9, 8), (4, 7), (15, 16), (0, 5), (1, 1), (2, 40), (3, 33)])
+def test_block_widths_bitwise(p, r):
+    """Every evaluator variant: V = 1/2 columns per lane, Q = 1..8 column
+    chunks, p = 0 (F width r) and wide F widths, with recovery sweeps."""
+    P_ = P()
+    n, rp, ci, av = _random_sparse(700, 4, 1000 + 17 * p + r)
+    av = av * 25.0  # ||A|| large enough for recovery sweeps
+    op = P_.CsrOperator(n, rp, ci, av)
+    oop = O.csr_from_arrays(n, rp, ci, av)
+    rng = O.Rng(31 + p + r)
+    V = rng.matrix(n, p + 1)
+    t = 0.05 + 0.4 * rng.uniforms(r)
+    alpha = -1.0 + 2.0 * rng.uniforms(r)
+    tol = 1e-12
+    ss = O.select_parameters(oop, 61, tol)
+    ss.s *= 4.0  # force recovery sweeps
+    Wo, ro = O.phimv_block(oop, t, alpha, V, tol, ss)
+    res = P_.phimv_block(op, P_.BlockPhiRequest(t, alpha, V, tol, P_.ScalingShift(*ss.astuple())))
+    assert ro.s_effective > 1
+    assert res.stats.series_len_S == ro.series_len_S
+    assert res.stats.series_lens_F == ro.series_lens_F
+    assert np.array_equal(res.W, Wo)
+
+
+def test_single_variant_with_recovery_bitwise():
+    P_ = P()
+    wl = P_.workload(5, 3000)
+    op = P_.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    oop = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    ss = O.select_parameters(oop, 61, wl.tol)
+    w, e0, tail, rec = O.phimv(oop, 2.0, 0.75, wl.V, wl.tol, ss)
+    res = P_.phimv(op, P_.PhiRequest(2.0, 0.75, wl.V, wl.tol, P_.ScalingShift(*ss.astuple())))
+    assert rec.s_effective > 1
+    assert res.stats.series_lens_F == rec.series_lens_F
+    assert np.array_equal(res.w, w) and np.array_equal(res.exp_v0, e0) and np.array_equal(res.tail, tail)
