@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -706,7 +707,15 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   int max_blocks = 0;
   PHX_CUDA(phx::coop_grid_size(QT, V, R, block, &max_blocks));
   const int64_t ntiles = (n + tile - 1) / tile;
-  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(max_blocks, ntiles)));
+  // developer knob for tuning studies: PHX_GRID_FRAC = fraction (0, 1] of the
+  // co-resident CTA count to launch
+  static const double grid_frac = [] {
+    const char* e = std::getenv("PHX_GRID_FRAC");
+    const double f = e ? std::atof(e) : 1.0;
+    return (f > 0.0 && f <= 1.0) ? f : 1.0;
+  }();
+  const int64_t cap = std::max<int64_t>(1, int64_t(double(max_blocks) * grid_frac));
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(cap, ntiles)));
   PHX_CUDA(cudaEventRecord(op->ev0, st));
   PHX_CUDA(phx::launch_phimv_block(a, grid, block, st));
   PHX_CUDA(cudaEventRecord(op->ev1, st));
