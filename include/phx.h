@@ -85,6 +85,19 @@ typedef struct {
 phx_status phx_op_create_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                              const double* vals, int32_t device, phx_op* out);
 phx_status phx_op_destroy(phx_op op);
+/* Row-partitioned operator: rows split into nparts
+ * contiguous parts, part q resident on devices[q] (NULL or -1: the current
+ * device).  phx_phimv_block on it evaluates every part's rows on its device,
+ * reading other parts' block rows over NVLink peer memory and combining the
+ * per-term stopping norms across parts; the result is bitwise the
+ * unpartitioned one.  Parts that share a device run as one launch (single-GPU
+ * emulation).  Parameter selection and apply need an unpartitioned operator:
+ * select on the whole operator and reuse the ScalingShift.  nparts <= 16,
+ * each part < 2^27 rows. */
+phx_status phx_op_create_csr_partitioned(int64_t n, const int64_t* row_ptr,
+                                         const int32_t* col_idx, const double* vals,
+                                         int32_t nparts, const int32_t* devices, phx_op* out);
+int32_t phx_op_nparts(phx_op op);
 int64_t phx_op_dim(phx_op op);
 int64_t phx_op_nnz(phx_op op);
 /* The CUDA stream (cudaStream_t) every call on this operator runs on; lets a

@@ -69,7 +69,8 @@ _WL = None
 
 # every exported symbol of include/phx.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = (
-    "phx_op_create_csr", "phx_op_destroy", "phx_op_dim", "phx_op_nnz", "phx_op_stream", "phx_apply",
+    "phx_op_create_csr", "phx_op_create_csr_partitioned", "phx_op_nparts", "phx_op_destroy",
+    "phx_op_dim", "phx_op_nnz", "phx_op_stream", "phx_apply",
     "phx_shifted_apply", "phx_select_parameters", "phx_basis_build", "phx_basis_destroy",
     "phx_basis_info", "phx_objective", "phx_minimize_shift", "phx_parameters_for_shift",
     "phx_phimv_block", "phx_phimv_block_device", "phx_phimv", "phx_last_error",
@@ -100,6 +101,10 @@ def lib():
     L.phx_op_nnz.argtypes = [C.c_void_p]
     L.phx_op_create_csr.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int32, C.POINTER(C.c_void_p)]
     L.phx_op_destroy.argtypes = [C.c_void_p]
+    L.phx_op_create_csr_partitioned.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int32, i32p,
+                                                C.POINTER(C.c_void_p)]
+    L.phx_op_nparts.restype = C.c_int32
+    L.phx_op_nparts.argtypes = [C.c_void_p]
     L.phx_op_stream.restype = C.c_void_p
     L.phx_op_stream.argtypes = [C.c_void_p]
     L.phx_apply.argtypes = [C.c_void_p, dp, C.c_int64, C.c_int64, dp, C.c_int64]
@@ -216,15 +221,26 @@ class CsrOperator:
     """Device-resident CSR operator (the LinearOperator of linop.hpp:19-37
     for CSR matrices).  Column indices are used in storage order."""
 
-    def __init__(self, n, row_ptr, col_idx, vals, device: int = -1):
+    def __init__(self, n, row_ptr, col_idx, vals, device: int = -1, parts: int = 1,
+                 devices=None):
+        """parts > 1: row-partitioned operator, part q on
+        devices[q] (default: all on `device`; one device = emulation)."""
         self.n = int(n)
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
         av = np.ascontiguousarray(vals, dtype=np.float64)
         h = C.c_void_p()
-        _check(lib().phx_op_create_csr(self.n, rp.ctypes.data_as(i64p), ci.ctypes.data_as(i32p),
-                                       _d(av), device, C.byref(h)))
+        if parts == 1 and devices is None:
+            _check(lib().phx_op_create_csr(self.n, rp.ctypes.data_as(i64p),
+                                           ci.ctypes.data_as(i32p), _d(av), device, C.byref(h)))
+        else:
+            devs = np.ascontiguousarray(devices if devices is not None else [device] * parts,
+                                        dtype=np.int32)
+            _check(lib().phx_op_create_csr_partitioned(
+                self.n, rp.ctypes.data_as(i64p), ci.ctypes.data_as(i32p), _d(av), int(parts),
+                devs.ctypes.data_as(i32p), C.byref(h)))
         self._h = h
+        self.parts = int(lib().phx_op_nparts(h))
 
     @staticmethod
     def from_dense(A, device: int = -1):

@@ -181,21 +181,23 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_grou
 // The warp's tiles: within every CTA tile the warp owns warp tiles
 // wt = warp, warp + 8, ... (m of them); CTA tiles t = blockIdx.x + k*grid.
 struct TileSeq {
-  int m, ntiles, tile, RW, warp;
+  int m, ntiles, tile, RW, warp, cta, ncta;
   __device__ __forceinline__ int base(int s) const {
-    const int t = int(blockIdx.x) + (s / m) * int(gridDim.x);
+    const int t = cta + (s / m) * ncta;
     return t < ntiles ? t * tile + (warp + (s % m) * kWarps) * RW : -1;
   }
 };
 
 __device__ __forceinline__ TileSeq make_seq(const BlockArgs& a, const Layout& L, int ntiles,
-                                            int warp) {
+                                            int warp, int cta, int ncta) {
   TileSeq ts;
   ts.m = a.tile / (L.RW * kWarps);
   ts.ntiles = ntiles;
   ts.tile = a.tile;
   ts.RW = L.RW;
   ts.warp = warp;
+  ts.cta = cta;
+  ts.ncta = ncta;
   return ts;
 }
 
@@ -249,12 +251,26 @@ __device__ __forceinline__ void pipelined(const BlockArgs& a, const TileSeq& ts,
 // acc[rr][q][e] = sum over row rr's entries (storage order, from +0) of
 // av * X[col*ld + c].  X was written before the last grid.sync(), which
 // invalidates L1 (CCTL.IVALL), so plain cached loads are coherent.
-template <int Q, int V, int R, int B, bool SMEM>
+// PART: column indices are encoded (owner part << 27 | row within the owner)
+// and X is resolved per entry through the gather table Xt (one base pointer
+// per part: peer-GPU memory in a multi-GPU run).
+constexpr unsigned kOwnerShift = 27;
+constexpr unsigned kLocalMask = (1u << kOwnerShift) - 1u;
+
+template <bool PART>
+__device__ __forceinline__ const double* gather_row_ptr(const double* X,
+                                                        const double* const* Xt, unsigned enc,
+                                                        unsigned ld) {
+  if (PART) return Xt[enc >> kOwnerShift] + size_t(enc & kLocalMask) * ld;
+  return X + enc * ld;
+}
+
+template <int Q, int V, int R, int B, bool SMEM, bool PART>
 __device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const double* av_s,
                                        int e_lo, unsigned ld, const int (&rs)[R],
                                        const int (&cnt)[R], const double* X,
-                                       const unsigned (&cq)[Q], const bool (&vq)[Q],
-                                       double (&acc)[R][Q][V]) {
+                                       const double* const* Xt, const unsigned (&cq)[Q],
+                                       const bool (&vq)[Q], double (&acc)[R][Q][V]) {
   int maxc = 0;
 #pragma unroll
   for (int rr = 0; rr < R; ++rr) maxc = max(maxc, cnt[rr]);
@@ -265,15 +281,15 @@ __device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const 
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         const bool ok = u0 + u < cnt[rr];
-        unsigned off = 0;
+        const double* xr = X;
         if (ok) {
           const int e = rs[rr] + u0 + u;
-          off = unsigned(SMEM ? ci[e] : __ldg(a.ci + e_lo + e)) * ld;
+          xr = gather_row_ptr<PART>(X, Xt, unsigned(SMEM ? ci[e] : __ldg(a.ci + e_lo + e)), ld);
         }
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           if (ok && vq[q]) {
-            Vio<V>::ld(X + (off + cq[q]), xv[u][rr][q]);
+            Vio<V>::ld(xr + cq[q], xv[u][rr][q]);
           } else {
 #pragma unroll
             for (int e = 0; e < V; ++e) xv[u][rr][q][e] = 0.0;
@@ -295,11 +311,12 @@ __device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const 
   }
 }
 
-template <int Q, int V, int R, int B>
+template <int Q, int V, int R, int B, bool PART>
 __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L, const int* rp,
                                             const int* ci, const double* av, unsigned ld,
-                                            const double* X, const unsigned (&cq)[Q],
-                                            const bool (&vq)[Q], double (&acc)[R][Q][V]) {
+                                            const double* X, const double* const* Xt,
+                                            const unsigned (&cq)[Q], const bool (&vq)[Q],
+                                            double (&acc)[R][Q][V]) {
   const int e_lo = rp[0];
   int rs[R], cnt[R];
 #pragma unroll
@@ -309,27 +326,69 @@ __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L,
     cnt[rr] = rp[li + 1] - rp[li];
   }
   if (rp[L.RW] - e_lo <= kEC)
-    gather<Q, V, R, B, true>(a, ci, av, e_lo, ld, rs, cnt, X, cq, vq, acc);
+    gather<Q, V, R, B, true, PART>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
   else
-    gather<Q, V, R, B, false>(a, ci, av, e_lo, ld, rs, cnt, X, cq, vq, acc);
+    gather<Q, V, R, B, false, PART>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
 }
 
-template <int Q, int V, int RR>
-__global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs a) {
+template <int Q, int V, int RR, bool PART>
+__global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs ga) {
   constexpr int R = Cfg<Q, V, RR>::R;
   constexpr int B = Cfg<Q, V, RR>::B;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long red[2][kWarps];
   __shared__ WarpPipe pipe[kWarps];
+  // gather tables [D0, D1, S, F0, F1][part] (PART only)
+  __shared__ const double* gtab[5][PART ? kMaxParts : 1];
+  __shared__ double gmax[2];
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpPipe& pp = pipe[warp];
+
+  // Partitioned operator: this launch handles parts
+  // plo .. plo+pcount-1, CTAs split evenly; a CTA rebinds the row-local
+  // fields of its part (rows are part-local from here on).
+  BlockArgs a = ga;
+  int my = 0, cta = int(blockIdx.x), ncta = int(gridDim.x);
+  const PartTab* T = nullptr;
+  if (PART) {
+    const int per = int(gridDim.x) / ga.pcount;
+    my = ga.plo + int(blockIdx.x) / per;
+    cta = int(blockIdx.x) % per;
+    ncta = per;
+    T = ga.ptab + my;
+    a.n = T->nrows;
+    a.rp = T->rp;
+    a.ci = T->ci;
+    a.av = T->av;
+    a.V = T->V;
+    a.Vw = T->Vw;
+    a.D0 = T->D0;
+    a.D1 = T->D1;
+    a.S = T->S;
+    a.F0 = T->F0;
+    a.F1 = T->F1;
+    a.E = T->E;
+    a.W = T->W;
+    a.slots = T->slots;
+    for (int q = threadIdx.x; q < ga.nparts; q += blockDim.x) {
+      const PartTab& U = ga.ptab[q];
+      gtab[0][q] = U.D0;
+      gtab[1][q] = U.D1;
+      gtab[2][q] = U.S;
+      gtab[3][q] = U.F0;
+      gtab[4][q] = U.F1;
+    }
+    __syncthreads();
+  }
+  int dpar = 0, fpar = 0;  // D / F ping-pong parity (all parts swap in lockstep)
 
   const int n = a.n, r = a.r, p = a.p;
   const unsigned ldb = unsigned(a.ldb), ldf = unsigned(a.ldf);
   const int ntiles = (n + a.tile - 1) / a.tile;
   const bool has_xi = a.xi != 0.0;
-  const bool master = blockIdx.x == 0 && threadIdx.x == 0;
+  const bool master = blockIdx.x == 0 && threadIdx.x == 0 && (!PART || ga.plo == 0);
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;  // writes this launch's status
   const Layout LS = make_layout(a.GS, a.QS, a.w, R, V);
   const Layout LF = make_layout(a.GF, a.QF, a.fcols, R, V);
 
@@ -348,18 +407,62 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   auto sync_step = [&](unsigned long long ma, unsigned long long mb, double& ra, double& rb) {
     unsigned long long* slot = a.slots + 2 * (step % 3);
     publish2(ma, mb, slot, red);
-    if (master) {
-      unsigned long long* nxt = a.slots + 2 * ((step + 1) % 3);
-      nxt[0] = 0ull;
-      nxt[1] = 0ull;
+    if (!PART) {
+      if (master) {
+        unsigned long long* nxt = a.slots + 2 * ((step + 1) % 3);
+        nxt[0] = 0ull;
+        nxt[1] = 0ull;
+      }
+      grid.sync();
+      ra = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot)));
+      rb = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot + 1)));
+    } else {
+      // part-local arrival; the part's last CTA publishes the part maxima
+      // into every part's mailbox (peer memory); everyone waits for all parts
+      if (threadIdx.x == 0) {
+        const unsigned gen = unsigned(step) + 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(T->arrive + (step % 3), 1u);
+        if (old == unsigned(ncta) - 1u) {
+          __threadfence();
+          const unsigned long long A = __ldcg(slot), Bv = __ldcg(slot + 1);
+          unsigned long long* nxt = a.slots + 2 * ((step + 1) % 3);
+          nxt[0] = 0ull;
+          nxt[1] = 0ull;
+          T->arrive[(step + 1) % 3] = 0u;
+          // mailboxes are double-buffered by step parity: a part can run one
+          // step ahead and must not overwrite what a slower part still reads
+          const int buf = (step & 1) * ga.nparts;
+          for (int q = 0; q < ga.nparts; ++q) {
+            MailBox* mbx = ga.ptab[q].mbox + buf + my;
+            mbx->a = A;
+            mbx->b = Bv;
+          }
+          __threadfence_system();
+          for (int q = 0; q < ga.nparts; ++q)
+            atomicExch(&(ga.ptab[q].mbox + buf + my)->gen, gen);
+        }
+        unsigned long long A = 0, Bv = 0;
+        for (int q = 0; q < ga.nparts; ++q) {
+          const MailBox* mbx = T->mbox + (step & 1) * ga.nparts + q;
+          while (atomicAdd(const_cast<unsigned*>(&mbx->gen), 0u) < gen) {
+          }
+          __threadfence_system();
+          A = umax64(A, __ldcg(&mbx->a));
+          Bv = umax64(Bv, __ldcg(&mbx->b));
+        }
+        gmax[0] = from_bits(A);
+        gmax[1] = from_bits(Bv);
+        __threadfence();  // invalidates L1 before the next step's gathers
+      }
+      __syncthreads();
+      ra = gmax[0];
+      rb = gmax[1];
     }
-    grid.sync();
-    ra = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot)));
-    rb = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot + 1)));
     ++step;
   };
   auto finish = [&](int err, int idx, int L_S, int extra_steps) {
-    if (master) {
+    if (lead) {
       a.status[0] = err;
       a.status[1] = idx;
       a.status[2] = L_S;
@@ -383,7 +486,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
     unsigned c[Q];
     bool v[Q];
     cols(LS, c, v);
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+    for (int t = cta; t < ntiles; t += ncta)
       for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
         const int base = t * a.tile + wt * LS.RW;
 #pragma unroll
@@ -460,7 +563,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
           ka[q][e] = v[q] ? __ldg(a.colKa + cc) : 0.0;
           tos[q][e] = v[q] ? __ldg(a.colTos + cc) : 0.0;
         }
-      pipelined(a, make_seq(a, LS, ntiles, warp), pp, lane,
+      pipelined(a, make_seq(a, LS, ntiles, warp, cta, ncta), pp, lane,
                 [&](int base, const int* rp, const int* ci, const double* avs) {
           // row-local streams first (independent of the CSR slice)
           double vw[R][Q][V], vwl[R][Q][V], so[R][Q][V], ds[R][Q][V], acc[R][Q][V];
@@ -491,7 +594,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
               }
             }
           }
-          gather_tile<Q, V, R, B>(a, LS, rp, ci, avs, ldb, Dc, c, v, acc);
+          gather_tile<Q, V, R, B, PART>(a, LS, rp, ci, avs, ldb, Dc, gtab[dpar], c, v, acc);
           double vn[R][Q][V], dn[R][Q][V], sn[R][Q][V];
 #pragma unroll
           for (int rr = 0; rr < R; ++rr)
@@ -552,6 +655,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
     double* tmp = Dc;
     Dc = Dn;
     Dn = tmp;
+    dpar ^= 1;
   }
   const int L_S = k;
   if (err != kStOk) {
@@ -571,7 +675,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
     cols(LF, c, v);
 #pragma unroll
     for (int q = 0; q < Q; ++q) vl[q] = v[q] && int(c[q]) < r;
-    pipelined(a, make_seq(a, LF, ntiles, warp), pp, lane,
+    pipelined(a, make_seq(a, LF, ntiles, warp, cta, ncta), pp, lane,
               [&](int base, const int* rp, const int* ci, const double* avs) {
         double acc[R][Q][V];
 #pragma unroll
@@ -583,7 +687,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
         // gathers S block-0 columns (left F columns live at the same column
         // index in S); a pair straddling the left/right split gathers one
         // extra column, unused
-        gather_tile<Q, V, R, B>(a, LF, rp, ci, avs, ldb, a.S, c, vl, acc);
+        gather_tile<Q, V, R, B, PART>(a, LF, rp, ci, avs, ldb, a.S, gtab[2], c, vl, acc);
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
           const int row = base + rr * LF.gpw + LF.g;
@@ -667,7 +771,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
             const int i = cc < r ? cc : cc - r;
             tosF[q][e] = v[q] ? __ldg(a.colTos + i) : 0.0;
           }
-        pipelined(a, make_seq(a, LF, ntiles, warp), pp, lane,
+        pipelined(a, make_seq(a, LF, ntiles, warp, cta, ncta), pp, lane,
                   [&](int base, const int* rp, const int* ci, const double* avs) {
             double eo[R][Q][V], fs[R][Q][V], acc[R][Q][V];
             bool vq[R][Q];
@@ -686,7 +790,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
                 }
               }
             }
-            gather_tile<Q, V, R, B>(a, LF, rp, ci, avs, ldf, Fc, c, v, acc);
+            gather_tile<Q, V, R, B, PART>(a, LF, rp, ci, avs, ldf, Fc, gtab[3 + fpar], c, v, acc);
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
               const int row = base + rr * LF.gpw + LF.g;
@@ -736,9 +840,10 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
       double* tmp = Fc;
       Fc = Fn;
       Fn = tmp;
+      fpar ^= 1;
     }
     if (err != kStOk) break;
-    if (master) a.lensF[sweep - 1] = kk;
+    if (lead) a.lensF[sweep - 1] = kk;
 
     // ---- sweep end (:141-145): E *= mu; Sadv = Sadv*Jexp; F refresh
     // phase A (S layout): Sadv blocks 1..p in place, ascending source column
@@ -746,7 +851,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
       unsigned c[Q];
       bool v[Q];
       cols(LS, c, v);
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int t = cta; t < ntiles; t += ncta)
         for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
           const int base = t * a.tile + wt * LS.RW;
 #pragma unroll
@@ -787,7 +892,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
       unsigned c[Q];
       bool v[Q];
       cols(LF, c, v);
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int t = cta; t < ntiles; t += ncta)
         for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
           const int base = t * a.tile + wt * LF.RW;
 #pragma unroll
@@ -846,24 +951,29 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   finish(err, err_idx, L_S, 0);
 }
 
-template <int Q, int V, int R>
+template <int Q, int V, int R, bool PART>
 cudaError_t occupancy(int block, int* per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_phimv_block<Q, V, R>, block, 0);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_phimv_block<Q, V, R, PART>,
+                                                       block, 0);
 }
 
-template <int Q, int V, int R>
+template <int Q, int V, int R, bool PART>
 const void* kernel_ptr() {
-  return reinterpret_cast<const void*>(k_phimv_block<Q, V, R>);
+  return reinterpret_cast<const void*>(k_phimv_block<Q, V, R, PART>);
 }
 
-// instantiated variants: (Q, V, R) with R = 2 only for single-chunk rows
-const void* select_kernel(int QT, int V, int R, cudaError_t (**occ)(int, int*)) {
-  const int key = QT * 100 + V * 10 + R;
+// instantiated variants: (Q, V, R) with R = 2 only for single-chunk rows,
+// each unpartitioned and partitioned
+const void* select_kernel(int QT, int V, int R, bool part, cudaError_t (**occ)(int, int*)) {
+  const int key = QT * 100 + V * 10 + R + (part ? 1000 : 0);
   switch (key) {
-#define PHX_CASE(q, v, r)          \
-  case q * 100 + v * 10 + r:       \
-    *occ = occupancy<q, v, r>;     \
-    return kernel_ptr<q, v, r>();
+#define PHX_CASE(q, v, r)                              \
+  case q * 100 + v * 10 + r:                           \
+    *occ = occupancy<q, v, r, false>;                  \
+    return kernel_ptr<q, v, r, false>();               \
+  case 1000 + q * 100 + v * 10 + r:                    \
+    *occ = occupancy<q, v, r, true>;                   \
+    return kernel_ptr<q, v, r, true>();
     PHX_CASE(1, 1, 1)
     PHX_CASE(1, 1, 2)
     PHX_CASE(1, 2, 1)
@@ -882,7 +992,7 @@ const void* select_kernel(int QT, int V, int R, cudaError_t (**occ)(int, int*)) 
 
 }  // namespace
 
-cudaError_t coop_grid_size(int QT, int V, int R, int block, int* max_blocks) {
+cudaError_t coop_grid_size(int QT, int V, int R, bool part, int block, int* max_blocks) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -890,7 +1000,7 @@ cudaError_t coop_grid_size(int QT, int V, int R, int block, int* max_blocks) {
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
   cudaError_t (*occ)(int, int*) = nullptr;
-  if (!select_kernel(QT, V, R, &occ)) return cudaErrorInvalidValue;
+  if (!select_kernel(QT, V, R, part, &occ)) return cudaErrorInvalidValue;
   int per_sm = 0;
   e = occ(block, &per_sm);
   if (e != cudaSuccess) return e;
@@ -902,7 +1012,7 @@ cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStre
   BlockArgs copy = a;
   void* args[] = {&copy};
   cudaError_t (*occ)(int, int*) = nullptr;
-  const void* fn = select_kernel(a.QT, a.vec, a.R, &occ);
+  const void* fn = select_kernel(a.QT, a.vec, a.R, a.nparts > 1, &occ);
   if (!fn) return cudaErrorInvalidValue;
   count_launch();
   return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);

@@ -131,9 +131,22 @@ int64_t g_trace_len = 0;
 double g_last_ms = 0.0;
 int64_t g_last_steps = 0;
 
+// One row part of a partitioned operator, resident on `dev`.
+struct PartDev {
+  int dev = 0;
+  int64_t row0 = 0, nrows = 0, nnz = 0;
+  int32_t* rp = nullptr;  // part-local row_ptr
+  int32_t* ci = nullptr;  // encoded columns: owner << 27 | row within owner
+  double* av = nullptr;
+  cudaStream_t stream = nullptr;
+  DevBuf Vw, D0, D1, S, F0, F1, E, W, V, coef, slots, arrive, mbox, status, lensF, trace, ptab;
+};
+
 }  // namespace
 
 struct phx_op_s {
+  int nparts = 1;                // > 1: row-partitioned (parts[], no d_rp/d_ci/d_av)
+  std::vector<PartDev> parts;
   int device = 0;
   int64_t n = 0, nnz = 0;
   int32_t* d_rp = nullptr;
@@ -172,6 +185,15 @@ struct DeviceGuard {
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
+
+// Parameter selection and the column-block apply run on an unpartitioned
+// operator; a partitioned one serves phimv_block with a reused ScalingShift.
+void require_whole(phx_op op, const char* who) {
+  if (op->nparts > 1)
+    throw_phx(PHX_EINVAL, std::string(who) +
+                              ": needs an unpartitioned operator (select parameters on the whole "
+                              "operator and reuse the ScalingShift)");
+}
 
 // ---------------------------------------------------------------------------
 // stableNorm (params.cpp call sites :108,117,124,168,201) on a device vector:
@@ -275,6 +297,7 @@ double log_binomial(int m, int j) {  // params.cpp:15-17
 
 // build_power_basis (params.cpp:81-154) with the n-sized work on the device
 phx_basis_s* build_basis(phx_op op, int m, double delta) {
+  require_whole(op, "build_power_basis");
   if (m < 1) throw_phx(PHX_EINVAL, "build_power_basis: m must be >= 1");
   if (!(delta > 0.0 && delta <= 1.0))
     throw_phx(PHX_EINVAL, "build_power_basis: delta must be in (0, 1]");
@@ -536,6 +559,164 @@ struct EvalIn {
   double* h_tail;
 };
 
+// Row-partitioned evaluation.  Every part runs the same
+// persistent kernel over its own rows; gathers of other parts' rows read
+// their buffers through the part table (P2P over NVLink when parts live on
+// different GPUs) and the per-step maxima are combined through mailboxes, so
+// every part takes the same stopping decisions and produces bitwise the rows
+// of an unpartitioned run.  Parts sharing one device run as ONE cooperative
+// launch (all CTAs co-resident: the single-GPU emulation used by the tests);
+// parts on distinct devices run one launch per device, started back to back.
+void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::vector<double>& coef,
+                  int64_t s_eff, int32_t* h_status, int32_t* h_lens, int64_t nsw,
+                  int64_t trace_cap, float* ms_out) {
+  const int P = op->nparts;
+  const int32_t r = base.r, p = base.p, ldb = base.ldb, ldf = base.ldf;
+  if (in.single || in.h_exp_v0 || in.h_tail)
+    throw_phx(PHX_EINVAL, "phimv: the single-combination evaluator needs an unpartitioned operator");
+  if (!in.hV || !in.hW)
+    throw_phx(PHX_EINVAL, "phimv_block: a partitioned operator takes host V and W buffers");
+  const size_t ncoef = coef.size();
+  std::vector<phx::PartTab> tab(static_cast<size_t>(P));
+  for (int q = 0; q < P; ++q) {
+    PartDev& d = op->parts[size_t(q)];
+    DeviceGuard guard(d.dev);
+    const size_t nr = size_t(d.nrows);
+    if (uint64_t(nr) * uint64_t(std::max(ldb, ldf)) >= (uint64_t(1) << 32))
+      throw_phx(PHX_EINVAL, "phimv_block: part rows * (p+1)*r >= 2^32 block entries");
+    phx::PartTab& T = tab[size_t(q)];
+    T.rp = d.rp;
+    T.ci = d.ci;
+    T.av = d.av;
+    double* dV = d.V.as<double>(nr * size_t(p + 1));
+    T.V = dV;
+    T.Vw = d.Vw.as<double>(nr * size_t(ldb));
+    T.D0 = d.D0.as<double>(nr * size_t(ldb));
+    T.D1 = d.D1.as<double>(nr * size_t(ldb));
+    T.S = d.S.as<double>(nr * size_t(ldb));
+    T.F0 = d.F0.as<double>(nr * size_t(ldf));
+    T.F1 = d.F1.as<double>(nr * size_t(ldf));
+    T.E = d.E.as<double>(nr * size_t(ldf));
+    T.W = d.W.as<double>(nr * size_t(r));
+    T.slots = d.slots.as<unsigned long long>(6);
+    T.arrive = d.arrive.as<unsigned>(3);
+    T.mbox = d.mbox.as<phx::MailBox>(2 * size_t(P));  // [step parity][part]
+    T.row0 = int32_t(d.row0);
+    T.nrows = int32_t(d.nrows);
+    PHX_CUDA(cudaMemcpy2DAsync(dV, nr * 8, in.hV + d.row0, size_t(in.ldv) * 8, nr * 8,
+                               size_t(p + 1), cudaMemcpyHostToDevice, d.stream));
+    PHX_CUDA(cudaMemsetAsync(T.slots, 0, 6 * sizeof(unsigned long long), d.stream));
+    PHX_CUDA(cudaMemsetAsync(T.arrive, 0, 3 * sizeof(unsigned), d.stream));
+    PHX_CUDA(cudaMemsetAsync(T.mbox, 0, 2 * size_t(P) * sizeof(phx::MailBox), d.stream));
+    double* dc = d.coef.as<double>(ncoef);
+    PHX_CUDA(cudaMemcpyAsync(dc, coef.data(), ncoef * 8, cudaMemcpyHostToDevice, d.stream));
+  }
+  // launch groups: consecutive parts on one device share a launch
+  struct Group {
+    int plo, pcount;
+  };
+  std::vector<Group> groups;
+  for (int q = 0; q < P;) {
+    int e = q + 1;
+    while (e < P && op->parts[size_t(e)].dev == op->parts[size_t(q)].dev) ++e;
+    groups.push_back({q, e - q});
+    q = e;
+  }
+  {
+    std::vector<int> seen;
+    for (const Group& g : groups) {
+      const int dev = op->parts[size_t(g.plo)].dev;
+      if (std::find(seen.begin(), seen.end(), dev) != seen.end())
+        throw_phx(PHX_EINVAL, "partitioned operator: a device's parts must be consecutive");
+      seen.push_back(dev);
+    }
+  }
+  for (const Group& g : groups) {
+    PartDev& d = op->parts[size_t(g.plo)];
+    DeviceGuard guard(d.dev);
+    phx::PartTab* dtab = d.ptab.as<phx::PartTab>(size_t(P));
+    PHX_CUDA(cudaMemcpyAsync(dtab, tab.data(), size_t(P) * sizeof(phx::PartTab),
+                             cudaMemcpyHostToDevice, d.stream));
+    PHX_CUDA(cudaStreamSynchronize(d.stream));  // host tab copy is a stack temporary
+  }
+  // all parts' uploads must land before any part's kernel reads a peer
+  for (int q = 0; q < P; ++q) {
+    DeviceGuard guard(op->parts[size_t(q)].dev);
+    PHX_CUDA(cudaStreamSynchronize(op->parts[size_t(q)].stream));
+  }
+  const int block = 256;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const Group& g = groups[gi];
+    PartDev& d = op->parts[size_t(g.plo)];
+    DeviceGuard guard(d.dev);
+    phx::BlockArgs a = base;
+    const double* dc = static_cast<const double*>(d.coef.p);
+    const int32_t w = base.w;
+    a.colKd = dc;
+    a.colKa = dc + w;
+    a.colTos = dc + 2 * w;
+    a.t = dc + 3 * w;
+    a.alpha = a.t + r;
+    a.mu = a.alpha + r;
+    a.g = a.mu + r;
+    a.jc = a.g + r;
+    a.nparts = P;
+    a.plo = g.plo;
+    a.pcount = g.pcount;
+    a.ptab = static_cast<const phx::PartTab*>(d.ptab.p);
+    a.status = d.status.as<int32_t>(8);
+    a.lensF = d.lensF.as<int32_t>(size_t(std::max<int64_t>(1, s_eff - 1)));
+    a.trace = (g.plo == 0 && trace_cap > 0) ? d.trace.as<double>(size_t(trace_cap)) : nullptr;
+    a.trace_cap = int32_t(trace_cap);
+    PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), d.stream));
+    int max_blocks = 0;
+    PHX_CUDA(phx::coop_grid_size(a.QT, a.vec, a.R, true, block, &max_blocks));
+    int64_t most = 1;
+    for (int q = g.plo; q < g.plo + g.pcount; ++q)
+      most = std::max<int64_t>(most, (op->parts[size_t(q)].nrows + a.tile - 1) / a.tile);
+    const int per = int(std::max<int64_t>(1, std::min<int64_t>(max_blocks / g.pcount, most)));
+    if (gi == 0) {
+      PHX_CUDA(cudaEventCreate(&e0));
+      PHX_CUDA(cudaEventCreate(&e1));
+      PHX_CUDA(cudaEventRecord(e0, d.stream));
+    }
+    PHX_CUDA(phx::launch_phimv_block(a, per * g.pcount, block, d.stream));
+    if (gi == 0) PHX_CUDA(cudaEventRecord(e1, d.stream));
+  }
+  // collect: status / sweep lengths / trace from part 0's launch, W slices
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const Group& g = groups[gi];
+    PartDev& d0 = op->parts[size_t(g.plo)];
+    DeviceGuard guard(d0.dev);
+    for (int q = g.plo; q < g.plo + g.pcount; ++q) {
+      PartDev& d = op->parts[size_t(q)];
+      PHX_CUDA(cudaMemcpy2DAsync(in.hW + d.row0, size_t(in.ldw) * 8, d.W.p, size_t(d.nrows) * 8,
+                                 size_t(d.nrows) * 8, size_t(r), cudaMemcpyDeviceToHost,
+                                 d0.stream));
+    }
+    int32_t st[8];
+    PHX_CUDA(cudaMemcpyAsync(st, d0.status.p, sizeof(st), cudaMemcpyDeviceToHost, d0.stream));
+    PHX_CUDA(cudaStreamSynchronize(d0.stream));
+    if (gi == 0) {
+      std::copy(st, st + 8, h_status);
+      if (nsw > 0)
+        PHX_CUDA(cudaMemcpy(h_lens, d0.lensF.p, size_t(nsw) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      if (trace_cap > 0) {
+        std::lock_guard<std::mutex> lk(g_trace_mu);
+        g_trace.assign(size_t(trace_cap), 0.0);
+        g_trace_len = st[5];
+        PHX_CUDA(cudaMemcpy(g_trace.data(), d0.trace.p, size_t(trace_cap) * 8, cudaMemcpyDeviceToHost));
+      }
+      PHX_CUDA(cudaEventElapsedTime(ms_out, e0, e1));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    } else if (st[0] != h_status[0] || st[2] != h_status[2]) {
+      throw_phx(PHX_ECUDA, "partitioned evaluation: parts disagree on the stopping decisions");
+    }
+  }
+}
+
 void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   const char* who = in.single ? "phimv" : "phimv_block";
   const int64_t n = op->n;
@@ -630,6 +811,43 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   const int32_t R = (QT == 1 && (V == 1 || avg_nnz < 2.5)) ? 2 : 1;
   const int32_t tile = 8 * (32 / std::min(GS, GF)) * R;
 
+  const int64_t nsw = s_eff - 1;
+  int32_t* h_status = nullptr;
+  int32_t* h_lens = nullptr;
+  float ms = 0.f;
+  int64_t trace_cap;
+  {
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    trace_cap = g_trace_cap;
+  }
+  if (op->nparts > 1) {
+    phx::BlockArgs b{};
+    b.p = p;
+    b.r = r;
+    b.w = w;
+    b.fcols = fcols;
+    b.GS = GS;
+    b.QS = QS;
+    b.GF = GF;
+    b.QF = QF;
+    b.QT = QT;
+    b.vec = V;
+    b.R = R;
+    b.tile = tile;
+    b.xi = xi;
+    b.tol = tol;
+    b.s_eff = int32_t(s_eff);
+    b.single_variant = 0;
+    b.t_single = in.t[0];
+    b.ldb = w;
+    b.ldf = fcols;
+    h_status = op->h_small.as<int32_t>(8);
+    h_lens = op->h_lens.as<int32_t>(size_t(std::max<int64_t>(1, nsw)));
+    launch_parts(op, in, b, coef, s_eff, h_status, h_lens, nsw, trace_cap, &ms);
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    g_last_ms = ms;
+    g_last_steps = h_status[4];
+  } else {
   // workspace
   const int32_t ldb = w, ldf = fcols;
   if (uint64_t(n) * uint64_t(ldb) >= (uint64_t(1) << 32))
@@ -681,11 +899,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.slots = op->slots.as<unsigned long long>(6);  // [3][maxA, maxB]
   a.status = op->status.as<int32_t>(8);
   a.lensF = op->lensF.as<int32_t>(size_t(std::max<long>(1, s_eff - 1)));
-  int64_t trace_cap;
-  {
-    std::lock_guard<std::mutex> lk(g_trace_mu);
-    trace_cap = g_trace_cap;
-  }
+  a.nparts = 1;
   a.trace = trace_cap > 0 ? op->trace.as<double>(size_t(trace_cap)) : nullptr;
   a.trace_cap = int32_t(trace_cap);
 
@@ -705,7 +919,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), st));
 
   int max_blocks = 0;
-  PHX_CUDA(phx::coop_grid_size(QT, V, R, block, &max_blocks));
+  PHX_CUDA(phx::coop_grid_size(QT, V, R, false, block, &max_blocks));
   const int64_t ntiles = (n + tile - 1) / tile;
   // developer knob for tuning studies: PHX_GRID_FRAC = fraction (0, 1] of the
   // co-resident CTA count to launch
@@ -720,10 +934,9 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   PHX_CUDA(phx::launch_phimv_block(a, grid, block, st));
   PHX_CUDA(cudaEventRecord(op->ev1, st));
 
-  int32_t* h_status = op->h_small.as<int32_t>(8);
+  h_status = op->h_small.as<int32_t>(8);
   PHX_CUDA(cudaMemcpyAsync(h_status, a.status, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  const long nsw = s_eff - 1;
-  int32_t* h_lens = op->h_lens.as<int32_t>(size_t(std::max<long>(1, nsw)));
+  h_lens = op->h_lens.as<int32_t>(size_t(std::max<int64_t>(1, nsw)));
   if (nsw > 0)
     PHX_CUDA(cudaMemcpyAsync(h_lens, a.lensF, size_t(nsw) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   if (in.hW) {
@@ -738,7 +951,6 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   if (in.h_tail)
     PHX_CUDA(cudaMemcpyAsync(in.h_tail, a.FRo, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
   PHX_CUDA(cudaStreamSynchronize(st));
-  float ms = 0.f;
   PHX_CUDA(cudaEventElapsedTime(&ms, op->ev0, op->ev1));
   {
     std::lock_guard<std::mutex> lk(g_trace_mu);
@@ -750,6 +962,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
       PHX_CUDA(cudaMemcpy(g_trace.data(), a.trace, size_t(trace_cap) * 8, cudaMemcpyDeviceToHost));
     }
   }
+  }  // single-device path
 
   const int32_t code = h_status[0];
   const int32_t idx = h_status[1];
@@ -854,8 +1067,107 @@ phx_status phx_op_create_csr(int64_t n, const int64_t* row_ptr, const int32_t* c
   });
 }
 
+phx_status phx_op_create_csr_partitioned(int64_t n, const int64_t* row_ptr,
+                                         const int32_t* col_idx, const double* vals,
+                                         int32_t nparts, const int32_t* devices, phx_op* out) {
+  return guarded([&] {
+    if (!out) throw_phx(PHX_EINVAL, "phx_op_create_csr_partitioned: out is null");
+    *out = nullptr;
+    if (nparts < 1 || nparts > phx::kMaxParts)
+      throw_phx(PHX_EINVAL, "phx_op_create_csr_partitioned: nparts must be in [1, 16]");
+    if (n < nparts) throw_phx(PHX_EINVAL, "phx_op_create_csr_partitioned: fewer rows than parts");
+    if (n >= (int64_t(1) << 31) - 1) throw_phx(PHX_EINVAL, "phx_op_create_csr: n must be < 2^31");
+    if (!row_ptr || row_ptr[0] != 0) throw_phx(PHX_EINVAL, "phx_op_create_csr: row_ptr[0] must be 0");
+    const int64_t nnz = row_ptr[n];
+    if (nnz < 0 || nnz >= (int64_t(1) << 31))
+      throw_phx(PHX_EINVAL, "phx_op_create_csr: nnz must be in [0, 2^31)");
+    for (int64_t i = 0; i < n; ++i)
+      if (row_ptr[i + 1] < row_ptr[i]) throw_phx(PHX_EINVAL, "phx_op_create_csr: row_ptr not monotone");
+    for (int64_t e = 0; e < nnz; ++e) {
+      if (col_idx[e] < 0 || col_idx[e] >= n)
+        throw_phx(PHX_EINVAL, "phx_op_create_csr: column index out of range");
+      if (!std::isfinite(vals[e])) throw_phx(PHX_EINVAL, "dense_operator: matrix has non-finite entries");
+    }
+    // contiguous row parts; columns encoded as owner << 27 | row within owner
+    std::vector<int64_t> bnd(size_t(nparts) + 1);
+    for (int q = 0; q <= nparts; ++q) bnd[size_t(q)] = int64_t(q) * n / nparts;
+    for (int q = 0; q < nparts; ++q)
+      if (bnd[size_t(q + 1)] - bnd[size_t(q)] >= (int64_t(1) << 27))
+        throw_phx(PHX_EINVAL, "phx_op_create_csr_partitioned: a part exceeds 2^27 rows");
+    auto* op = new phx_op_s();
+    op->n = n;
+    op->nnz = nnz;
+    op->nparts = nparts;
+    try {
+      int cur = 0;
+      PHX_CUDA(cudaGetDevice(&cur));
+      op->device = (devices && devices[0] >= 0) ? devices[0] : cur;
+      op->parts.resize(size_t(nparts));
+      for (int q = 0; q < nparts; ++q) {
+        PartDev& d = op->parts[size_t(q)];
+        d.dev = (devices && devices[q] >= 0) ? devices[q] : cur;
+        d.row0 = bnd[size_t(q)];
+        d.nrows = bnd[size_t(q + 1)] - bnd[size_t(q)];
+        const int64_t e0 = row_ptr[d.row0], e1 = row_ptr[d.row0 + d.nrows];
+        d.nnz = e1 - e0;
+        std::vector<int32_t> rp(size_t(d.nrows) + 1), ci(std::max<size_t>(1, size_t(d.nnz)));
+        for (int64_t i = 0; i <= d.nrows; ++i) rp[size_t(i)] = int32_t(row_ptr[d.row0 + i] - e0);
+        for (int64_t e = e0; e < e1; ++e) {
+          const int64_t col = col_idx[e];
+          const int owner = int(std::upper_bound(bnd.begin(), bnd.end(), col) - bnd.begin()) - 1;
+          ci[size_t(e - e0)] = int32_t((uint32_t(owner) << 27) | uint32_t(col - bnd[size_t(owner)]));
+        }
+        DeviceGuard guard(d.dev);
+        PHX_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+        PHX_CUDA(cudaMalloc(&d.rp, rp.size() * 4));
+        PHX_CUDA(cudaMalloc(&d.ci, ci.size() * 4));
+        PHX_CUDA(cudaMalloc(&d.av, std::max<size_t>(1, size_t(d.nnz)) * 8));
+        PHX_CUDA(cudaMemcpy(d.rp, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
+        if (d.nnz > 0) {
+          PHX_CUDA(cudaMemcpy(d.ci, ci.data(), size_t(d.nnz) * 4, cudaMemcpyHostToDevice));
+          PHX_CUDA(cudaMemcpy(d.av, vals + e0, size_t(d.nnz) * 8, cudaMemcpyHostToDevice));
+        }
+      }
+      // peer access between the parts' devices (NVLink P2P)
+      for (int q = 0; q < nparts; ++q)
+        for (int u = 0; u < nparts; ++u) {
+          const int a = op->parts[size_t(q)].dev, b = op->parts[size_t(u)].dev;
+          if (a == b) continue;
+          int can = 0;
+          PHX_CUDA(cudaDeviceCanAccessPeer(&can, a, b));
+          if (!can) throw_phx(PHX_ECUDA, "partitioned operator: no peer access between devices");
+          DeviceGuard guard(a);
+          const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) PHX_CUDA(e);
+          cudaGetLastError();
+        }
+      DeviceGuard guard(op->device);
+      PHX_CUDA(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
+      PHX_CUDA(cudaEventCreate(&op->ev0));
+      PHX_CUDA(cudaEventCreate(&op->ev1));
+    } catch (...) {
+      phx_op_destroy(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
+int32_t phx_op_nparts(phx_op op) { return op ? op->nparts : 0; }
+
 phx_status phx_op_destroy(phx_op op) {
   if (!op) return PHX_OK;
+  for (PartDev& d : op->parts) {
+    cudaSetDevice(d.dev);
+    if (d.stream) cudaStreamSynchronize(d.stream);
+    for (DevBuf* b : {&d.Vw, &d.D0, &d.D1, &d.S, &d.F0, &d.F1, &d.E, &d.W, &d.V, &d.coef, &d.slots,
+                      &d.arrive, &d.mbox, &d.status, &d.lensF, &d.trace, &d.ptab})
+      b->release();
+    if (d.rp) cudaFree(d.rp);
+    if (d.ci) cudaFree(d.ci);
+    if (d.av) cudaFree(d.av);
+    if (d.stream) cudaStreamDestroy(d.stream);
+  }
   {
     int prev = -1;
     cudaGetDevice(&prev);
@@ -887,6 +1199,7 @@ static phx_status apply_impl(phx_op op, int mode, double xi, const double* X, in
                              int64_t k, double* Y, int64_t ldy) {
   return guarded([&] {
     if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    require_whole(op, "LinearOperator::apply");
     if (mode == 1 && !std::isfinite(xi)) throw_phx(PHX_EINVAL, "shifted_apply: shift must be finite");
     if (ldx < op->n || ldy < op->n)
       throw_phx(PHX_EINVAL, "LinearOperator::apply: block rows do not match the operator dimension");

@@ -11,6 +11,38 @@ namespace phx {
 constexpr int kChunk = 4096;       // stableNorm block (Eigen blocking)
 constexpr int kNormThreads = 256;  // canonical lane count of a chunk
 
+constexpr int kMaxParts = 16;  // row parts of a partitioned operator
+
+// Cross-part step mailbox: part p's leader writes (a, b) then gen into slot
+// p of every part's mailbox array (peer memory in a multi-GPU run).
+struct MailBox {
+  unsigned gen;
+  unsigned pad;
+  unsigned long long a, b;
+};
+
+// One row part of a partitioned operator: its CSR rows with
+// encoded columns (owner part << 27 | row within the owner), its block
+// buffers (part-local rows), its step slots, arrival counters and mailboxes.
+struct PartTab {
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* av;
+  const double* V;
+  double* Vw;
+  double* D0;
+  double* D1;
+  double* S;
+  double* F0;
+  double* F1;
+  double* E;
+  double* W;
+  unsigned long long* slots;  // [3][2]
+  unsigned* arrive;           // [3]
+  MailBox* mbox;              // [2 step parities][nparts]
+  int32_t row0, nrows;
+};
+
 // Per-call parameters of the persistent phimv_block kernel.
 struct BlockArgs {
   // operator (CSR, int32 indices)
@@ -60,6 +92,10 @@ struct BlockArgs {
   int32_t* lensF;             // [s_eff-1]
   double* trace;              // optional (kind, a, b) triples
   int32_t trace_cap;
+  // partitioned operator (nparts > 1): this launch handles parts
+  // plo .. plo+pcount-1; ptab (device, nparts entries) describes all parts
+  int32_t nparts, plo, pcount;
+  const PartTab* ptab;
 };
 
 // status codes written by the kernel
@@ -74,7 +110,7 @@ enum : int32_t {
 
 // launch wrappers (phx_kernels.cu)
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st);
-cudaError_t coop_grid_size(int QT, int V, int R, int block, int* max_blocks);
+cudaError_t coop_grid_size(int QT, int V, int R, bool part, int block, int* max_blocks);
 
 // y = f(A x) with mode 0: A x, 1: A x - fl(xi x), 2: (A x) / div ; fused
 // per-chunk max|y| into chunkmax (bit patterns) when chunkmax != nullptr

@@ -1,0 +1,62 @@
+"""Row-partitioned evaluation in its single-GPU emulation:
+every part is processed by its own CTA group of ONE cooperative launch with
+its own buffers; other parts' block rows are read through the part table and
+the per-term maxima are combined through the cross-part mailboxes — the
+exact protocol of the multi-GPU run.  The result must be bitwise the
+unpartitioned one (rows are independent given the previous term; maxima
+are order-free)."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def P():
+    import paper_2509_26475_b200 as mod
+    return mod
+
+
+@pytest.mark.parametrize("cfg,size,parts", [(1, 0, 2), (1, 0, 3), (2, 64, 2), (2, 64, 4),
+                                            (3, 12, 3), (4, 1024, 4), (5, 2000, 2),
+                                            (5, 2000, 7)])
+def test_partitioned_bitwise(cfg, size, parts):
+    p = P()
+    wl = p.workload(cfg, size)
+    whole = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    ss = p.select_parameters(whole, 61, wl.tol)
+    ref = p.phimv_block(whole, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    part = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=parts)
+    assert part.parts == parts
+    p.set_trace(3 * 100000)
+    res = p.phimv_block(part, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    tr = p.get_trace(3 * 100000)
+    p.set_trace(0)
+    assert res.stats.series_len_S == ref.stats.series_len_S
+    assert res.stats.series_lens_F == ref.stats.series_lens_F
+    assert res.stats.matvecs == ref.stats.matvecs
+    assert np.array_equal(res.W, ref.W)
+    oop = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    _, _, otr = O.phimv_block(oop, wl.t, wl.alpha, wl.V, wl.tol, O.ScalingShift(*ss.astuple()),
+                              trace=True)
+    assert np.array_equal(tr, otr)
+
+
+def test_partitioned_full_c2_bitwise():
+    p = P()
+    wl = p.workload(2, 0)
+    whole = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    ss = p.select_parameters(whole, 61, wl.tol)
+    ref = p.phimv_block(whole, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss)).W
+    part = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=8)
+    W = p.phimv_block(part, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss)).W
+    assert np.array_equal(W, ref)
+
+
+def test_partitioned_rejects_selection():
+    p = P()
+    wl = p.workload(2, 32)
+    part = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=2)
+    with pytest.raises(ValueError, match="unpartitioned"):
+        p.select_parameters(part, 61, wl.tol)
