@@ -348,29 +348,32 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   // Partitioned operator: this launch handles parts
   // plo .. plo+pcount-1, CTAs split evenly; a CTA rebinds the row-local
   // fields of its part (rows are part-local from here on).
-  BlockArgs a = ga;
+  // (unpartitioned: `a` aliases the kernel parameter, read from the constant
+  // bank; partitioned: a local copy with the part's fields)
+  BlockArgs pa;
   int my = 0, cta = int(blockIdx.x), ncta = int(gridDim.x);
   const PartTab* T = nullptr;
   if (PART) {
+    pa = ga;
     const int per = int(gridDim.x) / ga.pcount;
     my = ga.plo + int(blockIdx.x) / per;
     cta = int(blockIdx.x) % per;
     ncta = per;
     T = ga.ptab + my;
-    a.n = T->nrows;
-    a.rp = T->rp;
-    a.ci = T->ci;
-    a.av = T->av;
-    a.V = T->V;
-    a.Vw = T->Vw;
-    a.D0 = T->D0;
-    a.D1 = T->D1;
-    a.S = T->S;
-    a.F0 = T->F0;
-    a.F1 = T->F1;
-    a.E = T->E;
-    a.W = T->W;
-    a.slots = T->slots;
+    pa.n = T->nrows;
+    pa.rp = T->rp;
+    pa.ci = T->ci;
+    pa.av = T->av;
+    pa.V = T->V;
+    pa.Vw = T->Vw;
+    pa.D0 = T->D0;
+    pa.D1 = T->D1;
+    pa.S = T->S;
+    pa.F0 = T->F0;
+    pa.F1 = T->F1;
+    pa.E = T->E;
+    pa.W = T->W;
+    pa.slots = T->slots;
     for (int q = threadIdx.x; q < ga.nparts; q += blockDim.x) {
       const PartTab& U = ga.ptab[q];
       gtab[0][q] = U.D0;
@@ -381,6 +384,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
     }
     __syncthreads();
   }
+  const BlockArgs& a = PART ? pa : ga;
   int dpar = 0, fpar = 0;  // D / F ping-pong parity (all parts swap in lockstep)
 
   const int n = a.n, r = a.r, p = a.p;
