@@ -125,6 +125,18 @@ void fill_normal(uint64_t seed, int64_t n, int cols, double* V) {
 
 extern "C" {
 
+// The reference Rng streams (for tests of the product's Rng against the
+// oracle's): n normals from seed, and Rng(seed).unit_vector(n).
+void phx_wl_normals(uint64_t seed, int64_t n, double* out) {
+  phx::Rng rng(seed);
+  rng.matrix(n, 1, out);
+}
+void phx_wl_unit_vector(uint64_t seed, int64_t n, double* out) {
+  phx::Rng rng(seed);
+  const std::vector<double> v = phx::unit_vector(rng, n);
+  std::copy(v.begin(), v.end(), out);
+}
+
 int phx_wl_info_get(int32_t cfg, int64_t size, phx_wl_info* out) {
   return info(cfg, size, out) ? 0 : 1;
 }
