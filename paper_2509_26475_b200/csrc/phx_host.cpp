@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1303,10 +1305,26 @@ phx_status phx_select_parameters(phx_op op, int32_t m, double tol, double delta,
     std::lock_guard<std::mutex> lk(op->mu);
     DeviceGuard guard(op->device);
     if (tol <= 0.0) tol = std::ldexp(1.0, -53);  // params.cpp:243
+    static const bool prof = std::getenv("PHX_PROFILE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
+    start_vector(op, 1);
+    const auto t1 = now();
     phx_basis_s* b = build_basis(op, m, delta);
+    const auto t2 = now();
     try {
-      const double xi_star = minimize_shift_dev(b, nullptr).first;
+      std::vector<double> path;
+      const double xi_star = minimize_shift_dev(b, prof ? &path : nullptr).first;
+      const auto t3 = now();
       *out = params_for_shift_dev(b, xi_star, tol);
+      const auto t4 = now();
+      if (prof)
+        std::fprintf(stderr,
+                     "[phx] select_parameters n=%lld: start vector %.1f ms, power basis %.1f ms "
+                     "(r=%d), Brent %.1f ms (%zu objective evals), parameters_for_shift %.1f ms\n",
+                     static_cast<long long>(op->n), ms(t0, t1), ms(t1, t2), b->r, ms(t2, t3),
+                     path.size() / 2 + 4, ms(t3, t4));
     } catch (...) {
       destroy_basis(b);
       throw;
