@@ -418,6 +418,11 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
         nxt[1] = 0ull;
       }
       grid.sync();
+      if (master && a.tstamp != nullptr && step < a.tstamp_cap) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        a.tstamp[step] = ns;
+      }
       ra = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot)));
       rb = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot + 1)));
     } else {

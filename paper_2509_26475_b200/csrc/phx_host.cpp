@@ -158,7 +158,7 @@ struct phx_op_s {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::mutex mu;
   // evaluation workspace
-  DevBuf Vw, D0, D1, S, F0, F1, E, W, V, coef, slots, status, lensF, FLo, FRo, trace;
+  DevBuf Vw, D0, D1, S, F0, F1, E, W, V, coef, slots, status, lensF, FLo, FRo, trace, tstamp;
   // selection workspace
   DevBuf w0, w1, y, chunkmax, inv, partial, gcoef, spx, spy;
   HostBuf h_small, h_chunk, h_inv, h_part, h_lens;
@@ -902,6 +902,10 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.status = op->status.as<int32_t>(8);
   a.lensF = op->lensF.as<int32_t>(size_t(std::max<long>(1, s_eff - 1)));
   a.nparts = 1;
+  static const bool step_times = std::getenv("PHX_STEP_TIMES") != nullptr;
+  a.tstamp_cap = step_times ? 1 << 16 : 0;
+  a.tstamp = step_times ? op->tstamp.as<unsigned long long>(size_t(a.tstamp_cap)) : nullptr;
+  if (step_times) PHX_CUDA(cudaMemsetAsync(a.tstamp, 0, size_t(a.tstamp_cap) * 8, st));
   a.trace = trace_cap > 0 ? op->trace.as<double>(size_t(trace_cap)) : nullptr;
   a.trace_cap = int32_t(trace_cap);
 
@@ -935,6 +939,15 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   PHX_CUDA(cudaEventRecord(op->ev0, st));
   PHX_CUDA(phx::launch_phimv_block(a, grid, block, st));
   PHX_CUDA(cudaEventRecord(op->ev1, st));
+  if (step_times) {
+    std::vector<unsigned long long> ts(size_t(a.tstamp_cap));
+    PHX_CUDA(cudaMemcpyAsync(ts.data(), a.tstamp, ts.size() * 8, cudaMemcpyDeviceToHost, st));
+    PHX_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "[phx] step durations (us):");
+    for (size_t q = 1; q < ts.size() && ts[q] != 0 && q < 48; ++q)
+      std::fprintf(stderr, " %.1f", double(ts[q] - ts[q - 1]) * 1e-3);
+    std::fprintf(stderr, "\n");
+  }
 
   h_status = op->h_small.as<int32_t>(8);
   PHX_CUDA(cudaMemcpyAsync(h_status, a.status, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));

@@ -96,6 +96,9 @@ struct BlockArgs {
   // plo .. plo+pcount-1; ptab (device, nparts entries) describes all parts
   int32_t nparts, plo, pcount;
   const PartTab* ptab;
+  // diagnostics (PHX_STEP_TIMES): %globaltimer after each grid step barrier
+  unsigned long long* tstamp;
+  int32_t tstamp_cap;
 };
 
 // status codes written by the kernel
