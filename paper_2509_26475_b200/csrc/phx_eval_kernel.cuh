@@ -1,0 +1,1054 @@
+// The persistent phimv_block kernel (phi_block.cpp:48-157, Alg. 3), sm_100a.
+// Template definitions; the variants are instantiated by phx_eval_q*.cu and
+// dispatched by phx_eval.cu.
+//
+// ONE cooperative launch per evaluation.  Every Taylor term is a grid step:
+// the CTAs sweep their row tiles, each lane group (G lanes of a warp, V = 1
+// or 2 adjacent columns per lane, Q column chunks) gathers the CSR row's
+// block rows (row-interleaved layout, one coalesced vector load per gathered
+// row), fuses the shift, scaling, J-term and accumulator updates with both
+// |.| row sums, and publishes a per-CTA max with one atomicMax; after
+// grid.sync() every CTA reads the two maxima and takes the same stopping
+// decision, so loop control never leaves the device.
+//
+// Compiled with --fmad=false (no FMA): bit-for-bit the oracle's operation
+// order (oracle/phx_oracle.cpp).  Row sums use the canonical
+// pairwise tree over pow2-padded natural column order: with V = 2 the
+// lane-local pair is the tree's first level, the butterfly the next ones.
+#include <cooperative_groups.h>
+
+#pragma once
+#include "phx_kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace phx {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int kMaxRW = 64;  // rows per warp tile
+constexpr double DBL_MAX_D = 1.7976931348623157e308;
+
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ double from_bits(unsigned long long b) {
+  return __longlong_as_double(static_cast<long long>(b));
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+
+template <int V>
+struct Vio;
+// ld/st: default caching (gather sources and their producers);
+// ldcs/stcs: evict-first streaming hints for the read-once / write-once
+// accumulator streams (Vw, S, E), so L2 keeps the gather targets
+template <>
+struct Vio<1> {
+  __device__ __forceinline__ static void ld(const double* p, double (&x)[1]) { x[0] = *p; }
+  __device__ __forceinline__ static void st(double* p, const double (&x)[1]) { *p = x[0]; }
+  __device__ __forceinline__ static void ldcs(const double* p, double (&x)[1]) { x[0] = __ldcs(p); }
+  __device__ __forceinline__ static void stcs(double* p, const double (&x)[1]) { __stcs(p, x[0]); }
+};
+template <>
+struct Vio<2> {
+  __device__ __forceinline__ static void ld(const double* p, double (&x)[2]) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    x[0] = t.x;
+    x[1] = t.y;
+  }
+  __device__ __forceinline__ static void st(double* p, const double (&x)[2]) {
+    *reinterpret_cast<double2*>(p) = make_double2(x[0], x[1]);
+  }
+  __device__ __forceinline__ static void ldcs(const double* p, double (&x)[2]) {
+    const double2 t = __ldcs(reinterpret_cast<const double2*>(p));
+    x[0] = t.x;
+    x[1] = t.y;
+  }
+  __device__ __forceinline__ static void stcs(double* p, const double (&x)[2]) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(x[0], x[1]));
+  }
+};
+
+template <int Q, int V, int R_>
+struct Cfg {
+  static constexpr int R = R_;  // rows per lane group per warp tile
+  // gather batch: entries in flight per lane group
+  static constexpr int B = (Q == 1 && V == 2 && R_ == 1) ? 8 : ((Q * V * R_ <= 4) ? 4 : 2);
+  // resident CTAs per SM the register budget is sized for
+  static constexpr int MINB = (Q * V * R_ <= 2) ? 4 : ((Q * V * R_ <= 4) ? 3 : ((Q * V <= 4) ? 2 : 1));
+};
+
+// Lane-group layout of one phase (S width or F width).
+struct Layout {
+  int G, gpw, g, lg, RW, qn, qp, width;
+};
+
+__device__ __forceinline__ Layout make_layout(int G, int qn, int width, int R, int V) {
+  Layout L;
+  const int lane = threadIdx.x & 31;
+  L.G = G;
+  L.gpw = 32 / G;
+  L.g = lane / G;
+  L.lg = lane % G;
+  L.RW = L.gpw * R;
+  L.qn = qn;
+  L.width = width;
+  const int chunk = 32 * V;  // columns per chunk q
+  int chunks = (width + chunk - 1) / chunk;
+  int qp = 1;
+  while (qp < chunks) qp <<= 1;
+  L.qp = width > chunk ? qp : 1;
+  return L;
+}
+
+// Canonical row sum of the group's |values| (pairwise tree over pow2-padded
+// natural column order; invalid lanes hold 0).
+template <int Q, int V>
+__device__ __forceinline__ double group_rowsum(const double (&v)[Q][V], int G, int qp) {
+  double T[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    double x = v[q][0];
+    if (V == 2) x = x + v[q][V - 1];
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1)
+      if (m < G) x = x + __shfl_xor_sync(kFull, x, m);  // G is warp-uniform
+    T[q] = x;
+  }
+#pragma unroll
+  for (int h = 1; h < Q; h <<= 1) {
+    if (h < qp) {
+#pragma unroll
+      for (int q = 0; q + h < Q; q += 2 * h) T[q] = T[q] + T[q + h];
+    }
+  }
+  return T[0];
+}
+
+// CTA max of two bit patterns -> one atomicMax each into the step's slot.
+__device__ __forceinline__ void publish2(unsigned long long a, unsigned long long b,
+                                         unsigned long long* slot,
+                                         unsigned long long (*red)[kWarps]) {
+  for (int m = 16; m >= 1; m >>= 1) {
+    a = umax64(a, __shfl_xor_sync(kFull, a, m));
+    b = umax64(b, __shfl_xor_sync(kFull, b, m));
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = a;
+    red[1][warp] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ma = 0, mb = 0;
+    for (int q = 0; q < kWarps; ++q) {
+      ma = umax64(ma, red[0][q]);
+      mb = umax64(mb, red[1][q]);
+    }
+    atomicMax(slot, ma);
+    atomicMax(slot + 1, mb);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Per-warp cp.async pipeline over the warp's sequence of row tiles.  While
+// tile s is computed, the CSR entries of tile s+1 and the row_ptr slice of
+// tile s+2 are in flight into warp-private shared memory (LDGSTS, no
+// registers held), so the row_ptr -> entries -> gather dependency chain costs
+// one round trip per tile instead of three.
+// ---------------------------------------------------------------------------
+constexpr int kEC = 160;  // staged CSR entries per warp tile
+
+struct WarpPipe {
+  int rp[3][kMaxRW + 1];
+  int ci[2][kEC];
+  double av[2][kEC];
+};
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// A phase's tiles come in two parts.  The first static_frac of the CTA tiles
+// are assigned round-robin (tile t to CTA t mod ncta; within it the warp takes
+// warp tiles warp, warp+8, ...: m of them) -- no atomics, neighbouring rows in
+// flight together.  The remaining warp tiles are grabbed one at a time from
+// the step's counter, so the CTAs that run faster absorb the tail instead of
+// waiting at the step barrier (per-CTA speed differs by up to ~20% and is
+// stable from step to step).  The two parts run as separate pipelined loops
+// so each keeps only its own state live.  Sequences are asked for positions in
+// increasing order, each at most twice in a row.
+struct TileSeq {
+  int m, ntiles, tile, RW, warp, cta, ncta;
+  __device__ __forceinline__ int at(int s, int) const {
+    const int t = cta + (s / m) * ncta;
+    return t < ntiles ? t * tile + (warp + (s % m) * kWarps) * RW : -1;
+  }
+};
+
+struct DynSeq {
+  int dyn0, dynN, RW, mpos, mval;
+  unsigned long long* ctr;
+  unsigned long long pend;  // lane 0: the grab in flight (issued one tile ahead)
+  // positions are asked for in order, the newest possibly twice (memoized)
+  __device__ __forceinline__ int at(int pos, int lane) {
+    if (pos == mpos) return mval;
+    const int id = dyn0 + int(__shfl_sync(kFull, pend, 0));
+    mpos = pos;
+    mval = id < dynN ? id * RW : -1;
+    if (id < dynN && lane == 0) pend = atomicAdd(ctr, 1ull);
+    return mval;
+  }
+};
+
+// static CTA tiles of a phase with ntiles tiles (the DYN kernels; the host
+// picks them when the CTAs get many tiles each -- DESIGN.md §4)
+__device__ __forceinline__ int static_tiles(const BlockArgs& a, int ntiles, int ncta) {
+  if (!(a.static_frac < 1.0)) return ntiles;
+  return min(ntiles, int(a.static_frac * double(ntiles) / double(ncta)) * ncta);
+}
+
+__device__ __forceinline__ void issue_rp(const BlockArgs& a, int* dst, int base, int RW, int lane) {
+  for (int l = lane; l <= RW; l += 32) cp_async4(dst + l, a.rp + min(base + l, a.n));
+}
+
+__device__ __forceinline__ void issue_entries(const BlockArgs& a, const int* rp, int RW, int* ci,
+                                              double* av, int lane) {
+  const int e_lo = rp[0], E = rp[RW] - e_lo;
+  if (E <= kEC)
+    for (int e = lane; e < E; e += 32) {
+      cp_async4(ci + e, a.ci + e_lo + e);
+      cp_async8(av + e, a.av + e_lo + e);
+    }
+}
+
+// body(base, rp, ci, av): rp = row_ptr[base .. base+RW] (clamped at n); when
+// rp[RW] - rp[0] <= kEC, ci/av hold the tile's entries from index 0.
+template <class Seq, class Body>
+__device__ __forceinline__ void pipelined(const BlockArgs& a, Seq& ts, int RW, WarpPipe& pp,
+                                          int lane, Body& body) {
+  const int b0 = ts.at(0, lane);
+  if (b0 < 0) return;  // warp-uniform
+  __syncwarp();
+  issue_rp(a, pp.rp[0], b0, RW, lane);
+  cp_commit();
+  cp_wait_all();
+  __syncwarp();
+  issue_entries(a, pp.rp[0], RW, pp.ci[0], pp.av[0], lane);
+  const int b1 = ts.at(1, lane);
+  if (b1 >= 0) issue_rp(a, pp.rp[1], b1, RW, lane);
+  cp_commit();
+  int base = b0;
+  for (int s = 0; base >= 0; ++s) {
+    cp_wait_all();
+    __syncwarp();  // tile s's entries and tile s+1's row_ptr have landed
+    const int nb = ts.at(s + 1, lane);
+    if (nb >= 0) {
+      issue_entries(a, pp.rp[(s + 1) % 3], RW, pp.ci[(s + 1) & 1], pp.av[(s + 1) & 1], lane);
+      const int nnb = ts.at(s + 2, lane);
+      if (nnb >= 0) issue_rp(a, pp.rp[(s + 2) % 3], nnb, RW, lane);
+    }
+    cp_commit();
+    body(base, pp.rp[s % 3], pp.ci[s & 1], pp.av[s & 1]);
+    __syncwarp();  // done with slot s before it is refilled
+    base = nb;
+  }
+}
+
+// every warp tile of a phase: the static part, then the dynamic tail from
+// counter ctr (zeroed before the phase's step began)
+template <bool DYN, class Body>
+__device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, int ntiles,
+                                          int warp, int cta, int ncta,
+                                          unsigned long long* ctr, WarpPipe& pp, int lane,
+                                          Body&& body) {
+  const int tst = DYN ? static_tiles(a, ntiles, ncta) : ntiles;
+  {
+    TileSeq ts;
+    ts.m = a.tile / (L.RW * kWarps);
+    ts.ntiles = tst;
+    ts.tile = a.tile;
+    ts.RW = L.RW;
+    ts.warp = warp;
+    ts.cta = cta;
+    ts.ncta = ncta;
+    pipelined(a, ts, L.RW, pp, lane, body);
+  }
+  if (DYN && tst < ntiles) {
+    DynSeq ds;
+    ds.dyn0 = tst * (a.tile / L.RW);
+    ds.dynN = (a.n + L.RW - 1) / L.RW;
+    ds.RW = L.RW;
+    ds.ctr = ctr;
+    ds.pend = 0;
+    ds.mpos = -1;
+    ds.mval = -1;
+    if (lane == 0) ds.pend = atomicAdd(ctr, 1ull);
+    pipelined(a, ds, L.RW, pp, lane, body);
+  }
+}
+
+// acc[rr][q][e] = sum over row rr's entries (storage order, from +0) of
+// av * X[col*ld + c].  X was written before the last grid.sync(), which
+// invalidates L1 (CCTL.IVALL), so plain cached loads are coherent.
+// PART: column indices are encoded (owner part << 27 | row within the owner)
+// and X is resolved per entry through the gather table Xt (one base pointer
+// per part: peer-GPU memory in a multi-GPU run).
+constexpr unsigned kOwnerShift = 27;
+constexpr unsigned kLocalMask = (1u << kOwnerShift) - 1u;
+
+template <bool PART>
+__device__ __forceinline__ const double* gather_row_ptr(const double* X,
+                                                        const double* const* Xt, unsigned enc,
+                                                        unsigned ld) {
+  if (PART) return Xt[enc >> kOwnerShift] + size_t(enc & kLocalMask) * ld;
+  return X + enc * ld;
+}
+
+template <int Q, int V, int R, int B, bool SMEM, bool PART>
+__device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const double* av_s,
+                                       int e_lo, unsigned ld, const int (&rs)[R],
+                                       const int (&cnt)[R], const double* X,
+                                       const double* const* Xt, const unsigned (&cq)[Q],
+                                       const bool (&vq)[Q], double (&acc)[R][Q][V]) {
+  int maxc = 0;
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) maxc = max(maxc, cnt[rr]);
+  for (int u0 = 0; u0 < maxc; u0 += B) {
+    double xv[B][R][Q][V];
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const bool ok = u0 + u < cnt[rr];
+        const double* xr = X;
+        if (ok) {
+          const int e = rs[rr] + u0 + u;
+          xr = gather_row_ptr<PART>(X, Xt, unsigned(SMEM ? ci[e] : __ldg(a.ci + e_lo + e)), ld);
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          if (ok && vq[q]) {
+            Vio<V>::ld(xr + cq[q], xv[u][rr][q]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) xv[u][rr][q][e] = 0.0;
+          }
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr)
+        if (u0 + u < cnt[rr]) {
+          const int e = rs[rr] + u0 + u;
+          const double av = SMEM ? av_s[e] : __ldg(a.av + e_lo + e);
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[rr][q][v] = acc[rr][q][v] + av * xv[u][rr][q][v];
+        }
+  }
+}
+
+template <int Q, int V, int R, int B, bool PART>
+__device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L, const int* rp,
+                                            const int* ci, const double* av, unsigned ld,
+                                            const double* X, const double* const* Xt,
+                                            const unsigned (&cq)[Q], const bool (&vq)[Q],
+                                            double (&acc)[R][Q][V]) {
+  const int e_lo = rp[0];
+  int rs[R], cnt[R];
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) {
+    const int li = rr * L.gpw + L.g;
+    rs[rr] = rp[li] - e_lo;
+    cnt[rr] = rp[li + 1] - rp[li];
+  }
+  if (rp[L.RW] - e_lo <= kEC)
+    gather<Q, V, R, B, true, PART>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
+  else
+    gather<Q, V, R, B, false, PART>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
+}
+
+template <int Q, int V, int RR, bool PART, bool DYN>
+__global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs ga) {
+  constexpr int R = Cfg<Q, V, RR>::R;
+  constexpr int B = Cfg<Q, V, RR>::B;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long red[2][kWarps];
+  __shared__ WarpPipe pipe[kWarps];
+  // gather tables [D0, D1, S, F0, F1][part] (PART only)
+  __shared__ const double* gtab[5][PART ? kMaxParts : 1];
+  __shared__ double gmax[2];
+  const double INF = __longlong_as_double(0x7FF0000000000000ll);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpPipe& pp = pipe[warp];
+
+  // Partitioned operator: this launch handles parts
+  // plo .. plo+pcount-1, CTAs split evenly; a CTA rebinds the row-local
+  // fields of its part (rows are part-local from here on).
+  // (unpartitioned: `a` aliases the kernel parameter, read from the constant
+  // bank; partitioned: a local copy with the part's fields)
+  BlockArgs pa;
+  int my = 0, cta = int(blockIdx.x), ncta = int(gridDim.x);
+  const PartTab* T = nullptr;
+  if (PART) {
+    pa = ga;
+    const int per = int(gridDim.x) / ga.pcount;
+    my = ga.plo + int(blockIdx.x) / per;
+    cta = int(blockIdx.x) % per;
+    ncta = per;
+    T = ga.ptab + my;
+    pa.n = T->nrows;
+    pa.rp = T->rp;
+    pa.ci = T->ci;
+    pa.av = T->av;
+    pa.V = T->V;
+    pa.Vw = T->Vw;
+    pa.D0 = T->D0;
+    pa.D1 = T->D1;
+    pa.S = T->S;
+    pa.F0 = T->F0;
+    pa.F1 = T->F1;
+    pa.E = T->E;
+    pa.W = T->W;
+    pa.slots = T->slots;
+    for (int q = threadIdx.x; q < ga.nparts; q += blockDim.x) {
+      const PartTab& U = ga.ptab[q];
+      gtab[0][q] = U.D0;
+      gtab[1][q] = U.D1;
+      gtab[2][q] = U.S;
+      gtab[3][q] = U.F0;
+      gtab[4][q] = U.F1;
+    }
+    __syncthreads();
+  }
+  const BlockArgs& a = PART ? pa : ga;
+  int dpar = 0, fpar = 0;  // D / F ping-pong parity (all parts swap in lockstep)
+
+  const int n = a.n, r = a.r, p = a.p;
+  const unsigned ldb = unsigned(a.ldb), ldf = unsigned(a.ldf);
+  const int ntiles = (n + a.tile - 1) / a.tile;
+  const bool has_xi = a.xi != 0.0;
+  const bool master = blockIdx.x == 0 && threadIdx.x == 0 && (!PART || ga.plo == 0);
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;  // writes this launch's status
+  const Layout LS = make_layout(a.GS, a.QS, a.w, R, V);
+  const Layout LF = make_layout(a.GF, a.QF, a.fcols, R, V);
+
+  int step = 0;
+  int tr_len = 0;
+  auto trace = [&](double kind, double x, double y) {
+    if (master && a.trace != nullptr && tr_len + 3 <= a.trace_cap) {
+      a.trace[tr_len] = kind;
+      a.trace[tr_len + 1] = x;
+      a.trace[tr_len + 2] = y;
+    }
+    tr_len += 3;
+  };
+  // publish this CTA's maxima, zero the next step's slot (its last readers
+  // finished before the previous grid sync), grid-sync, read the maxima
+  auto sync_step = [&](unsigned long long ma, unsigned long long mb, double& ra, double& rb) {
+    unsigned long long* slot = a.slots + 4 * (step % 3);
+    if (a.tstamp != nullptr && threadIdx.x == 0) {  // diagnostics: CTA arrival, SM id
+      const int q = kCtaStampBase + step * ncta + cta;
+      if (q < a.tstamp_cap) {
+        unsigned long long ns;
+        unsigned sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        a.tstamp[q] = (ns & ((1ull << 48) - 1ull)) | (static_cast<unsigned long long>(sm) << 48);
+      }
+    }
+    publish2(ma, mb, slot, red);
+    if (!PART) {
+      if (master) {
+        unsigned long long* nxt = a.slots + 4 * ((step + 1) % 3);
+        nxt[0] = 0ull;
+        nxt[1] = 0ull;
+        nxt[2] = 0ull;  // the next step's tile counter
+      }
+      grid.sync();
+      if (master && a.tstamp != nullptr && step < a.tstamp_cap) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        a.tstamp[step] = ns;
+      }
+      ra = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot)));
+      rb = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot + 1)));
+    } else {
+      // part-local arrival; the part's last CTA publishes the part maxima
+      // into every part's mailbox (peer memory); everyone waits for all parts
+      if (threadIdx.x == 0) {
+        const unsigned gen = unsigned(step) + 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(T->arrive + (step % 3), 1u);
+        if (old == unsigned(ncta) - 1u) {
+          __threadfence();
+          const unsigned long long A = __ldcg(slot), Bv = __ldcg(slot + 1);
+          unsigned long long* nxt = a.slots + 4 * ((step + 1) % 3);
+          nxt[0] = 0ull;
+          nxt[1] = 0ull;
+          nxt[2] = 0ull;  // the part's next tile counter
+          T->arrive[(step + 1) % 3] = 0u;
+          // mailboxes are double-buffered by step parity: a part can run one
+          // step ahead and must not overwrite what a slower part still reads
+          const int buf = (step & 1) * ga.nparts;
+          for (int q = 0; q < ga.nparts; ++q) {
+            MailBox* mbx = ga.ptab[q].mbox + buf + my;
+            mbx->a = A;
+            mbx->b = Bv;
+          }
+          __threadfence_system();
+          for (int q = 0; q < ga.nparts; ++q)
+            atomicExch(&(ga.ptab[q].mbox + buf + my)->gen, gen);
+        }
+        unsigned long long A = 0, Bv = 0;
+        for (int q = 0; q < ga.nparts; ++q) {
+          const MailBox* mbx = T->mbox + (step & 1) * ga.nparts + q;
+          while (atomicAdd(const_cast<unsigned*>(&mbx->gen), 0u) < gen) {
+          }
+          __threadfence_system();
+          A = umax64(A, __ldcg(&mbx->a));
+          Bv = umax64(Bv, __ldcg(&mbx->b));
+        }
+        gmax[0] = from_bits(A);
+        gmax[1] = from_bits(Bv);
+        __threadfence();  // invalidates L1 before the next step's gathers
+      }
+      __syncthreads();
+      ra = gmax[0];
+      rb = gmax[1];
+    }
+    ++step;
+  };
+  auto finish = [&](int err, int idx, int L_S, int extra_steps) {
+    if (lead) {
+      a.status[0] = err;
+      a.status[1] = idx;
+      a.status[2] = L_S;
+      a.status[3] = 0;
+      a.status[4] = step + extra_steps;
+      a.status[5] = min(tr_len, a.trace_cap);
+    }
+  };
+  // lane column offsets (first column of each chunk) and chunk validity
+  auto cols = [&](const Layout& L, unsigned (&c)[Q], bool (&v)[Q]) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      c[q] = unsigned(V * (L.lg + L.G * q));
+      v[q] = (q < L.qn) && (int(c[q]) < L.width);
+    }
+  };
+
+  // ================= init: Vw = V[src]*g, D = S = Vw (phi_block.cpp:76-92)
+  unsigned long long m0 = 0, mv = 0;  // max |Vw| row sum; max |V| entry (finiteness)
+  {
+    unsigned c[Q];
+    bool v[Q];
+    cols(LS, c, v);
+    for (int t = cta; t < ntiles; t += ncta)
+      for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+        const int base = t * a.tile + wt * LS.RW;
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = base + rr * LS.gpw + LS.g;
+          const bool rv = row < n;
+          double x[Q][V], ax[Q][V];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+              x[q][e] = 0.0;
+              if (rv && v[q]) {
+                const int cc = int(c[q]) + e;
+                const int j = cc / r, i = cc - j * r;
+                const int src = j == 0 ? 0 : p + 1 - j;
+                const double vraw = __ldg(a.V + size_t(src) * size_t(n) + row);
+                mv = umax64(mv, abs_bits(vraw));
+                x[q][e] = vraw * __ldg(a.g + i);
+              }
+              ax[q][e] = fabs(x[q][e]);
+            }
+            if (rv && v[q]) {
+              const unsigned o = unsigned(row) * ldb + c[q];
+              Vio<V>::st(a.Vw + o, x[q]);
+              Vio<V>::st(a.D0 + o, x[q]);
+              Vio<V>::st(a.S + o, x[q]);
+            }
+          }
+          const double rsum = group_rowsum<Q, V>(ax, LS.G, LS.qp);
+          if (rv) m0 = umax64(m0, abs_bits(rsum));
+        }
+      }
+  }
+  double mD, mSn;
+  sync_step(m0, mv, mD, mSn);
+  if (!(mSn <= DBL_MAX_D)) {  // a non-finite entry of V (check_request, phi_block.cpp:25-26)
+    finish(kStInputNonFinite, 0, 1, 0);
+    return;
+  }
+  double c1 = INF, c2 = mD, nS = mD;  // c2 = inf_norm(D) = ||S|| at k = 1 (S = D = Vw)
+  trace(0.0, c2, nS);
+
+  // ================= S series (phi_block.cpp:93-106)
+  int k = 1;
+  double sigma = 1.0;
+  double* Dc = a.D0;
+  double* Dn = a.D1;
+  int err = kStOk, err_idx = 0;
+  const bool vwl_vec = V == 2 && (r % 2) == 0;
+  while (c1 + c2 > a.tol * nS) {
+    if (k >= 500) {
+      err = kStSeriesCap;
+      err_idx = 500;
+      break;
+    }
+    ++k;
+    c1 = c2;
+    sigma *= k;
+    unsigned long long mdb = 0, msb = 0;
+    {
+      unsigned c[Q];
+      bool v[Q];
+      cols(LS, c, v);
+      int jj[Q][V];
+      double kd[Q][V], ka[Q][V], tos[Q][V];
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const int cc = int(c[q]) + e;
+          jj[q][e] = v[q] ? cc / r : 0;
+          kd[q][e] = v[q] ? __ldg(a.colKd + cc) : 0.0;
+          ka[q][e] = v[q] ? __ldg(a.colKa + cc) : 0.0;
+          tos[q][e] = v[q] ? __ldg(a.colTos + cc) : 0.0;
+        }
+      run_tiles<DYN>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+                [&](int base, const int* rp, const int* ci, const double* avs) {
+          // row-local streams first (independent of the CSR slice)
+          double vw[R][Q][V], vwl[R][Q][V], so[R][Q][V], ds[R][Q][V], acc[R][Q][V];
+          bool vq[R][Q];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              vq[rr][q] = row < n && v[q];
+              const unsigned o = unsigned(row) * ldb + c[q];
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                vw[rr][q][e] = vwl[rr][q][e] = so[rr][q][e] = ds[rr][q][e] = 0.0;
+                acc[rr][q][e] = 0.0;
+              }
+              if (vq[rr][q]) {
+                Vio<V>::ldcs(a.Vw + o, vw[rr][q]);
+                Vio<V>::ldcs(a.S + o, so[rr][q]);
+                if (has_xi) Vio<V>::ld(Dc + o, ds[rr][q]);
+                if (vwl_vec) {
+                  if (jj[q][0] >= 2) Vio<V>::ld(a.Vw + (o - unsigned(r)), vwl[rr][q]);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < V; ++e)
+                    if (jj[q][e] >= 2) vwl[rr][q][e] = a.Vw[o + e - unsigned(r)];
+                }
+              }
+            }
+          }
+          gather_tile<Q, V, R, B, PART>(a, LS, rp, ci, avs, ldb, Dc, gtab[dpar], c, v, acc);
+          double vn[R][Q][V], dn[R][Q][V], sn[R][Q][V];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                // Vw = Vw * Kiter: ascending source column from +0 (:98)
+                double g2 = 0.0;
+                if (jj[q][e] >= 2) g2 = g2 + vwl[rr][q][e] * ka[q][e];
+                g2 = g2 + vw[rr][q][e] * kd[q][e];
+                vn[rr][q][e] = g2;
+                // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
+                double y = acc[rr][q][e];
+                if (has_xi) y = y - a.xi * ds[rr][q][e];
+                y = y * tos[q][e];
+                dn[rr][q][e] = y + g2;
+                sn[rr][q][e] = so[rr][q][e] + dn[rr][q][e] / sigma;  // S += D/sigma (:105)
+              }
+          __syncwarp();  // every lane has read its Vw[c - r] before any lane writes Vw
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
+            double ad[Q][V], as[Q][V];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              if (vq[rr][q]) {
+                const unsigned o = unsigned(row) * ldb + c[q];
+                Vio<V>::stcs(a.Vw + o, vn[rr][q]);
+                Vio<V>::st(Dn + o, dn[rr][q]);
+                Vio<V>::stcs(a.S + o, sn[rr][q]);
+              }
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                ad[q][e] = vq[rr][q] ? fabs(dn[rr][q][e]) : 0.0;
+                as[q][e] = vq[rr][q] ? fabs(sn[rr][q][e]) : 0.0;
+              }
+            }
+            const double rd = group_rowsum<Q, V>(ad, LS.G, LS.qp);
+            const double rsm = group_rowsum<Q, V>(as, LS.G, LS.qp);
+            if (row < n) {
+              mdb = umax64(mdb, abs_bits(rd));
+              msb = umax64(msb, abs_bits(rsm));
+            }
+          }
+                });
+    }
+    double maxD, maxS;
+    sync_step(mdb, msb, maxD, maxS);
+    c2 = maxD / sigma;  // :103
+    if (!isfinite(c2)) {
+      err = kStSeriesDiverged;
+      err_idx = k;
+      break;
+    }
+    nS = maxS;
+    trace(1.0, c2, nS);
+    double* tmp = Dc;
+    Dc = Dn;
+    Dn = tmp;
+    dpar ^= 1;
+  }
+  const int L_S = k;
+  if (err != kStOk) {
+    finish(err, err_idx, L_S, 0);
+    return;
+  }
+
+  // ================= promotion (phi_block.cpp:109-120)
+  // F_L = fl(fl(A S_L * t_i) + v0) (unshifted A), F_R = S block p.
+  double* Fc = a.F0;
+  double* Fn = a.F1;
+  const bool sweeps = a.s_eff > 1;
+  unsigned long long mf = 0;
+  {
+    unsigned c[Q];
+    bool v[Q], vl[Q];
+    cols(LF, c, v);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) vl[q] = v[q] && int(c[q]) < r;
+    run_tiles<DYN>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+              [&](int base, const int* rp, const int* ci, const double* avs) {
+        double acc[R][Q][V];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[rr][q][e] = 0.0;
+        // gathers S block-0 columns (left F columns live at the same column
+        // index in S); a pair straddling the left/right split gathers one
+        // extra column, unused
+        gather_tile<Q, V, R, B, PART>(a, LF, rp, ci, avs, ldb, a.S, gtab[2], c, vl, acc);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = base + rr * LF.gpw + LF.g;
+          const bool rv = row < n;
+          double f[Q][V], af[Q][V];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+              f[q][e] = 0.0;
+              const int cc = int(c[q]) + e;
+              if (rv && v[q]) {
+                const int i = cc < r ? cc : cc - r;
+                const size_t srow = size_t(row) * ldb + size_t(p) * size_t(r);
+                if (cc < r) {
+                  const double sc = acc[rr][q][e] * __ldg(a.t + i);
+                  f[q][e] = sc + __ldg(a.V + row);
+                } else {
+                  f[q][e] = a.S[srow + i];
+                }
+                if (!sweeps && cc < r) {
+                  // assembly W = F_L + fl(F_R * alpha) (:148-154)
+                  double wv = f[q][e];
+                  double fr = 0.0;
+                  if (p > 0) {
+                    fr = a.S[srow + i];
+                    wv = wv + fr * __ldg(a.alpha + i);
+                  }
+                  a.W[size_t(i) * size_t(n) + row] = wv;
+                  if (a.FLo) a.FLo[size_t(i) * size_t(n) + row] = f[q][e];
+                  if (a.FRo) a.FRo[size_t(i) * size_t(n) + row] = fr;
+                }
+              }
+              af[q][e] = fabs(f[q][e]);
+            }
+            if (sweeps && rv && v[q]) {
+              const unsigned o = unsigned(row) * ldf + c[q];
+              Vio<V>::st(Fc + o, f[q]);
+              Vio<V>::st(a.E + o, f[q]);
+            }
+          }
+          if (sweeps) {
+            const double rf = group_rowsum<Q, V>(af, LF.G, LF.qp);
+            if (rv) mf = umax64(mf, abs_bits(rf));
+          }
+        }
+              });
+  }
+  if (!sweeps) {
+    finish(kStOk, 0, L_S, 1);
+    return;
+  }
+  double fnorm, dummy;
+  sync_step(mf, mf, fnorm, dummy);
+
+  // ================= recovery sweeps (phi_block.cpp:122-146)
+  for (int sweep = 1; sweep < a.s_eff; ++sweep) {
+    int kk = 0;
+    double d1 = INF, d2 = fnorm, nE = fnorm;  // E = F
+    trace(2.0, d2, nE);
+    while (d1 + d2 > a.tol * nE) {
+      if (kk >= 300) {
+        err = kStRecoveryCap;
+        err_idx = 300;
+        break;
+      }
+      ++kk;
+      d1 = d2;
+      const double fac = a.single_variant ? a.t_single / (double(a.s_eff) * kk) : 0.0;
+      unsigned long long mfb = 0, meb = 0;
+      {
+        unsigned c[Q];
+        bool v[Q];
+        double tosF[Q][V];
+        cols(LF, c, v);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            const int cc = int(c[q]) + e;
+            const int i = cc < r ? cc : cc - r;
+            tosF[q][e] = v[q] ? __ldg(a.colTos + i) : 0.0;
+          }
+        run_tiles<DYN>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+                  [&](int base, const int* rp, const int* ci, const double* avs) {
+            double eo[R][Q][V], fs[R][Q][V], acc[R][Q][V];
+            bool vq[R][Q];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              const int row = base + rr * LF.gpw + LF.g;
+#pragma unroll
+              for (int q = 0; q < Q; ++q) {
+                vq[rr][q] = row < n && v[q];
+                const unsigned o = unsigned(row) * ldf + c[q];
+#pragma unroll
+                for (int e = 0; e < V; ++e) eo[rr][q][e] = fs[rr][q][e] = acc[rr][q][e] = 0.0;
+                if (vq[rr][q]) {
+                  Vio<V>::ldcs(a.E + o, eo[rr][q]);
+                  if (has_xi) Vio<V>::ld(Fc + o, fs[rr][q]);
+                }
+              }
+            }
+            gather_tile<Q, V, R, B, PART>(a, LF, rp, ci, avs, ldf, Fc, gtab[3 + fpar], c, v, acc);
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              const int row = base + rr * LF.gpw + LF.g;
+              double y[Q][V], en[Q][V], ay[Q][V], ae[Q][V];
+#pragma unroll
+              for (int q = 0; q < Q; ++q) {
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                  double yv = acc[rr][q][e];
+                  if (has_xi) yv = yv - a.xi * fs[rr][q][e];
+                  if (a.single_variant) {
+                    yv = fac * yv;  // phi_single.cpp:106
+                  } else {
+                    yv = yv / double(kk);  // phi_block.cpp:132
+                    yv = yv * tosF[q][e];  // :134-135
+                  }
+                  y[q][e] = yv;
+                  en[q][e] = eo[rr][q][e] + yv;  // E += F (:138)
+                  ay[q][e] = vq[rr][q] ? fabs(yv) : 0.0;
+                  ae[q][e] = vq[rr][q] ? fabs(en[q][e]) : 0.0;
+                }
+                if (vq[rr][q]) {
+                  const unsigned o = unsigned(row) * ldf + c[q];
+                  Vio<V>::st(Fn + o, y[q]);
+                  Vio<V>::stcs(a.E + o, en[q]);
+                }
+              }
+              const double ry = group_rowsum<Q, V>(ay, LF.G, LF.qp);
+              const double re = group_rowsum<Q, V>(ae, LF.G, LF.qp);
+              if (row < n) {
+                mfb = umax64(mfb, abs_bits(ry));
+                meb = umax64(meb, abs_bits(re));
+              }
+            }
+                  });
+      }
+      double maxF2, maxE;
+      sync_step(mfb, meb, maxF2, maxE);
+      d2 = maxF2;
+      if (!isfinite(d2)) {
+        err = kStRecoveryDiverged;
+        err_idx = kk;
+        break;
+      }
+      nE = maxE;
+      trace(3.0, d2, nE);
+      double* tmp = Fc;
+      Fc = Fn;
+      Fn = tmp;
+      fpar ^= 1;
+    }
+    if (err != kStOk) break;
+    if (lead) a.lensF[sweep - 1] = kk;
+
+    // ---- sweep end (:141-145): E *= mu; Sadv = Sadv*Jexp; F refresh
+    // phase A (S layout): Sadv blocks 1..p in place, ascending source column
+    {
+      unsigned c[Q];
+      bool v[Q];
+      cols(LS, c, v);
+      for (int t = cta; t < ntiles; t += ncta)
+        for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+          const int base = t * a.tile + wt * LS.RW;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
+            double nv[Q][V];
+            bool wq[Q][V];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                const int cc = int(c[q]) + e;
+                const int j = v[q] ? cc / r : 0, i = cc - j * r;
+                wq[q][e] = row < n && v[q] && j >= 1;
+                nv[q][e] = 0.0;
+                if (wq[q][e]) {
+                  const double* srow = a.S + size_t(row) * ldb;
+                  const double* cj = a.jc + size_t(i) * size_t(p + 1);
+                  double accv = 0.0;
+                  for (int l = 1; l <= j; ++l) accv = accv + srow[l * r + i] * __ldg(cj + (j - l));
+                  nv[q][e] = accv;
+                }
+              }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e)
+                if (wq[q][e]) a.S[size_t(row) * ldb + c[q] + e] = nv[q][e];
+          }
+        }
+    }
+    __syncthreads();
+    // phase B (F layout): F_L = E_L*mu, F_R = E_R*mu + Sadv_p; E = F
+    const bool last = sweep == a.s_eff - 1;
+    unsigned long long mfe = 0;
+    {
+      unsigned c[Q];
+      bool v[Q];
+      cols(LF, c, v);
+      for (int t = cta; t < ntiles; t += ncta)
+        for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
+          const int base = t * a.tile + wt * LF.RW;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LF.gpw + LF.g;
+            const bool rv = row < n;
+            double f[Q][V], af[Q][V];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                f[q][e] = 0.0;
+                const int cc = int(c[q]) + e;
+                if (rv && v[q]) {
+                  const int i = cc < r ? cc : cc - r;
+                  const size_t srow = size_t(row) * ldb + size_t(p) * size_t(r);
+                  const double en = a.E[size_t(row) * ldf + cc] * __ldg(a.mu + i);
+                  double fv = en;
+                  if (cc >= r) fv = en + a.S[srow + i];
+                  f[q][e] = fv;
+                  if (last && cc < r) {
+                    double wv = fv;
+                    double fr = 0.0;
+                    if (p > 0) {
+                      const double er = a.E[size_t(row) * ldf + r + i] * __ldg(a.mu + i);
+                      fr = er + a.S[srow + i];
+                      wv = wv + (a.single_variant ? __ldg(a.alpha + i) * fr : fr * __ldg(a.alpha + i));
+                    }
+                    a.W[size_t(i) * size_t(n) + row] = wv;
+                    if (a.FLo) a.FLo[size_t(i) * size_t(n) + row] = fv;
+                    if (a.FRo) a.FRo[size_t(i) * size_t(n) + row] = fr;
+                  }
+                }
+                af[q][e] = (rv && v[q]) ? fabs(f[q][e]) : 0.0;
+              }
+            if (!last) {
+              __syncwarp();
+#pragma unroll
+              for (int q = 0; q < Q; ++q)
+                if (rv && v[q]) {
+                  const unsigned o = unsigned(row) * ldf + c[q];
+                  Vio<V>::st(Fc + o, f[q]);
+                  Vio<V>::st(a.E + o, f[q]);
+                }
+              const double rf = group_rowsum<Q, V>(af, LF.G, LF.qp);
+              if (rv) mfe = umax64(mfe, abs_bits(rf));
+            }
+          }
+        }
+    }
+    if (!last) {
+      double dmy;
+      sync_step(mfe, mfe, fnorm, dmy);
+    }
+  }
+  finish(err, err_idx, L_S, 0);
+}
+
+template <int Q, int V, int R, bool PART, bool DYN>
+cudaError_t eval_occupancy(int block, int* per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_phimv_block<Q, V, R, PART, DYN>,
+                                                       block, 0);
+}
+
+template <int Q, int V, int R, bool PART, bool DYN>
+EvalKernel eval_kernel() {
+  return EvalKernel{reinterpret_cast<const void*>(k_phimv_block<Q, V, R, PART, DYN>),
+                    eval_occupancy<Q, V, R, PART, DYN>};
+}
+
+}  // namespace
+
+// one instantiated (Q, V, R): unpartitioned static or dynamic-tail kernels,
+// partitioned kernels always with the dynamic tail
+#define PHX_EVAL_CASE(q, v, r)                                 \
+  if (QT == q && V == v && R == r) {                           \
+    if (part)                                                  \
+      *out = eval_kernel<q, v, r, true, true>();               \
+    else if (dyn)                                              \
+      *out = eval_kernel<q, v, r, false, true>();              \
+    else                                                       \
+      *out = eval_kernel<q, v, r, false, false>();             \
+    return true;                                               \
+  }
+
+}  // namespace phx

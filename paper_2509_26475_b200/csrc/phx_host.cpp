@@ -177,6 +177,9 @@ struct phx_basis_s {
 
 namespace {
 
+// tiles per co-resident CTA from which the dynamic-tail kernel is used
+constexpr int kDynTilesPerCta = 64;
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -600,14 +603,14 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     T.F1 = d.F1.as<double>(nr * size_t(ldf));
     T.E = d.E.as<double>(nr * size_t(ldf));
     T.W = d.W.as<double>(nr * size_t(r));
-    T.slots = d.slots.as<unsigned long long>(6);
+    T.slots = d.slots.as<unsigned long long>(12);
     T.arrive = d.arrive.as<unsigned>(3);
     T.mbox = d.mbox.as<phx::MailBox>(2 * size_t(P));  // [step parity][part]
     T.row0 = int32_t(d.row0);
     T.nrows = int32_t(d.nrows);
     PHX_CUDA(cudaMemcpy2DAsync(dV, nr * 8, in.hV + d.row0, size_t(in.ldv) * 8, nr * 8,
                                size_t(p + 1), cudaMemcpyHostToDevice, d.stream));
-    PHX_CUDA(cudaMemsetAsync(T.slots, 0, 6 * sizeof(unsigned long long), d.stream));
+    PHX_CUDA(cudaMemsetAsync(T.slots, 0, 12 * sizeof(unsigned long long), d.stream));
     PHX_CUDA(cudaMemsetAsync(T.arrive, 0, 3 * sizeof(unsigned), d.stream));
     PHX_CUDA(cudaMemsetAsync(T.mbox, 0, 2 * size_t(P) * sizeof(phx::MailBox), d.stream));
     double* dc = d.coef.as<double>(ncoef);
@@ -673,7 +676,7 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     a.trace_cap = int32_t(trace_cap);
     PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), d.stream));
     int max_blocks = 0;
-    PHX_CUDA(phx::coop_grid_size(a.QT, a.vec, a.R, true, block, &max_blocks));
+    PHX_CUDA(phx::coop_grid_size(a.QT, a.vec, a.R, true, true, block, &max_blocks));
     int64_t most = 1;
     for (int q = g.plo; q < g.plo + g.pcount; ++q)
       most = std::max<int64_t>(most, (op->parts[size_t(q)].nrows + a.tile - 1) / a.tile);
@@ -812,6 +815,13 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   const double avg_nnz = double(op->nnz) / double(n);
   const int32_t R = (QT == 1 && (V == 1 || avg_nnz < 2.5)) ? 2 : 1;
   const int32_t tile = 8 * (32 / std::min(GS, GF)) * R;
+  // share of each phase's tiles assigned statically (the rest are grabbed
+  // dynamically to absorb per-CTA speed differences); PHX_STATIC_FRAC tunes it
+  static const double static_frac = [] {
+    const char* e = std::getenv("PHX_STATIC_FRAC");
+    const double f = e ? std::atof(e) : 0.8;
+    return (f >= 0.0 && f <= 1.0) ? f : 0.8;
+  }();
 
   const int64_t nsw = s_eff - 1;
   int32_t* h_status = nullptr;
@@ -836,6 +846,8 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
     b.vec = V;
     b.R = R;
     b.tile = tile;
+    b.static_frac = static_frac;
+    b.dyn = 1;
     b.xi = xi;
     b.tol = tol;
     b.s_eff = int32_t(s_eff);
@@ -872,6 +884,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.vec = V;
   a.R = R;
   a.tile = tile;
+  a.static_frac = static_frac;
   a.xi = xi;
   a.tol = tol;
   a.s_eff = int32_t(s_eff);
@@ -898,12 +911,12 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.W = in.dW ? in.dW : op->W.as<double>(size_t(n) * size_t(r));
   a.FLo = in.h_exp_v0 ? op->FLo.as<double>(size_t(n) * size_t(r)) : nullptr;
   a.FRo = in.h_tail ? op->FRo.as<double>(size_t(n) * size_t(r)) : nullptr;
-  a.slots = op->slots.as<unsigned long long>(6);  // [3][maxA, maxB]
+  a.slots = op->slots.as<unsigned long long>(12);  // [3][maxA, maxB, tile counter, pad]
   a.status = op->status.as<int32_t>(8);
   a.lensF = op->lensF.as<int32_t>(size_t(std::max<long>(1, s_eff - 1)));
   a.nparts = 1;
   static const bool step_times = std::getenv("PHX_STEP_TIMES") != nullptr;
-  a.tstamp_cap = step_times ? 1 << 16 : 0;
+  a.tstamp_cap = step_times ? 1 << 20 : 0;
   a.tstamp = step_times ? op->tstamp.as<unsigned long long>(size_t(a.tstamp_cap)) : nullptr;
   if (step_times) PHX_CUDA(cudaMemsetAsync(a.tstamp, 0, size_t(a.tstamp_cap) * 8, st));
   a.trace = trace_cap > 0 ? op->trace.as<double>(size_t(trace_cap)) : nullptr;
@@ -921,12 +934,17 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
     a.V = dV;
   }
   PHX_CUDA(cudaMemcpyAsync(d_coef, coef.data(), ncoef * 8, cudaMemcpyHostToDevice, st));
-  PHX_CUDA(cudaMemsetAsync(a.slots, 0, 6 * sizeof(unsigned long long), st));
+  PHX_CUDA(cudaMemsetAsync(a.slots, 0, 12 * sizeof(unsigned long long), st));
   PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), st));
 
   int max_blocks = 0;
-  PHX_CUDA(phx::coop_grid_size(QT, V, R, false, block, &max_blocks));
+  PHX_CUDA(phx::coop_grid_size(QT, V, R, false, false, block, &max_blocks));
   const int64_t ntiles = (n + tile - 1) / tile;
+  // the dynamic-tail kernel when the CTAs get many tiles each: per-CTA speed
+  // differs by up to ~20% on long steps; on short ones the tail grabs and the
+  // larger kernel cost more than they balance
+  a.dyn = ntiles >= int64_t(kDynTilesPerCta) * max_blocks ? 1 : 0;
+  if (a.dyn) PHX_CUDA(phx::coop_grid_size(QT, V, R, false, true, block, &max_blocks));
   // developer knob for tuning studies: PHX_GRID_FRAC = fraction (0, 1] of the
   // co-resident CTA count to launch
   static const double grid_frac = [] {
@@ -947,6 +965,14 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
     for (size_t q = 1; q < ts.size() && ts[q] != 0 && q < 48; ++q)
       std::fprintf(stderr, " %.1f", double(ts[q] - ts[q - 1]) * 1e-3);
     std::fprintf(stderr, "\n");
+    if (const char* path = std::getenv("PHX_CTA_TIMES")) {  // raw CTA arrivals
+      if (FILE* f = std::fopen(path, "wb")) {
+        const int32_t hdr[2] = {grid, phx::kCtaStampBase};
+        std::fwrite(hdr, sizeof hdr, 1, f);
+        std::fwrite(ts.data(), 8, ts.size(), f);
+        std::fclose(f);
+      }
+    }
   }
 
   h_status = op->h_small.as<int32_t>(8);

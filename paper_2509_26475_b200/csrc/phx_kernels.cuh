@@ -11,7 +11,8 @@ namespace phx {
 constexpr int kChunk = 4096;       // stableNorm block (Eigen blocking)
 constexpr int kNormThreads = 256;  // canonical lane count of a chunk
 
-constexpr int kMaxParts = 16;  // row parts of a partitioned operator
+constexpr int kMaxParts = 16;
+constexpr int kCtaStampBase = 4096;  // diagnostics layout of BlockArgs::tstamp  // row parts of a partitioned operator
 
 // Cross-part step mailbox: part p's leader writes (a, b) then gen into slot
 // p of every part's mailbox array (peer memory in a multi-GPU run).
@@ -37,7 +38,7 @@ struct PartTab {
   double* F1;
   double* E;
   double* W;
-  unsigned long long* slots;  // [3][2]
+  unsigned long long* slots;  // [3][4]
   unsigned* arrive;           // [3]
   MailBox* mbox;              // [2 step parities][nparts]
   int32_t row0, nrows;
@@ -58,6 +59,8 @@ struct BlockArgs {
   int32_t vec;     // adjacent columns per lane (2 when both widths are even)
   int32_t R;       // rows per lane group per warp tile (1 or 2; 2 only when QT == 1)
   int32_t tile;    // rows per tile (row -> CTA mapping, independent of layout)
+  int32_t dyn;          // 1: dynamic-tail kernel (always for partitioned runs)
+  double static_frac;  // DYN kernels: share of a phase's CTA tiles assigned statically
   // scalars
   double xi, tol;
   int32_t s_eff;
@@ -87,7 +90,7 @@ struct BlockArgs {
   double* FLo;  // optional n x r exp_v0 (single variant), ld n
   double* FRo;  // optional n x r tail, ld n
   // control
-  unsigned long long* slots;  // [3][2] ring of per-step row-sum maxima
+  unsigned long long* slots;  // [3][4] ring: row-sum maxima A, B, tile counter, pad
   int32_t* status;            // [8]: code, index, L_S, sweeps done, steps
   int32_t* lensF;             // [s_eff-1]
   double* trace;              // optional (kind, a, b) triples
@@ -97,6 +100,8 @@ struct BlockArgs {
   int32_t nparts, plo, pcount;
   const PartTab* ptab;
   // diagnostics (PHX_STEP_TIMES): %globaltimer after each grid step barrier
+  // at [step]; CTA arrivals (time mod 2^48 | smid << 48) at
+  // [kCtaStampBase + step * ncta + cta]
   unsigned long long* tstamp;
   int32_t tstamp_cap;
 };
@@ -113,7 +118,20 @@ enum : int32_t {
 
 // launch wrappers (phx_kernels.cu)
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st);
-cudaError_t coop_grid_size(int QT, int V, int R, bool part, int block, int* max_blocks);
+cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, int block, int* max_blocks);
+
+// one instantiated kernel variant and its occupancy query
+struct EvalKernel {
+  const void* fn;
+  cudaError_t (*occ)(int block, int* per_sm);
+};
+// per-file variant tables (phx_eval_q*.cu): true when the file holds the
+// variant (QT, V, R, partitioned, dynamic tail)
+bool eval_kernels_q1v1(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
+bool eval_kernels_q1v2(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
+bool eval_kernels_q2(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
+bool eval_kernels_q4(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
+bool eval_kernels_q8(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
 
 // y = f(A x) with mode 0: A x, 1: A x - fl(xi x), 2: (A x) / div ; fused
 // per-chunk max|y| into chunkmax (bit patterns) when chunkmax != nullptr

@@ -17,7 +17,7 @@ def pytest_configure(config):
     if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
     if not os.path.exists(os.path.join(ROOT, "paper_2509_26475_b200", "lib", "libphx.so")):
-        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2509_26475_b200", "csrc")],
+        subprocess.run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "paper_2509_26475_b200", "csrc")],
                        check=True)
 
 
