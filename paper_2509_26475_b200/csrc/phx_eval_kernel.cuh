@@ -191,10 +191,10 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_grou
 // so each keeps only its own state live.  Sequences are asked for positions in
 // increasing order, each at most twice in a row.
 struct TileSeq {
-  int m, ntiles, tile, RW, warp, cta, ncta;
+  int mlog, ntiles, tile, RW, warp, cta, ncta;  // m = 1 << mlog warp tiles per CTA tile
   __device__ __forceinline__ int at(int s, int) const {
-    const int t = cta + (s / m) * ncta;
-    return t < ntiles ? t * tile + (warp + (s % m) * kWarps) * RW : -1;
+    const int t = cta + (s >> mlog) * ncta;
+    return t < ntiles ? t * tile + (warp + (s & ((1 << mlog) - 1)) * kWarps) * RW : -1;
   }
 };
 
@@ -277,7 +277,7 @@ __device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, i
   const int tst = DYN ? static_tiles(a, ntiles, ncta) : ntiles;
   {
     TileSeq ts;
-    ts.m = a.tile / (L.RW * kWarps);
+    ts.mlog = __ffs(a.tile / (L.RW * kWarps)) - 1;  // a power of two: G / min(GS, GF)
     ts.ntiles = tst;
     ts.tile = a.tile;
     ts.RW = L.RW;
