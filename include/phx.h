@@ -171,6 +171,41 @@ phx_status phx_phimv(phx_op op, double t, double alpha, int32_t p, const double*
                      double* tail, phx_run_record* rec);
 
 /* ---------------------------------------------------------------------------
+ * The evaluator's consumer: the fourth-order six-stage
+ * exponential Runge-Kutta integrator on the 2D advection-diffusion-reaction
+ * problem.
+ */
+
+/* adr_build (problems.hpp:46-70, problems.cpp:184-250) as CSR: n = nx*ny
+ * rows, at most 5n entries (row_ptr n+1, col_idx / vals nnz = row_ptr[n]),
+ * columns ascending; u0 (n) is the reference's initial condition bit for bit.
+ * Any output pointer may be NULL.  PHX_EINVAL when nx < 8 or ny < 8
+ * ("adr_build: grid must be at least 8x8").  Host-only (no device work). */
+phx_status phx_adr_csr(int32_t nx, int32_t ny, double eps, double alpha_adv, int64_t* row_ptr,
+                       int32_t* col_idx, double* vals, double* u0);
+
+/* exprk4s6_step (integrator.hpp:36-38, integrator.cpp:29-105): one step of
+ * size h from u (host, n) with reaction gamma*u*(u-1/2)*(1-u); four block
+ * evaluations {U2}, {U3,U4}, {U5,U6}, {u_next} sharing params.  recs: NULL or
+ * 4 records (one per evaluator call, StepRecord::calls).  Single-device
+ * operators only. */
+phx_status phx_exprk4s6_step(phx_op op, double gamma, const double* u, double h, double tol,
+                             const phx_scaling_shift* params, double* u_next,
+                             phx_run_record* recs);
+
+/* integrate (integrator.hpp:47-49, integrator.cpp:107-134): fixed-step
+ * integration from t = 0 to t_end with the state resident on the device.
+ * u_out (n) receives the final state (the last finite one on failure);
+ * t_out the time reached; n_steps_out the step count; recs NULL or
+ * recs_cap records, 4 per step in step order.  Errors: PHX_EINVAL "integrate:
+ * h must be positive" / "step count out of range" / "t_end is not a multiple
+ * of h"; PHX_ENUMERIC "integrate: state left the finite range at t = ...". */
+phx_status phx_integrate(phx_op op, double gamma, const double* u0, double h, double t_end,
+                         double tol, const phx_scaling_shift* params, double* u_out,
+                         double* t_out, int64_t* n_steps_out, phx_run_record* recs,
+                         int64_t recs_cap);
+
+/* ---------------------------------------------------------------------------
  * Introspection.
  * ------------------------------------------------------------------------- */
 const char* phx_last_error(void);

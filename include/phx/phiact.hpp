@@ -244,4 +244,134 @@ inline PhiResult phimv(const LinearOperator& op, const PhiRequest& req) {
   return out;
 }
 
+// ---------------------------------------------------------------------------
+// The evaluator's consumer (integrator.hpp, problems.hpp:46-70)
+struct ExpRK4s6Coefficients {  // integrator.hpp:13-19
+  static constexpr double c2 = 0.5;
+  static constexpr double c3 = 0.5;
+  static constexpr double c4 = 1.0 / 3.0;
+  static constexpr double c5 = 5.0 / 6.0;
+  static constexpr double c6 = 1.0 / 3.0;
+};
+
+// ADRProblem (problems.hpp:46-66) with the operator stored as CSR.
+struct ADRProblem {
+  int nx = 0;
+  int ny = 0;
+  double eps = 1e-3;
+  double alpha_adv = -0.5;
+  double gamma = 1000.0;
+  LinearOperator op;
+  Vector u0;
+  double t_end = 0.5;
+  // gamma u (u - 1/2)(1 - u) (problems.cpp:180-182)
+  Vector reaction(const Vector& u) const {
+    Vector g(u.size());
+    for (Index i = 0; i < u.size(); ++i) g(i) = gamma * u(i) * (u(i) - 0.5) * (1.0 - u(i));
+    return g;
+  }
+};
+
+inline ADRProblem adr_build(int nx, int ny, double eps = 1e-3, double alpha_adv = -0.5,
+                            double gamma = 1000.0, int device = -1) {
+  if (nx < 8 || ny < 8) throw std::invalid_argument("adr_build: grid must be at least 8x8");
+  const Index n = Index(nx) * Index(ny);
+  std::vector<std::int64_t> rp(size_t(n + 1));
+  std::vector<std::int32_t> ci(size_t(5 * n));
+  std::vector<double> av(size_t(5 * n));
+  ADRProblem prob;
+  prob.u0 = Vector(n);
+  detail::check(phx_adr_csr(nx, ny, eps, alpha_adv, rp.data(), ci.data(), av.data(),
+                            prob.u0.data()));
+  ci.resize(size_t(rp[size_t(n)]));
+  av.resize(size_t(rp[size_t(n)]));
+  prob.nx = nx;
+  prob.ny = ny;
+  prob.eps = eps;
+  prob.alpha_adv = alpha_adv;
+  prob.gamma = gamma;
+  prob.op = csr_operator(n, rp, ci, av, "adr", device);
+  return prob;
+}
+
+struct StepState {  // integrator.hpp:21-25
+  double t = 0.0;
+  Vector u;
+  double h = 0.0;
+};
+
+struct StepRecord {  // integrator.hpp:27-30
+  double t = 0.0;
+  RunRecord calls[4];
+};
+
+namespace detail {
+inline RunRecord from_rec(const phx_run_record& r, const std::vector<int32_t>& lens) {
+  RunRecord o;
+  o.s_effective = r.s_effective;
+  o.series_len_S = r.series_len_S;
+  o.series_lens_F.assign(lens.begin(),
+                         lens.begin() + std::min<int64_t>(r.n_sweeps, int64_t(lens.size())));
+  o.matvecs = r.matvecs;
+  return o;
+}
+}  // namespace detail
+
+// exprk4s6_step (integrator.hpp:36-38)
+inline Vector exprk4s6_step(const ADRProblem& problem, const StepState& state, double tol,
+                            const ScalingShift& params, StepRecord* record = nullptr) {
+  Vector out(state.u.size());
+  const phx_scaling_shift ss = detail::to_c(params);
+  std::vector<std::vector<int32_t>> lens(4, std::vector<int32_t>(1 << 16));
+  phx_run_record recs[4];
+  for (int k = 0; k < 4; ++k)
+    recs[k] = phx_run_record{0, 0, 0, lens[size_t(k)].data(), int64_t(1 << 16), 0};
+  detail::check(phx_exprk4s6_step(problem.op.handle(), problem.gamma, state.u.data(), state.h,
+                                  tol, &ss, out.data(), record ? recs : nullptr));
+  if (record) {
+    record->t = state.t;
+    for (int k = 0; k < 4; ++k) record->calls[k] = detail::from_rec(recs[k], lens[size_t(k)]);
+  }
+  return out;
+}
+
+struct IntegrateResult {  // integrator.hpp:40-44
+  Vector u;
+  double t = 0.0;
+  std::vector<StepRecord> steps;
+};
+
+// integrate (integrator.hpp:47-49)
+inline IntegrateResult integrate(const ADRProblem& problem, double h, double t_end, double tol,
+                                 const ScalingShift& params, bool keep_records = true) {
+  IntegrateResult out;
+  out.u = Vector(problem.u0.size());
+  const phx_scaling_shift ss = detail::to_c(params);
+  int64_t nrec = 0;
+  if (keep_records && h > 0.0) {
+    const double q = t_end / h;
+    if (q >= 0.5 && q < 1.0e6 + 0.5) nrec = 4 * int64_t(std::llround(q));
+  }
+  constexpr int64_t kLens = 1 << 10;
+  std::vector<int32_t> lens(size_t(std::max<int64_t>(1, nrec) * kLens));
+  std::vector<phx_run_record> recs(size_t(std::max<int64_t>(1, nrec)));
+  for (int64_t k = 0; k < nrec; ++k)
+    recs[size_t(k)] = phx_run_record{0, 0, 0, lens.data() + k * kLens, kLens, 0};
+  int64_t nsteps = 0;
+  detail::check(phx_integrate(problem.op.handle(), problem.gamma, problem.u0.data(), h, t_end,
+                              tol, &ss, out.u.data(), &out.t, &nsteps,
+                              nrec ? recs.data() : nullptr, nrec));
+  for (int64_t s = 0; s < nsteps && 4 * s + 3 < nrec; ++s) {
+    StepRecord st;
+    st.t = double(s) * h;
+    for (int k = 0; k < 4; ++k) {
+      const phx_run_record& r = recs[size_t(4 * s + k)];
+      const std::vector<int32_t> l(r.series_lens_F, r.series_lens_F + kLens);
+      st.calls[k] = detail::from_rec(r, l);
+    }
+    out.steps.push_back(std::move(st));
+  }
+  return out;
+}
+
 }  // namespace phiact

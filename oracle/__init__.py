@@ -87,6 +87,14 @@ def lib():
         L.orc_reference_w.argtypes = [C.c_int64, dp, C.c_int32, dp, C.c_double, C.c_double, dp]
         L.orc_dense_phi.argtypes = [C.c_int64, dp, C.c_double, C.c_int32, dp]
         L.orc_jexp_chain.argtypes = [C.c_double, C.c_double, C.c_int32, dp]
+        L.orc_adr_apply_stencil.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_double, dp, dp]
+        L.orc_adr_apply_stencil.restype = None
+        L.orc_adr_u0.argtypes = [C.c_int32, C.c_int32, dp]
+        L.orc_adr_u0.restype = None
+        L.orc_exprk4s6_step.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, dp, C.c_double,
+                                        C.c_double, C.c_void_p, dp, i64p]
+        L.orc_integrate.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, dp, C.c_double,
+                                    C.c_double, C.c_double, C.c_void_p, dp, dp, i64p, C.c_int64]
         _LIB = L
     return _LIB
 
@@ -368,3 +376,51 @@ def jexp_chain(alpha, s, p):
     out = np.empty(p + 1)
     lib().orc_jexp_chain(alpha, s, p, _d(out))
     return out
+
+
+# ---------------------------------------------------------------------------
+# the evaluator's consumer: integrator.cpp restated
+def adr_apply_stencil(nx, ny, eps, alpha_adv, u):
+    """adr_build's matrix-free apply (problems.cpp:206-231), restated."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    y = np.empty_like(u)
+    lib().orc_adr_apply_stencil(nx, ny, eps, alpha_adv, _d(u), _d(y))
+    return y
+
+
+def adr_u0(nx, ny):
+    """adr_build's initial condition (problems.cpp:239-246)."""
+    out = np.empty(nx * ny)
+    lib().orc_adr_u0(nx, ny, _d(out))
+    return out
+
+
+def _recs(rec4):
+    return [RunRecord(int(r[0]), int(r[1]), [], int(r[3])) for r in rec4.reshape(-1, 4)]
+
+
+def exprk4s6_step(op: Csr, gamma, u, h, tol, params: ScalingShift):
+    """exprk4s6_step (integrator.cpp:29-105) -> (u_next, 4 RunRecords)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty_like(u)
+    rec4 = np.zeros(16, dtype=np.int64)
+    pc = params.c()
+    _check(lib().orc_exprk4s6_step(*op.args(), float(gamma), _d(u), float(h), float(tol),
+                                   C.byref(pc), _d(out), rec4.ctypes.data_as(i64p)))
+    return out, _recs(rec4)
+
+
+def integrate(op: Csr, gamma, u0, h, t_end, tol, params: ScalingShift, keep_records=True):
+    """integrate (integrator.cpp:107-134) -> (u, t, RunRecords, 4 per step)."""
+    u0 = np.ascontiguousarray(u0, dtype=np.float64)
+    out = np.empty_like(u0)
+    t = C.c_double()
+    steps = max(1, int(round(t_end / h))) if h > 0 else 1
+    cap = 4 * steps if keep_records else 0
+    rec4 = np.zeros(4 * max(cap, 1), dtype=np.int64)
+    pc = params.c()
+    _check(lib().orc_integrate(*op.args(), float(gamma), _d(u0), float(h), float(t_end),
+                               float(tol), C.byref(pc), _d(out), C.byref(t),
+                               rec4.ctypes.data_as(i64p) if keep_records else None, cap))
+    return out, t.value, (_recs(rec4[: 4 * cap]) if keep_records else [])
+

@@ -1024,6 +1024,158 @@ static std::vector<Mat> dense_phi(const Mat& M, double t, int jmax) {
 // 1 = std::invalid_argument, 2 = std::runtime_error, 3 = std::logic_error,
 // 9 = other; message via orc_last_error().
 // ============================================================================
+namespace orc {
+
+// ---------------------------------------------------------------------------
+// The evaluator's consumer
+// ---------------------------------------------------------------------------
+
+// ADRProblem::reaction (problems.cpp:180-182): gamma * u * (u - 1/2) * (1 - u),
+// left-associative like the Eigen array expression.
+static double adr_reaction(double gamma, double u) { return gamma * u * (u - 0.5) * (1.0 - u); }
+
+// adr_build's matrix-free apply (problems.cpp:184-231), restated verbatim:
+// mirror ghosts at x = 0 / y = 0, eliminated Dirichlet edges at x = 1 / y = 1.
+static void adr_apply_stencil(int nx, int ny, double eps, double alpha_adv, const double* u,
+                              double* y) {
+  const double hx = 1.0 / nx, hy = 1.0 / ny;
+  const double dxx = eps / (hx * hx), dyy = eps / (hy * hy);
+  const double ax = alpha_adv / (2.0 * hx), ay = alpha_adv / (2.0 * hy);
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) {
+      const long idx = long(j) * nx + i;
+      const double uc = u[idx];
+      const double uw = i > 0 ? u[idx - 1] : u[idx + 1];
+      const double ue = i < nx - 1 ? u[idx + 1] : 0.0;
+      const double us = j > 0 ? u[idx - nx] : u[idx + nx];
+      const double un = j < ny - 1 ? u[idx + nx] : 0.0;
+      const double lap = dxx * (uw - 2.0 * uc + ue) + dyy * (us - 2.0 * uc + un);
+      const double adv = ax * (ue - uw) + ay * (un - us);
+      y[idx] = lap - adv;
+    }
+}
+
+// adr_build's initial condition (problems.cpp:239-246)
+static void adr_u0(int nx, int ny, double* u0) {
+  const double hx = 1.0 / nx, hy = 1.0 / ny;
+  for (int j = 0; j < ny; ++j) {
+    const double y = j * hy;
+    for (int i = 0; i < nx; ++i) {
+      const double x = i * hx;
+      u0[long(j) * nx + i] = 256.0 * x * x * y * y * (1.0 - x) * (1.0 - x) * (1.0 - y) * (1.0 - y);
+    }
+  }
+}
+
+// ExpRK4s6Coefficients (integrator.hpp:13-19)
+constexpr double kC2 = 0.5, kC3 = 0.5, kC4 = 1.0 / 3.0, kC5 = 5.0 / 6.0, kC6 = 1.0 / 3.0;
+
+// exprk4s6_step (integrator.cpp:29-105) on a CSR operator with reaction gamma
+static Vec exprk4s6_step(const Op& op, double gamma, const Vec& u, double h, double tol,
+                         const ScalingShift& params, RunRecord* recs) {
+  const long n = long(u.size());
+  Vec g_n(static_cast<size_t>(n)), hf(static_cast<size_t>(n));
+  {
+    Mat U(n, 1);
+    std::copy(u.begin(), u.end(), U.col(0));
+    const Mat AU = apply(op, U);
+    for (long i = 0; i < n; ++i) {
+      g_n[size_t(i)] = adr_reaction(gamma, u[size_t(i)]);
+      const double f = AU(i, 0) + g_n[size_t(i)];  // op.apply(u) + g_n
+      hf[size_t(i)] = h * f;
+    }
+  }
+  auto stage_call = [&](const Vec& t, const Vec& alpha, const Mat& V, RunRecord* rec) {
+    Trace trc;
+    BlockResult res = phimv_block(op, t, alpha, V, tol, params, trc);
+    if (rec) *rec = res.rec;
+    return res.W;
+  };
+  auto react_diff = [&](const double* W) {
+    Vec d(static_cast<size_t>(n));
+    for (long i = 0; i < n; ++i)
+      d[size_t(i)] = adr_reaction(gamma, u[size_t(i)] + W[i]) - g_n[size_t(i)];
+    return d;
+  };
+  // stage 2 alone
+  Mat V2(n, 2);
+  for (long i = 0; i < n; ++i) V2(i, 1) = kC2 * hf[size_t(i)];
+  const Mat U2 = stage_call({kC2 * h}, {1.0}, V2, recs ? recs + 0 : nullptr);
+  const Vec d2 = react_diff(U2.col(0));
+  // stages 3 and 4, alpha_i = c_i
+  Mat V34(n, 3);
+  const double s34 = h / kC2;
+  for (long i = 0; i < n; ++i) {
+    V34(i, 1) = hf[size_t(i)];
+    V34(i, 2) = s34 * d2[size_t(i)];
+  }
+  const Mat U34 = stage_call({kC3 * h, kC4 * h}, {kC3, kC4}, V34, recs ? recs + 1 : nullptr);
+  const Vec d3 = react_diff(U34.col(0)), d4 = react_diff(U34.col(1));
+  // stages 5 and 6
+  const double c34 = kC3 - kC4;
+  Mat V56(n, 4);
+  {
+    const double A = h / c34, B = -(kC4 / kC3), C = kC3 / kC4, D = 2.0 * h / c34;
+    for (long i = 0; i < n; ++i) {
+      V56(i, 1) = hf[size_t(i)];
+      V56(i, 2) = A * (B * d3[size_t(i)] + C * d4[size_t(i)]);
+      V56(i, 3) = D * (d3[size_t(i)] / kC3 - d4[size_t(i)] / kC4);
+    }
+  }
+  const Mat U56 = stage_call({kC5 * h, kC6 * h}, {kC5, kC6}, V56, recs ? recs + 2 : nullptr);
+  const Vec d5 = react_diff(U56.col(0)), d6 = react_diff(U56.col(1));
+  // the update, alpha = 1
+  const double c56 = kC5 - kC6;
+  Mat Vn(n, 4);
+  {
+    const double A = h / c56, B = -(kC6 / kC5), C = kC5 / kC6, D = 2.0 * h / c56;
+    for (long i = 0; i < n; ++i) {
+      Vn(i, 1) = hf[size_t(i)];
+      Vn(i, 2) = A * (B * d5[size_t(i)] + C * d6[size_t(i)]);
+      Vn(i, 3) = D * (d5[size_t(i)] / kC5 - d6[size_t(i)] / kC6);
+    }
+  }
+  const Mat Un = stage_call({h}, {1.0}, Vn, recs ? recs + 3 : nullptr);
+  Vec out(static_cast<size_t>(n));
+  for (long i = 0; i < n; ++i) out[size_t(i)] = u[size_t(i)] + Un(i, 0);
+  return out;
+}
+
+struct IntegrateResult {
+  Vec u;
+  double t = 0.0;
+  std::vector<RunRecord> recs;  // 4 per step
+};
+
+// integrate (integrator.cpp:107-134)
+static IntegrateResult integrate(const Op& op, double gamma, const Vec& u0, double h, double t_end,
+                                 double tol, const ScalingShift& params, bool keep_records) {
+  if (!(h > 0.0)) throw std::invalid_argument("integrate: h must be positive");
+  const double span = t_end;
+  const long n_steps = std::lround(span / h);
+  if (n_steps < 1 || n_steps > 1000000)
+    throw std::invalid_argument("integrate: step count out of range");
+  if (std::abs(n_steps * h - span) > 1e-9 * std::max(1.0, span))
+    throw std::invalid_argument("integrate: t_end is not a multiple of h");
+  IntegrateResult out;
+  out.u = u0;
+  out.t = 0.0;
+  for (long step = 0; step < n_steps; ++step) {
+    RunRecord rec[4];
+    Vec next = exprk4s6_step(op, gamma, out.u, h, tol, params, keep_records ? rec : nullptr);
+    if (!all_finite(next.data(), next.size()))
+      throw std::runtime_error("integrate: state left the finite range at t = " +
+                               std::to_string(out.t));
+    out.u = std::move(next);
+    out.t = (step + 1) * h;
+    if (keep_records)
+      for (auto& r : rec) out.recs.push_back(r);
+  }
+  return out;
+}
+
+}  // namespace orc
+
 namespace {
 thread_local std::string g_err;
 template <class F>
@@ -1246,6 +1398,43 @@ int orc_dense_phi(int64_t d, const double* M, double t, int32_t jmax, double* ou
     auto phis = orc::dense_phi(Mm, t, jmax);
     for (int k = 0; k <= jmax; ++k)
       std::copy(phis[size_t(k)].a.begin(), phis[size_t(k)].a.end(), out + size_t(k) * size_t(d * d));
+  });
+}
+
+// --- the integrator ---
+void orc_adr_apply_stencil(int32_t nx, int32_t ny, double eps, double alpha_adv, const double* u,
+                           double* y) {
+  orc::adr_apply_stencil(nx, ny, eps, alpha_adv, u, y);
+}
+void orc_adr_u0(int32_t nx, int32_t ny, double* u0) { orc::adr_u0(nx, ny, u0); }
+
+// rec4: 4 int64 per evaluator call (s_eff, L_S, sweeps, matvecs)
+int orc_exprk4s6_step(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, double gamma,
+                      const double* u, double h, double tol, const orc_scaling_shift* params,
+                      double* u_next, int64_t* rec4) {
+  return guarded([&] {
+    orc::Vec uu(u, u + n);
+    orc::RunRecord recs[4];
+    orc::Vec out = orc::exprk4s6_step(make_op(n, rp, ci, v), gamma, uu, h, tol, *params, recs);
+    std::copy(out.begin(), out.end(), u_next);
+    if (rec4)
+      for (int k = 0; k < 4; ++k) fill_rec(recs[k], rec4 + 4 * k, nullptr, 0);
+  });
+}
+
+int orc_integrate(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, double gamma,
+                  const double* u0, double h, double t_end, double tol,
+                  const orc_scaling_shift* params, double* u_out, double* t_out, int64_t* rec4,
+                  int64_t rec_cap) {
+  return guarded([&] {
+    orc::Vec uu(u0, u0 + n);
+    orc::IntegrateResult res = orc::integrate(make_op(n, rp, ci, v), gamma, uu, h, t_end, tol,
+                                              *params, rec4 != nullptr);
+    std::copy(res.u.begin(), res.u.end(), u_out);
+    if (t_out) *t_out = res.t;
+    if (rec4)
+      for (size_t k = 0; k < res.recs.size() && int64_t(k) < rec_cap; ++k)
+        fill_rec(res.recs[k], rec4 + 4 * k, nullptr, 0);
   });
 }
 

@@ -75,6 +75,7 @@ ABI_SYMBOLS = (
     "phx_basis_info", "phx_objective", "phx_minimize_shift", "phx_parameters_for_shift",
     "phx_phimv_block", "phx_phimv_block_device", "phx_phimv", "phx_last_error",
     "phx_kernel_launches", "phx_last_eval_stats", "phx_set_trace", "phx_get_trace",
+    "phx_adr_csr", "phx_exprk4s6_step", "phx_integrate",
 )
 
 
@@ -124,6 +125,11 @@ def lib():
                                          C.c_double, C.POINTER(_SS), C.c_void_p, C.POINTER(_Rec)]
     L.phx_phimv.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int32, dp, C.c_int64,
                             C.c_double, C.POINTER(_SS), dp, dp, dp, C.POINTER(_Rec)]
+    L.phx_adr_csr.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_double, i64p, i32p, dp, dp]
+    L.phx_exprk4s6_step.argtypes = [C.c_void_p, C.c_double, dp, C.c_double, C.c_double,
+                                    C.POINTER(_SS), dp, C.POINTER(_Rec)]
+    L.phx_integrate.argtypes = [C.c_void_p, C.c_double, dp, C.c_double, C.c_double, C.c_double,
+                                C.POINTER(_SS), dp, dp, i64p, C.POINTER(_Rec), C.c_int64]
     L.phx_last_eval_stats.argtypes = [dp, i64p]
     L.phx_set_trace.argtypes = [C.c_int64]
     L.phx_get_trace.argtypes = [dp, C.c_int64, i64p]
@@ -501,3 +507,126 @@ def workload(cfg: int, size: int = 0, with_V: bool = True) -> Workload:
     if code != 0:
         raise RuntimeError(f"workload generator failed ({code})")
     return Workload(cfg, int(info.size), n, nnz, p, r, info.tol, rp, ci, av, V, t, alpha)
+
+
+# ---------------------------------------------------------------------------
+# The evaluator's consumer: the expRK4s6 integrator
+# (include/phiact/integrator.hpp) on the ADR problem (problems.hpp:46-70),
+# device-resident through phx_exprk4s6_step / phx_integrate.
+class ExpRK4s6Coefficients:
+    """Stage abscissae (integrator.hpp:13-19)."""
+    c2 = 0.5
+    c3 = 0.5
+    c4 = 1.0 / 3.0
+    c5 = 5.0 / 6.0
+    c6 = 1.0 / 3.0
+
+
+@dataclass
+class ADRProblem:
+    """u_t = A u + gamma u (u - 1/2)(1 - u) with A a CsrOperator
+    (problems.hpp:46-66; the operator is stored as CSR, csrc/problems.cpp)."""
+    nx: int
+    ny: int
+    eps: float
+    alpha_adv: float
+    gamma: float
+    op: "CsrOperator"
+    u0: np.ndarray
+    t_end: float = 0.5
+
+    def reaction(self, u):
+        """Pointwise reaction gamma u (u - 1/2)(1 - u) (problems.cpp:180-182)."""
+        u = np.asarray(u, dtype=np.float64)
+        return self.gamma * u * (u - 0.5) * (1.0 - u)
+
+
+def adr_csr(nx: int, ny: int, eps: float = 1e-3, alpha_adv: float = -0.5):
+    """(row_ptr, col_idx, vals, u0) of adr_build's operator (phx_adr_csr)."""
+    n = int(nx) * int(ny)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    ci = np.zeros(max(1, 5 * n), dtype=np.int32)
+    av = np.zeros(max(1, 5 * n), dtype=np.float64)
+    u0 = np.zeros(n, dtype=np.float64)
+    code = lib().phx_adr_csr(int(nx), int(ny), float(eps), float(alpha_adv),
+                             rp.ctypes.data_as(i64p), ci.ctypes.data_as(i32p), _d(av), _d(u0))
+    if code != 0:
+        raise ValueError("adr_build: grid must be at least 8x8")
+    nnz = int(rp[n])
+    return rp, ci[:nnz].copy(), av[:nnz].copy(), u0
+
+
+def adr_build(nx: int, ny: int, eps: float = 1e-3, alpha_adv: float = -0.5,
+              gamma: float = 1000.0, device: int = -1) -> ADRProblem:
+    """adr_build (problems.cpp:184-250) with a device-resident CSR operator."""
+    rp, ci, av, u0 = adr_csr(nx, ny, eps, alpha_adv)
+    op = CsrOperator(int(nx) * int(ny), rp, ci, av, device=device)
+    return ADRProblem(int(nx), int(ny), float(eps), float(alpha_adv), float(gamma), op, u0, 0.5)
+
+
+@dataclass
+class StepState:
+    t: float = 0.0
+    u: np.ndarray = None
+    h: float = 0.0
+
+
+@dataclass
+class StepRecord:
+    t: float
+    calls: list  # 4 RunRecord, one per block-evaluator call
+
+
+@dataclass
+class IntegrateResult:
+    u: np.ndarray
+    t: float
+    steps: list  # StepRecord per step (empty without records)
+
+
+def _rk_recs(count, params: ScalingShift, h):
+    cap = _lens_cap(params, [h])
+    recs = (_Rec * max(1, count))()
+    lens = []
+    for k in range(count):
+        r, l = _mkrec(cap)
+        recs[k] = r
+        lens.append(l)
+    return recs, lens
+
+
+def exprk4s6_step(problem: ADRProblem, state: StepState, tol, params: ScalingShift):
+    """One expRK4s6 step (integrator.cpp:29-105) -> (u_next, StepRecord)."""
+    u = np.ascontiguousarray(state.u, dtype=np.float64)
+    if u.shape != (problem.op.n,):
+        raise ValueError("exprk4s6_step: state size does not match the operator")
+    out = np.empty_like(u)
+    recs, lens = _rk_recs(4, params, state.h)
+    ss = params._c()
+    _check(lib().phx_exprk4s6_step(problem.op._h, float(problem.gamma), _d(u), float(state.h),
+                                   float(tol), C.byref(ss), _d(out), recs))
+    return out, StepRecord(float(state.t), [_torec(recs[k], lens[k]) for k in range(4)])
+
+
+def integrate(problem: ADRProblem, h, t_end, tol, params: ScalingShift,
+              keep_records: bool = True) -> IntegrateResult:
+    """Fixed-step integration from t = 0 to t_end (integrator.cpp:107-134)."""
+    u0 = np.ascontiguousarray(problem.u0, dtype=np.float64)
+    out = np.empty_like(u0)
+    t = C.c_double()
+    nsteps = C.c_int64()
+    ss = params._c()
+    count = 0
+    if keep_records and h > 0 and np.isfinite(t_end / h):
+        count = 4 * int(max(1, min(1000000, round(t_end / h))))
+    recs, lens = _rk_recs(count, params, h)
+    _check(lib().phx_integrate(problem.op._h, float(problem.gamma), _d(u0), float(h),
+                               float(t_end), float(tol), C.byref(ss), _d(out), C.byref(t),
+                               C.byref(nsteps), recs if count else None, count))
+    steps = []
+    if count:
+        for k in range(int(nsteps.value)):
+            steps.append(StepRecord(k * float(h),
+                                    [_torec(recs[4 * k + q], lens[4 * k + q]) for q in range(4)]))
+    return IntegrateResult(out, float(t.value), steps)
+

@@ -1455,6 +1455,187 @@ phx_status phx_phimv(phx_op op, double t, double alpha, int32_t p, const double*
   });
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// expRK4s6 integrator (integrator.cpp:13-134) on a CSR
+// operator.  The state stays on the device: a step is four evaluator
+// launches (stage_call, :13-25) and four elementwise stage kernels on the
+// operator's stream, with the reference's expression order.
+namespace {
+
+struct RkCoef {  // ExpRK4s6Coefficients (integrator.hpp:13-19)
+  static constexpr double c2 = 0.5;
+  static constexpr double c3 = 0.5;
+  static constexpr double c4 = 1.0 / 3.0;
+  static constexpr double c5 = 5.0 / 6.0;
+  static constexpr double c6 = 1.0 / 3.0;
+};
+
+struct RkWork {
+  DevBuf gn, hf, V, W, u0, u1, flag;
+  ~RkWork() {
+    for (DevBuf* b : {&gn, &hf, &V, &W, &u0, &u1, &flag}) b->release();
+  }
+};
+
+void rk_check_op(phx_op op, const char* who) {
+  if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+  if (op->nparts > 1)
+    throw_phx(PHX_EINVAL, std::string(who) + ": row-partitioned operators are not supported");
+}
+
+// one exprk4s6_step (integrator.cpp:29-105): d_u -> d_next (device, n each);
+// returns true when d_next has a non-finite entry
+bool rk_step_dev(phx_op op, RkWork& w, double gamma, const double* d_u, double h, double tol,
+                 const phx_scaling_shift& ss, double* d_next, phx_run_record* recs) {
+  using C = RkCoef;
+  const int64_t n = op->n;
+  cudaStream_t st = op->stream;
+  phx::RkStageArgs a{};
+  a.n = n;
+  a.rp = op->d_rp;
+  a.ci = op->d_ci;
+  a.av = op->d_av;
+  a.u = d_u;
+  a.gn = w.gn.as<double>(size_t(n));
+  a.hf = w.hf.as<double>(size_t(n));
+  a.V = w.V.as<double>(size_t(4 * n));
+  a.W = w.W.as<double>(size_t(2 * n));
+  a.gamma = gamma;
+  a.h = h;
+  double* dW = w.W.as<double>(size_t(2 * n));
+  auto call = [&](int32_t r, const double* t, const double* al, int32_t p, int k) {
+    EvalIn in{};
+    in.r = r;
+    in.p = p;
+    in.t = t;
+    in.alpha = al;
+    in.dV = a.V;
+    in.tol = tol;
+    in.params = ss;
+    in.dW = dW;
+    evaluate(op, in, recs ? recs + k : nullptr);
+  };
+  // g_n, f_n = A u + g_n, hf = h f_n; stage 2 alone (:38-57)
+  a.mode = 0;
+  a.s0 = C::c2;
+  PHX_CUDA(phx::launch_rk_stage(a, st));
+  {
+    const double t1 = C::c2 * h, a1 = 1.0;
+    call(1, &t1, &a1, 1, 0);
+  }
+  // stages 3 and 4 together, alpha_i = c_i (:59-73)
+  a.mode = 1;
+  a.s0 = h / C::c2;
+  PHX_CUDA(phx::launch_rk_stage(a, st));
+  {
+    const double t34[2] = {C::c3 * h, C::c4 * h}, a34[2] = {C::c3, C::c4};
+    call(2, t34, a34, 2, 1);
+  }
+  // stages 5 and 6 together (:75-89)
+  const double c34 = C::c3 - C::c4;
+  a.mode = 2;
+  a.s0 = h / c34;
+  a.s1 = -(C::c4 / C::c3);
+  a.s2 = C::c3 / C::c4;
+  a.s3 = 2.0 * h / c34;
+  a.ca = C::c3;
+  a.cb = C::c4;
+  PHX_CUDA(phx::launch_rk_stage(a, st));
+  {
+    const double t56[2] = {C::c5 * h, C::c6 * h}, a56[2] = {C::c5, C::c6};
+    call(2, t56, a56, 3, 2);
+  }
+  // the update, alpha = 1 (:91-104)
+  const double c56 = C::c5 - C::c6;
+  a.s0 = h / c56;
+  a.s1 = -(C::c6 / C::c5);
+  a.s2 = C::c5 / C::c6;
+  a.s3 = 2.0 * h / c56;
+  a.ca = C::c5;
+  a.cb = C::c6;
+  PHX_CUDA(phx::launch_rk_stage(a, st));
+  {
+    const double tn = h, an = 1.0;
+    call(1, &tn, &an, 3, 3);
+  }
+  a.mode = 3;
+  a.out = d_next;
+  a.flag = w.flag.as<int>(1);
+  PHX_CUDA(cudaMemsetAsync(a.flag, 0, sizeof(int), st));
+  PHX_CUDA(phx::launch_rk_stage(a, st));
+  int flag = 0;
+  PHX_CUDA(cudaMemcpyAsync(&flag, a.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PHX_CUDA(cudaStreamSynchronize(st));
+  return flag != 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+phx_status phx_exprk4s6_step(phx_op op, double gamma, const double* u, double h, double tol,
+                             const phx_scaling_shift* params, double* u_next,
+                             phx_run_record* recs) {
+  return guarded([&] {
+    rk_check_op(op, "exprk4s6_step");
+    if (!u || !u_next || !params) throw_phx(PHX_EINVAL, "exprk4s6_step: null argument");
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    RkWork w;
+    const size_t n = size_t(op->n);
+    double* du = w.u0.as<double>(n);
+    double* dn = w.u1.as<double>(n);
+    PHX_CUDA(cudaMemcpyAsync(du, u, n * 8, cudaMemcpyHostToDevice, op->stream));
+    rk_step_dev(op, w, gamma, du, h, tol, *params, dn, recs);
+    PHX_CUDA(cudaMemcpyAsync(u_next, dn, n * 8, cudaMemcpyDeviceToHost, op->stream));
+    PHX_CUDA(cudaStreamSynchronize(op->stream));
+  });
+}
+
+phx_status phx_integrate(phx_op op, double gamma, const double* u0, double h, double t_end,
+                         double tol, const phx_scaling_shift* params, double* u_out,
+                         double* t_out, int64_t* n_steps_out, phx_run_record* recs,
+                         int64_t recs_cap) {
+  return guarded([&] {
+    rk_check_op(op, "integrate");
+    if (!u0 || !u_out || !params) throw_phx(PHX_EINVAL, "integrate: null argument");
+    // input validation (integrator.cpp:110-116)
+    if (!(h > 0.0)) throw_phx(PHX_EINVAL, "integrate: h must be positive");
+    const double span = t_end;
+    const long n_steps = std::lround(span / h);
+    if (n_steps < 1 || n_steps > 1000000)
+      throw_phx(PHX_EINVAL, "integrate: step count out of range");
+    if (std::abs(n_steps * h - span) > 1e-9 * std::max(1.0, span))
+      throw_phx(PHX_EINVAL, "integrate: t_end is not a multiple of h");
+    if (n_steps_out) *n_steps_out = n_steps;
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    RkWork w;
+    const size_t n = size_t(op->n);
+    double* cur = w.u0.as<double>(n);
+    double* nxt = w.u1.as<double>(n);
+    PHX_CUDA(cudaMemcpyAsync(cur, u0, n * 8, cudaMemcpyHostToDevice, op->stream));
+    double t = 0.0;
+    if (t_out) *t_out = t;
+    for (long step = 0; step < n_steps; ++step) {
+      phx_run_record* rs = (recs && 4 * int64_t(step) + 3 < recs_cap) ? recs + 4 * step : nullptr;
+      if (rk_step_dev(op, w, gamma, cur, h, tol, *params, nxt, rs)) {
+        PHX_CUDA(cudaMemcpyAsync(u_out, cur, n * 8, cudaMemcpyDeviceToHost, op->stream));
+        PHX_CUDA(cudaStreamSynchronize(op->stream));
+        throw_phx(PHX_ENUMERIC,
+                  "integrate: state left the finite range at t = " + std::to_string(t));
+      }
+      std::swap(cur, nxt);
+      t = (step + 1) * h;
+      if (t_out) *t_out = t;
+    }
+    PHX_CUDA(cudaMemcpyAsync(u_out, cur, n * 8, cudaMemcpyDeviceToHost, op->stream));
+    PHX_CUDA(cudaStreamSynchronize(op->stream));
+  });
+}
+
 phx_status phx_last_eval_stats(double* kernel_ms, int64_t* steps) {
   std::lock_guard<std::mutex> lk(g_trace_mu);
   if (kernel_ms) *kernel_ms = g_last_ms;

@@ -187,6 +187,71 @@ cudaError_t launch_spmv(int32_t n, const int32_t* rp, const int32_t* ci, const d
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// expRK4s6 stage kernels (integrator.cpp:29-105): elementwise, one thread per
+// row, the reference's Eigen expression order (left-associative, no FMA).
+// V blocks are column-major n x (p+1) with leading dimension n; column 0 is
+// zero in every call (the scheme has no phi_0 term).
+__device__ __forceinline__ double rk_reaction(double gamma, double u) {
+  return gamma * u * (u - 0.5) * (1.0 - u);  // problems.cpp ADRProblem::reaction
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_rk_stage(RkStageArgs a) {
+  const int64_t n = a.n;
+  for (int64_t i = int64_t(blockIdx.x) * kBlock + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * kBlock) {
+    const double ui = a.u[i];
+    double* V = a.V;
+    switch (a.mode) {
+      case 0: {  // g_n = r(u); f_n = A u + g_n; hf = h f_n; V2 = [0, c2 hf]
+        double acc = 0.0;
+        for (int e = __ldg(a.rp + i), e1 = __ldg(a.rp + i + 1); e < e1; ++e)
+          acc = acc + __ldg(a.av + e) * a.u[__ldg(a.ci + e)];
+        const double g = rk_reaction(a.gamma, ui);
+        const double hf = a.h * (acc + g);
+        a.gn[i] = g;
+        a.hf[i] = hf;
+        V[i] = 0.0;
+        V[n + i] = a.s0 * hf;
+        break;
+      }
+      case 1: {  // u2 = u + U; d2 = r(u2) - g_n; V34 = [0, hf, (h/c2) d2]
+        const double u2 = ui + a.W[i];
+        const double d2 = rk_reaction(a.gamma, u2) - a.gn[i];
+        V[i] = 0.0;
+        V[n + i] = a.hf[i];
+        V[2 * n + i] = a.s0 * d2;
+        break;
+      }
+      case 2: {  // two stages (ca, cb): V = [0, hf, A(B da + C db), D(da/ca - db/cb)]
+        const double ua = ui + a.W[i], ub = ui + a.W[n + i];
+        const double da = rk_reaction(a.gamma, ua) - a.gn[i];
+        const double db = rk_reaction(a.gamma, ub) - a.gn[i];
+        V[i] = 0.0;
+        V[n + i] = a.hf[i];
+        V[2 * n + i] = a.s0 * (a.s1 * da + a.s2 * db);
+        V[3 * n + i] = a.s3 * (da / a.ca - db / a.cb);
+        break;
+      }
+      default: {  // u_next = u + U; flag a non-finite entry
+        const double un = ui + a.W[i];
+        a.out[i] = un;
+        if (!isfinite(un)) atomicOr(a.flag, 1);
+        break;
+      }
+    }
+  }
+}
+
+cudaError_t launch_rk_stage(const RkStageArgs& a, cudaStream_t st) {
+  ++g_launches;
+  const int64_t blocks = (a.n + kBlock - 1) / kBlock;
+  const int grid = int(std::min<int64_t>(blocks, 148 * 16));
+  k_rk_stage<<<grid, kBlock, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gemv(int32_t n, int32_t ncol, const double* B, const double* c, double* y,
                         unsigned long long* chunkmax, cudaStream_t st) {
   if (ncol > 128) return cudaErrorInvalidValue;

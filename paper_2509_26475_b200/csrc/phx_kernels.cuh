@@ -155,6 +155,28 @@ cudaError_t launch_spmm_cols(int32_t n, int32_t k, const int32_t* rp, const int3
                              const double* av, const double* X, double* Y, int mode, double xi,
                              cudaStream_t st);
 
+// expRK4s6 stage kernel arguments (phx_kernels.cu k_rk_stage).  mode 0: f_n
+// (CSR A u + reaction) -> g_n, hf, V2; 1: stage 2 -> V34; 2: stage pair
+// (ca, cb) -> next V; 3: u_next = u + W with a non-finite flag.
+struct RkStageArgs {
+  int mode;
+  int64_t n;
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* av;
+  const double* u;
+  const double* W;  // n x (1 or 2), ld n
+  double* gn;
+  double* hf;
+  double* V;  // n x (p+1), ld n
+  double* out;
+  int* flag;
+  double gamma, h;
+  double s0, s1, s2, s3;  // per-mode stage scalars (computed on the host)
+  double ca, cb;
+};
+cudaError_t launch_rk_stage(const RkStageArgs& a, cudaStream_t st);
+
 int64_t kernel_launch_count();
 void count_launch();
 

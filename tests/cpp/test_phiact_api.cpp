@@ -86,6 +86,28 @@ int main() {
   } catch (const std::runtime_error& e) {
     std::printf("runtime_error: %s\n", e.what());
   }
+  // the integrator (integrator.hpp): four block calls per step, state on the device
+  {
+    const ADRProblem prob = adr_build(16, 16);
+    const ScalingShift isel = select_parameters(prob.op, kDefaultDegree, 1e-10);
+    StepState st;
+    st.u = prob.u0;
+    st.h = 0.125 / 16.0;
+    StepRecord rec;
+    const Vector u1 = exprk4s6_step(prob, st, 1e-10, isel, &rec);
+    const IntegrateResult ir = integrate(prob, st.h, 2 * st.h, 1e-10, isel);
+    int ok = ir.steps.size() == 2 && ir.t == 2 * st.h;
+    for (Index i = 0; i < u1.size(); ++i) ok = ok && std::isfinite(u1(i));
+    for (const RunRecord& c : rec.calls) ok = ok && c.matvecs > 0;
+    std::printf("integrator steps %zu t %.6f ok %d\n", ir.steps.size(), ir.t, ok);
+    if (!ok) ++fails;
+    try {
+      integrate(prob, 0.3, 1.0, 1e-8, isel);
+      ++fails;
+    } catch (const std::invalid_argument& e) {
+      std::printf("invalid_argument: %s\n", e.what());
+    }
+  }
   std::printf("%d failure(s)\n", fails);
   return fails;
 }

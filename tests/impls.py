@@ -48,6 +48,14 @@ class OracleImpl:
     def phimv(self, op, t, alpha, V, tol, params):
         return O.phimv(op, t, alpha, V, tol, O.ScalingShift(*params.astuple()))
 
+    # integrator.cpp: (u_next, records) / (u, t, records)
+    def rk_step(self, op, gamma, u, h, tol, params):
+        return O.exprk4s6_step(op, gamma, u, h, tol, O.ScalingShift(*params.astuple()))
+
+    def integrate(self, op, gamma, u0, h, t_end, tol, params, keep_records=True):
+        return O.integrate(op, gamma, u0, h, t_end, tol, O.ScalingShift(*params.astuple()),
+                           keep_records)
+
 
 class GpuImpl:
     name = "gpu"
@@ -95,6 +103,21 @@ class GpuImpl:
         P = self.P
         res = P.phimv(op, P.PhiRequest(t, alpha, V, tol, P.ScalingShift(*params.astuple())))
         return res.w, res.exp_v0, res.tail, res.stats
+
+    def _problem(self, op, gamma, u0):
+        return self.P.ADRProblem(0, 0, 0.0, 0.0, float(gamma), op, np.asarray(u0, dtype=float))
+
+    def rk_step(self, op, gamma, u, h, tol, params):
+        P = self.P
+        un, rec = P.exprk4s6_step(self._problem(op, gamma, u), P.StepState(0.0, u, h), tol,
+                                  P.ScalingShift(*params.astuple()))
+        return un, rec.calls
+
+    def integrate(self, op, gamma, u0, h, t_end, tol, params, keep_records=True):
+        P = self.P
+        res = P.integrate(self._problem(op, gamma, u0), h, t_end, tol,
+                          P.ScalingShift(*params.astuple()), keep_records)
+        return res.u, res.t, [c for st in res.steps for c in st.calls]
 
 
 def basis_columns(impl, b):

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_symbols():
     with open(os.path.join(ROOT, "include", "phx.h")) as f:
         txt = f.read()
-    return sorted(set(re.findall(r"\b(phx_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(phx_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_header_symbols_exported():

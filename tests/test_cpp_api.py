@@ -29,3 +29,5 @@ def test_cpp_api_runs(tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     assert "invalid_argument: phimv_block: at least one abscissa required" in out.stdout
     assert "runtime_error: phimv_block: shift undo factor" in out.stdout
+    assert "integrator steps 2" in out.stdout and "ok 1" in out.stdout
+    assert "invalid_argument: integrate: t_end is not a multiple of h" in out.stdout
