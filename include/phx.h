@@ -171,6 +171,28 @@ phx_status phx_phimv(phx_op op, double t, double alpha, int32_t p, const double*
                      double* tail, phx_run_record* rec);
 
 /* ---------------------------------------------------------------------------
+ * Sparse Matrix Market ingestion.  The reference's
+ * read_matrix_market (matrix_market.hpp:10-16, matrix_market.cpp:37-100)
+ * accepts the same files but reads them dense; these read CSR (structural
+ * entries, columns ascending, duplicates summed in file order from +0, so
+ * values equal the reference's dense entries bit for bit).  Failures return
+ * PHX_ENUMERIC (std::runtime_error) with the reference's message text
+ * "matrix market: <path>: <what>".  Host-only.
+ */
+
+/* Reads the file; always sets *n and *nnz.  Copies the CSR (row_ptr n+1,
+ * col_idx / vals nnz) only when all three buffers are given and
+ * cap_nnz >= nnz -- call once with NULL buffers to size them. */
+phx_status phx_mm_read_csr(const char* path, int64_t* n, int64_t* nnz, int64_t* row_ptr,
+                           int32_t* col_idx, double* vals, int64_t cap_nnz);
+/* Writes CSR as `coordinate real general` with 17 significant digits
+ * (round-trips bit for bit, like write_matrix_market's %.17g). */
+phx_status phx_mm_write_csr(const char* path, int64_t n, const int64_t* row_ptr,
+                            const int32_t* col_idx, const double* vals);
+/* phx_op_create_csr from a Matrix Market file in one call. */
+phx_status phx_op_create_mm(const char* path, int32_t device, phx_op* out);
+
+/* ---------------------------------------------------------------------------
  * The evaluator's consumer: the fourth-order six-stage
  * exponential Runge-Kutta integrator on the 2D advection-diffusion-reaction
  * problem.

@@ -91,6 +91,7 @@ def lib():
         L.orc_adr_apply_stencil.restype = None
         L.orc_adr_u0.argtypes = [C.c_int32, C.c_int32, dp]
         L.orc_adr_u0.restype = None
+        L.orc_read_matrix_market.argtypes = [C.c_char_p, i64p, dp, C.c_int64]
         L.orc_exprk4s6_step.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, dp, C.c_double,
                                         C.c_double, C.c_void_p, dp, i64p]
         L.orc_integrate.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, dp, C.c_double,
@@ -423,4 +424,13 @@ def integrate(op: Csr, gamma, u0, h, t_end, tol, params: ScalingShift, keep_reco
                                float(tol), C.byref(pc), _d(out), C.byref(t),
                                rec4.ctypes.data_as(i64p) if keep_records else None, cap))
     return out, t.value, (_recs(rec4[: 4 * cap]) if keep_records else [])
+
+
+def read_matrix_market(path):
+    """read_matrix_market (matrix_market.cpp:37-100), restated: dense n x n."""
+    n = C.c_int64()
+    _check(lib().orc_read_matrix_market(str(path).encode(), C.byref(n), None, 0))
+    A = np.empty((n.value, n.value), order="F")
+    _check(lib().orc_read_matrix_market(str(path).encode(), C.byref(n), _d(A), A.size))
+    return A
 

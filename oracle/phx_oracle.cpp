@@ -38,6 +38,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cerrno>
+#include <cstdio>
 #include <functional>
 #include <limits>
 #include <random>
@@ -1141,6 +1143,156 @@ static Vec exprk4s6_step(const Op& op, double gamma, const Vec& u, double h, dou
   return out;
 }
 
+// read_matrix_market (matrix_market.cpp:37-100), restated: the reference's
+// dense reader, for pinning the product's CSR reader.
+// Lines come from getline(3) instead of std::getline, and `stream >> x` is
+// restated as libstdc++'s classic-locale num_get: collect the decimal
+// grammar ([sign] digits [. digits] [(e|E) [sign] digits] for double,
+// [sign] digits for long), convert with strtod / strtol, fail when the
+// conversion stops early or overflows.  (No iostreams: the oracle is loaded
+// into processes with another libstdc++.)
+static std::string mm_lower(std::string s) {
+  for (char& c : s) c = char(std::tolower(static_cast<unsigned char>(c)));
+  return s;
+}
+[[noreturn]] static void mm_fail(const std::string& path, const std::string& what) {
+  throw std::runtime_error("matrix market: " + path + ": " + what);
+}
+struct MmIn {
+  FILE* f = nullptr;
+  ~MmIn() {
+    if (f) std::fclose(f);
+  }
+  bool getline(std::string& line) {  // std::getline: up to '\n', '\n' dropped
+    line.clear();
+    int c;
+    bool any = false;
+    while ((c = std::fgetc(f)) != EOF) {
+      any = true;
+      if (c == '\n') return true;
+      line.push_back(char(c));
+    }
+    return any;
+  }
+};
+static bool mm_next_data_line(MmIn& in, std::string& line) {
+  while (in.getline(line)) {
+    while (!line.empty() && (line.back() == '\r' || line.back() == '\n')) line.pop_back();
+    if (line.empty() || line[0] == '%') continue;
+    if (line.find_first_not_of(" \t") == std::string::npos) continue;
+    return true;
+  }
+  return false;
+}
+struct MmStream {  // istringstream >> long / double / string, classic locale
+  const std::string& s;
+  size_t i = 0;
+  bool ok = true;
+  explicit MmStream(const std::string& str) : s(str) {}
+  void ws() {
+    while (i < s.size() && std::isspace(static_cast<unsigned char>(s[i]))) ++i;
+  }
+  MmStream& operator>>(std::string& w) {
+    w.clear();
+    if (!ok) return *this;
+    ws();
+    while (i < s.size() && !std::isspace(static_cast<unsigned char>(s[i]))) w.push_back(s[i++]);
+    if (w.empty()) ok = false;
+    return *this;
+  }
+  MmStream& operator>>(long& v) {
+    if (!ok) return *this;
+    ws();
+    const size_t b = i;
+    if (i < s.size() && (s[i] == '+' || s[i] == '-')) ++i;
+    while (i < s.size() && std::isdigit(static_cast<unsigned char>(s[i]))) ++i;
+    const std::string tok = s.substr(b, i - b);
+    char* end = nullptr;
+    errno = 0;
+    v = std::strtol(tok.c_str(), &end, 10);
+    if (tok.empty() || *end != '\0' || errno == ERANGE) ok = false;
+    return *this;
+  }
+  MmStream& operator>>(double& v) {
+    if (!ok) return *this;
+    ws();
+    const size_t b = i;
+    bool mant = false;
+    if (i < s.size() && (s[i] == '+' || s[i] == '-')) ++i;
+    while (i < s.size() && std::isdigit(static_cast<unsigned char>(s[i]))) ++i, mant = true;
+    if (i < s.size() && s[i] == '.') {
+      ++i;
+      while (i < s.size() && std::isdigit(static_cast<unsigned char>(s[i]))) ++i, mant = true;
+    }
+    if (mant && i < s.size() && (s[i] == 'e' || s[i] == 'E')) {
+      ++i;
+      if (i < s.size() && (s[i] == '+' || s[i] == '-')) ++i;
+      while (i < s.size() && std::isdigit(static_cast<unsigned char>(s[i]))) ++i;
+    }
+    const std::string tok = s.substr(b, i - b);
+    char* end = nullptr;
+    v = std::strtod(tok.c_str(), &end);
+    if (tok.empty() || *end != '\0' || std::isinf(v)) ok = false;
+    return *this;
+  }
+  explicit operator bool() const { return ok; }
+};
+static Mat read_matrix_market(const std::string& path) {
+  MmIn in;
+  in.f = std::fopen(path.c_str(), "rb");
+  if (!in.f) mm_fail(path, "cannot open file");
+  std::string header;
+  if (!in.getline(header)) mm_fail(path, "empty file");
+  while (!header.empty() && (header.back() == '\r' || header.back() == '\n')) header.pop_back();
+  MmStream hs(header);
+  std::string banner, object, format, field, symmetry;
+  hs >> banner >> object >> format >> field >> symmetry;
+  if (mm_lower(banner) != "%%matrixmarket" || mm_lower(object) != "matrix")
+    mm_fail(path, "malformed header line");
+  format = mm_lower(format);
+  field = mm_lower(field);
+  symmetry = mm_lower(symmetry);
+  if (format != "array" && format != "coordinate") mm_fail(path, "unsupported format '" + format + "'");
+  if (field != "real" && field != "integer") mm_fail(path, "non-real field '" + field + "'");
+  if (symmetry != "general" && symmetry != "symmetric")
+    mm_fail(path, "unsupported symmetry '" + symmetry + "'");
+  const bool symmetric = symmetry == "symmetric";
+  std::string line;
+  if (!mm_next_data_line(in, line)) mm_fail(path, "missing size line");
+  MmStream ss(line);
+  long rows = 0, cols = 0, nnz = 0;
+  if (!(ss >> rows >> cols)) mm_fail(path, "malformed size line");
+  if (format == "coordinate" && !(ss >> nnz)) mm_fail(path, "missing entry count");
+  if (rows <= 0 || cols <= 0) mm_fail(path, "non-positive dimensions");
+  if (rows != cols)
+    mm_fail(path, "matrix is " + std::to_string(rows) + "x" + std::to_string(cols) + ", expected square");
+  Mat A(rows, cols);
+  if (format == "array") {
+    for (long j = 0; j < cols; ++j)
+      for (long i = symmetric ? j : 0; i < rows; ++i) {
+        if (!mm_next_data_line(in, line)) mm_fail(path, "truncated array data");
+        MmStream es(line);
+        double value = 0.0;
+        if (!(es >> value)) mm_fail(path, "malformed entry");
+        A(i, j) = value;
+        if (symmetric) A(j, i) = value;
+      }
+  } else {
+    for (long k = 0; k < nnz; ++k) {
+      if (!mm_next_data_line(in, line)) mm_fail(path, "truncated coordinate data");
+      MmStream es(line);
+      long i = 0, j = 0;
+      double value = 0.0;
+      if (!(es >> i >> j >> value)) mm_fail(path, "malformed entry");
+      if (i < 1 || i > rows || j < 1 || j > cols) mm_fail(path, "entry index out of range");
+      A(i - 1, j - 1) += value;
+      if (symmetric && i != j) A(j - 1, i - 1) += value;
+    }
+  }
+  if (!all_finite(A.a.data(), A.a.size())) mm_fail(path, "non-finite entries");
+  return A;
+}
+
 struct IntegrateResult {
   Vec u;
   double t = 0.0;
@@ -1398,6 +1550,16 @@ int orc_dense_phi(int64_t d, const double* M, double t, int32_t jmax, double* ou
     auto phis = orc::dense_phi(Mm, t, jmax);
     for (int k = 0; k <= jmax; ++k)
       std::copy(phis[size_t(k)].a.begin(), phis[size_t(k)].a.end(), out + size_t(k) * size_t(d * d));
+  });
+}
+
+// --- Matrix Market: the reference's dense reader ---
+// out: n*n column-major (NULL: only *n is set)
+int orc_read_matrix_market(const char* path, int64_t* n, double* out, int64_t cap) {
+  return guarded([&] {
+    orc::Mat A = orc::read_matrix_market(path);
+    *n = A.rows;
+    if (out && cap >= int64_t(A.a.size())) std::copy(A.a.begin(), A.a.end(), out);
   });
 }
 

@@ -76,6 +76,7 @@ ABI_SYMBOLS = (
     "phx_phimv_block", "phx_phimv_block_device", "phx_phimv", "phx_last_error",
     "phx_kernel_launches", "phx_last_eval_stats", "phx_set_trace", "phx_get_trace",
     "phx_adr_csr", "phx_exprk4s6_step", "phx_integrate",
+    "phx_mm_read_csr", "phx_mm_write_csr", "phx_op_create_mm",
 )
 
 
@@ -130,6 +131,9 @@ def lib():
                                     C.POINTER(_SS), dp, C.POINTER(_Rec)]
     L.phx_integrate.argtypes = [C.c_void_p, C.c_double, dp, C.c_double, C.c_double, C.c_double,
                                 C.POINTER(_SS), dp, dp, i64p, C.POINTER(_Rec), C.c_int64]
+    L.phx_mm_read_csr.argtypes = [C.c_char_p, i64p, i64p, i64p, i32p, dp, C.c_int64]
+    L.phx_mm_write_csr.argtypes = [C.c_char_p, C.c_int64, i64p, i32p, dp]
+    L.phx_op_create_mm.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]
     L.phx_last_eval_stats.argtypes = [dp, i64p]
     L.phx_set_trace.argtypes = [C.c_int64]
     L.phx_get_trace.argtypes = [dp, C.c_int64, i64p]
@@ -259,6 +263,11 @@ class CsrOperator:
         rp = np.arange(0, n * n + 1, n, dtype=np.int64)
         ci = np.tile(np.arange(n, dtype=np.int32), n)
         return CsrOperator(n, rp, ci, A.reshape(-1), device)
+
+    @staticmethod
+    def from_matrix_market(path, device: int = -1):
+        """Operator from a Matrix Market file (phx_mm_read_csr)."""
+        return CsrOperator(*read_matrix_market(path), device=device)
 
     def dim(self):
         return self.n
@@ -629,4 +638,30 @@ def integrate(problem: ADRProblem, h, t_end, tol, params: ScalingShift,
             steps.append(StepRecord(k * float(h),
                                     [_torec(recs[4 * k + q], lens[4 * k + q]) for q in range(4)]))
     return IntegrateResult(out, float(t.value), steps)
+
+
+# ---------------------------------------------------------------------------
+# Sparse Matrix Market ingestion (host-only)
+def read_matrix_market(path):
+    """(n, row_ptr, col_idx, vals) of a Matrix Market file: the files
+    read_matrix_market accepts (matrix_market.hpp:10-16), read as CSR.
+    Raises RuntimeError with the reference's diagnostics."""
+    n, nnz = C.c_int64(), C.c_int64()
+    bpath = os.fsencode(path)
+    _check(lib().phx_mm_read_csr(bpath, C.byref(n), C.byref(nnz), None, None, None, 0))
+    rp = np.empty(n.value + 1, dtype=np.int64)
+    ci = np.empty(max(1, nnz.value), dtype=np.int32)
+    av = np.empty(max(1, nnz.value), dtype=np.float64)
+    _check(lib().phx_mm_read_csr(bpath, C.byref(n), C.byref(nnz), rp.ctypes.data_as(i64p),
+                                 ci.ctypes.data_as(i32p), _d(av), ci.size))
+    return n.value, rp, ci[: nnz.value], av[: nnz.value]
+
+
+def write_matrix_market(path, n, row_ptr, col_idx, vals):
+    """CSR -> `coordinate real general`, 17 significant digits (bit-exact round trip)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    av = np.ascontiguousarray(vals, dtype=np.float64)
+    _check(lib().phx_mm_write_csr(os.fsencode(path), int(n), rp.ctypes.data_as(i64p),
+                                  ci.ctypes.data_as(i32p), _d(av)))
 

@@ -1056,6 +1056,15 @@ void check_block_request(phx_op op, int32_t r, const double* t, const double* al
 // ============================================================================
 extern "C" {
 
+}  // extern "C"
+
+namespace phx {
+// error channel for the host-only translation units (matrix_market.cpp)
+void set_last_error(const char* msg) { g_err = msg; }
+}  // namespace phx
+
+extern "C" {
+
 const char* phx_last_error(void) { return g_err.c_str(); }
 
 int64_t phx_kernel_launches(void) { return phx::kernel_launch_count(); }
