@@ -170,6 +170,18 @@ phx_status phx_phimv(phx_op op, double t, double alpha, int32_t p, const double*
                      double tol, const phx_scaling_shift* params, double* w, double* exp_v0,
                      double* tail, phx_run_record* rec);
 
+/* block_series_direct (phi_block.hpp:33-47, phi_block.cpp:158-212): the
+ * direct power series G = sum_j A^j V D_j Gamma T^j (D_j = diag(a_0j..a_pj),
+ * Gamma = [alpha_k^i]), the reference's cross-check of the scaled evaluator;
+ * converges only while the t_k A are small.  coeffs: NULL for
+ * phi_series_coeffs (a_ij = 1/(i+j)!), else a (p+1) x ncoef column-major
+ * table of a_ij.  G: n x r host output (leading dim ldg).  r <= 64.  Errors
+ * as phimv_block ("direct series did not converge within 500 terms",
+ * "direct series produced a non-finite term at index j"). */
+phx_status phx_block_series_direct(phx_op op, int32_t r, const double* t, const double* alpha,
+                                  int32_t p, const double* V, int64_t ldv, double tol,
+                                  const double* coeffs, int64_t ncoef, double* G, int64_t ldg);
+
 /* ---------------------------------------------------------------------------
  * Sparse Matrix Market ingestion.  The reference's
  * read_matrix_market (matrix_market.hpp:10-16, matrix_market.cpp:37-100)

@@ -92,6 +92,9 @@ def lib():
         L.orc_adr_u0.argtypes = [C.c_int32, C.c_int32, dp]
         L.orc_adr_u0.restype = None
         L.orc_read_matrix_market.argtypes = [C.c_char_p, i64p, dp, C.c_int64]
+        L.orc_block_series_direct.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int64, dp, dp,
+                                              C.c_int32, dp, C.c_int64, C.c_double, dp,
+                                              C.c_int64, dp, C.c_int64]
         L.orc_exprk4s6_step.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, dp, C.c_double,
                                         C.c_double, C.c_void_p, dp, i64p]
         L.orc_integrate.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, dp, C.c_double,
@@ -433,4 +436,18 @@ def read_matrix_market(path):
     A = np.empty((n.value, n.value), order="F")
     _check(lib().orc_read_matrix_market(str(path).encode(), C.byref(n), _d(A), A.size))
     return A
+
+
+def block_series_direct(op: Csr, t, alpha, V, tol, coeffs=None):
+    """block_series_direct (phi_block.cpp:172-212); coeffs None = phi_series_coeffs,
+    else a (p+1) x ncoef array of a_ij."""
+    t = np.ascontiguousarray(np.atleast_1d(t), dtype=np.float64)
+    alpha = np.ascontiguousarray(np.atleast_1d(alpha), dtype=np.float64)
+    V = np.asfortranarray(np.asarray(V, dtype=np.float64).reshape(op.n, -1))
+    G = np.empty((op.n, t.size), order="F")
+    cf = None if coeffs is None else np.asfortranarray(np.asarray(coeffs, dtype=np.float64))
+    _check(lib().orc_block_series_direct(*op.args(), t.size, _d(t), _d(alpha), V.shape[1] - 1,
+                                         _d(V), op.n, float(tol), None if cf is None else _d(cf),
+                                         0 if cf is None else cf.shape[1], _d(G), op.n))
+    return G
 

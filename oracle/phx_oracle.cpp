@@ -1029,6 +1029,84 @@ static std::vector<Mat> dense_phi(const Mat& M, double t, int jmax) {
 namespace orc {
 
 // ---------------------------------------------------------------------------
+// block_series_direct (phi_block.cpp:158-212): the
+// direct power series G = sum_j A^j V D_j Gamma T^j, a cross-check of the
+// scaled evaluator.  Canonical orders (the reference delegates them to
+// Eigen): term(:,k) = sum_{i=0..p} X(:,i) * M(i,k) accumulated from +0 in
+// ascending i (M = diag(d_j) Gamma formed first), then * tpow_k, then
+// G += term; inf-norms as everywhere else.
+// phi_series_coeffs (:158-169): a_ij = 1/(i+j)! on the chain f_k = f_{k-1}/k.
+static std::vector<double> phi_inv_factorials(int upto) {
+  std::vector<double> t{1.0};
+  while (int(t.size()) <= upto) t.push_back(t.back() / double(t.size()));
+  return t;
+}
+
+// coeff(i, j): the series coefficients; nullptr = phi_series_coeffs
+static Mat block_series_direct(const Op& op, const Vec& t, const Vec& alpha, const Mat& V,
+                               double req_tol,
+                               const std::function<double(int, int)>* coeff = nullptr) {
+  // check_request (phi_block.cpp:15-27)
+  if (t.empty()) throw std::invalid_argument("phimv_block: at least one abscissa required");
+  if (alpha.size() != t.size()) throw std::invalid_argument("phimv_block: t and alpha lengths differ");
+  if (V.cols < 1) throw std::invalid_argument("phimv_block: V must have at least one column");
+  if (V.rows != op.n) throw std::invalid_argument("phimv_block: V row count does not match operator");
+  if (!all_finite(t.data(), t.size()) || !all_finite(alpha.data(), alpha.size()) ||
+      !all_finite(V.a.data(), V.a.size()))
+    throw std::invalid_argument("phimv_block: inputs must be finite");
+  const double tol = req_tol > 0.0 ? req_tol : default_tolerance();
+  const long r = long(t.size());
+  const int p = int(V.cols) - 1;
+  const long n = op.n;
+  std::vector<double> inv_fact = phi_inv_factorials(p);
+  auto a = [&](int i, int j) -> double {
+    if (coeff) return (*coeff)(i, j);
+    while (int(inv_fact.size()) <= i + j) inv_fact.push_back(inv_fact.back() / double(inv_fact.size()));
+    return inv_fact[size_t(i + j)];
+  };
+  Mat gamma(p + 1, r);  // Gamma = [alpha_k^i]
+  for (long k = 0; k < r; ++k) {
+    double power = 1.0;
+    for (int i = 0; i <= p; ++i) {
+      gamma(i, k) = power;
+      power *= alpha[size_t(k)];
+    }
+  }
+  Mat X = V;
+  Vec tpow(static_cast<size_t>(r), 1.0);
+  Mat G(n, r);
+  Mat term(n, r);
+  double c1 = std::numeric_limits<double>::infinity(), c2 = 0.0;
+  for (int j = 0;; ++j) {
+    if (j >= kSeriesCap)
+      throw std::runtime_error("phimv_block: direct series did not converge within " +
+                               std::to_string(kSeriesCap) + " terms");
+    if (j > 0) {
+      X = apply(op, X);
+      for (long k = 0; k < r; ++k) tpow[size_t(k)] = tpow[size_t(k)] * t[size_t(k)];
+    }
+    Mat M(p + 1, r);
+    for (long k = 0; k < r; ++k)
+      for (int i = 0; i <= p; ++i) M(i, k) = a(i, j) * gamma(i, k);
+    for (long k = 0; k < r; ++k)
+      for (long q = 0; q < n; ++q) {
+        double acc = 0.0;
+        for (int i = 0; i <= p; ++i) acc = acc + X(q, i) * M(i, k);
+        acc = acc * tpow[size_t(k)];
+        term(q, k) = acc;
+        G(q, k) = G(q, k) + acc;
+      }
+    c1 = c2;
+    c2 = inf_norm(term);
+    if (!std::isfinite(c2))
+      throw std::runtime_error("phimv_block: direct series produced a non-finite term at index " +
+                               std::to_string(j));
+    if (j >= 1 && c1 + c2 <= tol * inf_norm(G)) break;
+  }
+  return G;
+}
+
+// ---------------------------------------------------------------------------
 // The evaluator's consumer
 // ---------------------------------------------------------------------------
 
@@ -1550,6 +1628,26 @@ int orc_dense_phi(int64_t d, const double* M, double t, int32_t jmax, double* ou
     auto phis = orc::dense_phi(Mm, t, jmax);
     for (int k = 0; k <= jmax; ++k)
       std::copy(phis[size_t(k)].a.begin(), phis[size_t(k)].a.end(), out + size_t(k) * size_t(d * d));
+  });
+}
+
+// --- block_series_direct ---
+// coeffs: NULL (phi_series_coeffs) or (p+1) x ncoef column-major a_ij
+int orc_block_series_direct(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                            int64_t r, const double* t, const double* alpha, int32_t p,
+                            const double* V, int64_t ldv, double tol, const double* coeffs,
+                            int64_t ncoef, double* G, int64_t ldg) {
+  return guarded([&] {
+    orc::Vec tv(t, t + r), av(alpha, alpha + r);
+    orc::Mat Vm = wrap(V, n, p + 1, ldv);
+    std::function<double(int, int)> cf = [&](int i, int j) -> double {
+      if (j >= ncoef) throw std::invalid_argument("block_series_direct: coefficient table exhausted");
+      return coeffs[size_t(i) + size_t(j) * size_t(p + 1)];
+    };
+    orc::Mat Gm = orc::block_series_direct(make_op(n, rp, ci, v), tv, av, Vm, tol,
+                                           coeffs ? &cf : nullptr);
+    for (int64_t k = 0; k < r; ++k)
+      for (int64_t q = 0; q < n; ++q) G[q + k * ldg] = Gm(q, k);
   });
 }
 

@@ -76,7 +76,7 @@ ABI_SYMBOLS = (
     "phx_phimv_block", "phx_phimv_block_device", "phx_phimv", "phx_last_error",
     "phx_kernel_launches", "phx_last_eval_stats", "phx_set_trace", "phx_get_trace",
     "phx_adr_csr", "phx_exprk4s6_step", "phx_integrate",
-    "phx_mm_read_csr", "phx_mm_write_csr", "phx_op_create_mm",
+    "phx_mm_read_csr", "phx_mm_write_csr", "phx_op_create_mm", "phx_block_series_direct",
 )
 
 
@@ -134,6 +134,8 @@ def lib():
     L.phx_mm_read_csr.argtypes = [C.c_char_p, i64p, i64p, i64p, i32p, dp, C.c_int64]
     L.phx_mm_write_csr.argtypes = [C.c_char_p, C.c_int64, i64p, i32p, dp]
     L.phx_op_create_mm.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]
+    L.phx_block_series_direct.argtypes = [C.c_void_p, C.c_int32, dp, dp, C.c_int32, dp,
+                                          C.c_int64, C.c_double, dp, C.c_int64, dp, C.c_int64]
     L.phx_last_eval_stats.argtypes = [dp, i64p]
     L.phx_set_trace.argtypes = [C.c_int64]
     L.phx_get_trace.argtypes = [dp, C.c_int64, i64p]
@@ -185,6 +187,11 @@ class ScalingShift:
 
     def astuple(self):
         return (self.s, self.xi, self.s0, self.f_min, self.m, self.r)
+
+
+def default_tolerance() -> float:
+    """The evaluator's default tolerance 2^-53 (params.hpp:15)."""
+    return 2.0 ** -53
 
 
 @dataclass
@@ -664,4 +671,36 @@ def write_matrix_market(path, n, row_ptr, col_idx, vals):
     av = np.ascontiguousarray(vals, dtype=np.float64)
     _check(lib().phx_mm_write_csr(os.fsencode(path), int(n), rp.ctypes.data_as(i64p),
                                   ci.ctypes.data_as(i32p), _d(av)))
+
+
+# ---------------------------------------------------------------------------
+# block_series_direct: the reference's cross-check
+def phi_series_coeffs(p: int, ncoef: int) -> np.ndarray:
+    """a_ij = 1/(i+j)! for i <= p, j < ncoef on phi_series_coeffs' chain
+    (phi_block.cpp:158-169), as a (p+1) x ncoef table."""
+    inv = [1.0]
+    while len(inv) <= p + ncoef:
+        inv.append(inv[-1] / float(len(inv)))
+    return np.array([[inv[i + j] for j in range(ncoef)] for i in range(p + 1)], order="F")
+
+
+def block_series_direct(op: CsrOperator, req: BlockPhiRequest, coeffs=None) -> np.ndarray:
+    """G = sum_j A^j V D_j Gamma T^j on the device (phx_block_series_direct);
+    coeffs: None (phi_series_coeffs) or a (p+1) x ncoef table of a_ij."""
+    t = np.ascontiguousarray(np.atleast_1d(req.t), dtype=np.float64)
+    alpha = np.ascontiguousarray(np.atleast_1d(req.alpha), dtype=np.float64)
+    if alpha.size != t.size:
+        raise ValueError("phimv_block: t and alpha lengths differ")
+    V = np.asarray(req.V, dtype=np.float64)
+    if V.ndim == 1:
+        V = V.reshape(-1, 1)
+    if V.shape[0] != op.n:
+        raise ValueError("phimv_block: V row count does not match operator")
+    V = np.asfortranarray(V)
+    G = np.empty((op.n, max(1, t.size)), order="F")
+    cf = None if coeffs is None else np.asfortranarray(np.asarray(coeffs, dtype=np.float64))
+    _check(lib().phx_block_series_direct(op._h, t.size, _d(t), _d(alpha), V.shape[1] - 1, _d(V),
+                                         op.n, float(req.tol), None if cf is None else _d(cf),
+                                         0 if cf is None else cf.shape[1], _d(G), op.n))
+    return G
 

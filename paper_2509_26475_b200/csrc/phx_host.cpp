@@ -1645,6 +1645,106 @@ phx_status phx_integrate(phx_op op, double gamma, const double* u0, double h, do
   });
 }
 
+phx_status phx_block_series_direct(phx_op op, int32_t r, const double* t, const double* alpha,
+                                  int32_t p, const double* V, int64_t ldv, double tol,
+                                  const double* coeffs, int64_t ncoef, double* G, int64_t ldg) {
+  return guarded([&] {
+    if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    check_block_request(op, r, t, alpha, p, V, ldv, true);
+    if (!V || !G) throw_phx(PHX_EINVAL, "block_series_direct: null argument");
+    if (ldg < op->n) throw_phx(PHX_EINVAL, "block_series_direct: G leading dimension below n");
+    if (op->nparts > 1)
+      throw_phx(PHX_EINVAL, "block_series_direct: row-partitioned operators are not supported");
+    if (r > phx::kSeriesMaxR)
+      throw_phx(PHX_EINVAL, "block_series_direct: more than " + std::to_string(phx::kSeriesMaxR) +
+                                " abscissae are not supported");
+    const int64_t n = op->n;
+    for (int32_t j = 0; j <= p; ++j)
+      if (!finite_all(V + size_t(j) * size_t(ldv), size_t(n)))
+        throw_phx(PHX_EINVAL, "phimv_block: inputs must be finite");
+    const double rtol = tol > 0.0 ? tol : std::ldexp(1.0, -53);  // default_tolerance
+    const int32_t p1 = p + 1;
+    // coefficients a_ij: the table, or phi_series_coeffs (:158-169)
+    std::vector<double> inv_fact{1.0};
+    auto coef = [&](int i, int j) -> double {
+      if (coeffs) {
+        if (j >= ncoef)
+          throw_phx(PHX_EINVAL, "block_series_direct: coefficient table exhausted");
+        return coeffs[size_t(i) + size_t(j) * size_t(p1)];
+      }
+      while (int(inv_fact.size()) <= i + j)
+        inv_fact.push_back(inv_fact.back() / double(inv_fact.size()));
+      return inv_fact[size_t(i + j)];
+    };
+    std::vector<double> gamma(size_t(p1) * size_t(r));  // [alpha_k^i]
+    for (int32_t k = 0; k < r; ++k) {
+      double power = 1.0;
+      for (int32_t i = 0; i <= p; ++i) {
+        gamma[size_t(i) + size_t(k) * size_t(p1)] = power;
+        power *= alpha[k];
+      }
+    }
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    cudaStream_t st = op->stream;
+    DevBuf bX0, bX1, bG, bM, bT, bS;
+    struct Rel {
+      std::vector<DevBuf*> b;
+      ~Rel() {
+        for (DevBuf* x : b) x->release();
+      }
+    } rel{{&bX0, &bX1, &bG, &bM, &bT, &bS}};
+    double* X0 = bX0.as<double>(size_t(n) * size_t(p1));
+    double* X1 = bX1.as<double>(size_t(n) * size_t(p1));
+    double* dG = bG.as<double>(size_t(n) * size_t(r));
+    double* dM = bM.as<double>(size_t(p1) * size_t(r));
+    double* dT = bT.as<double>(size_t(r));
+    unsigned long long* slots = bS.as<unsigned long long>(2);
+    if (ldv == n)
+      PHX_CUDA(cudaMemcpyAsync(X0, V, size_t(n) * size_t(p1) * 8, cudaMemcpyHostToDevice, st));
+    else
+      PHX_CUDA(cudaMemcpy2DAsync(X0, size_t(n) * 8, V, size_t(ldv) * 8, size_t(n) * 8, size_t(p1),
+                                 cudaMemcpyHostToDevice, st));
+    PHX_CUDA(cudaMemsetAsync(dG, 0, size_t(n) * size_t(r) * 8, st));
+    std::vector<double> tpow(size_t(r), 1.0), M(size_t(p1) * size_t(r));
+    unsigned long long* hs = op->h_small.as<unsigned long long>(2);
+    double c1 = std::numeric_limits<double>::infinity(), c2 = 0.0;
+    for (int j = 0;; ++j) {
+      if (j >= 500)  // kSeriesCap (phi_single.hpp:11)
+        throw_phx(PHX_ENUMERIC, "phimv_block: direct series did not converge within 500 terms");
+      if (j > 0) {
+        PHX_CUDA(phx::launch_spmm_cols(int32_t(n), p1, op->d_rp, op->d_ci, op->d_av, X0, X1, 0, 0.0,
+                                       st));
+        std::swap(X0, X1);
+        for (int32_t k = 0; k < r; ++k) tpow[size_t(k)] = tpow[size_t(k)] * t[k];
+      }
+      for (int32_t k = 0; k < r; ++k)
+        for (int32_t i = 0; i <= p; ++i)
+          M[size_t(i) + size_t(k) * size_t(p1)] = coef(i, j) * gamma[size_t(i) + size_t(k) * size_t(p1)];
+      PHX_CUDA(cudaMemcpyAsync(dM, M.data(), M.size() * 8, cudaMemcpyHostToDevice, st));
+      PHX_CUDA(cudaMemcpyAsync(dT, tpow.data(), tpow.size() * 8, cudaMemcpyHostToDevice, st));
+      PHX_CUDA(cudaMemsetAsync(slots, 0, 16, st));
+      PHX_CUDA(phx::launch_series_term(int32_t(n), p1, r, X0, dM, dT, dG, slots, st));
+      PHX_CUDA(cudaMemcpyAsync(hs, slots, 16, cudaMemcpyDeviceToHost, st));
+      PHX_CUDA(cudaStreamSynchronize(st));  // M / tpow reuse and the stopping test
+      double normG;
+      c1 = c2;
+      std::memcpy(&c2, &hs[0], 8);
+      std::memcpy(&normG, &hs[1], 8);
+      if (!std::isfinite(c2))
+        throw_phx(PHX_ENUMERIC, "phimv_block: direct series produced a non-finite term at index " +
+                                    std::to_string(j));
+      if (j >= 1 && c1 + c2 <= rtol * normG) break;
+    }
+    if (ldg == n)
+      PHX_CUDA(cudaMemcpyAsync(G, dG, size_t(n) * size_t(r) * 8, cudaMemcpyDeviceToHost, st));
+    else
+      PHX_CUDA(cudaMemcpy2DAsync(G, size_t(ldg) * 8, dG, size_t(n) * 8, size_t(n) * 8, size_t(r),
+                                 cudaMemcpyDeviceToHost, st));
+    PHX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 phx_status phx_last_eval_stats(double* kernel_ms, int64_t* steps) {
   std::lock_guard<std::mutex> lk(g_trace_mu);
   if (kernel_ms) *kernel_ms = g_last_ms;

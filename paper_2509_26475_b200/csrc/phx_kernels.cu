@@ -252,6 +252,61 @@ cudaError_t launch_rk_stage(const RkStageArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// block_series_direct term (phi_block.cpp:186-209): one thread per row;
+// term(i,k) = (sum_q X(i,q) M(q,k) from +0, ascending q) * tpow_k,
+// G(i,k) += term(i,k); the canonical |.| row sums of term and G (pairwise
+// tree over pow2-padded columns) max-reduced into slots[0], slots[1].
+__global__ void __launch_bounds__(kBlock)
+    k_series_term(int32_t n, int32_t p1, int32_t r, const double* __restrict__ X,
+                  const double* __restrict__ M, const double* __restrict__ tpow, double* G,
+                  unsigned long long* slots) {
+  unsigned long long mt = 0, mg = 0;
+  int len = 1;
+  while (len < r) len <<= 1;
+  for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
+    double ta[kSeriesMaxR], ga[kSeriesMaxR];
+    for (int k = 0; k < len; ++k) {
+      if (k < r) {
+        double acc = 0.0;
+        for (int q = 0; q < p1; ++q) acc = acc + X[i + size_t(q) * n] * M[q + k * p1];
+        acc = acc * tpow[k];
+        const double g = G[i + size_t(k) * n] + acc;
+        G[i + size_t(k) * n] = g;
+        ta[k] = fabs(acc);
+        ga[k] = fabs(g);
+      } else {
+        ta[k] = ga[k] = 0.0;
+      }
+    }
+    for (int h = 1; h < len; h <<= 1)
+      for (int l = 0; l < len; l += 2 * h) {
+        ta[l] = ta[l] + ta[l + h];
+        ga[l] = ga[l] + ga[l + h];
+      }
+    mt = umax64(mt, abs_bits(ta[0]));
+    mg = umax64(mg, abs_bits(ga[0]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mt = umax64(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+    mg = umax64(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(slots, mt);
+    atomicMax(slots + 1, mg);
+  }
+}
+
+cudaError_t launch_series_term(int32_t n, int32_t p1, int32_t r, const double* X, const double* M,
+                               const double* tpow, double* G, unsigned long long* slots,
+                               cudaStream_t st) {
+  if (r > kSeriesMaxR) return cudaErrorInvalidValue;
+  ++g_launches;
+  const int grid = std::max(1, std::min(148 * 8, (n + kBlock - 1) / kBlock));
+  k_series_term<<<grid, kBlock, 0, st>>>(n, p1, r, X, M, tpow, G, slots);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gemv(int32_t n, int32_t ncol, const double* B, const double* c, double* y,
                         unsigned long long* chunkmax, cudaStream_t st) {
   if (ncol > 128) return cudaErrorInvalidValue;

@@ -48,6 +48,9 @@ class OracleImpl:
     def phimv(self, op, t, alpha, V, tol, params):
         return O.phimv(op, t, alpha, V, tol, O.ScalingShift(*params.astuple()))
 
+    def series_direct(self, op, t, alpha, V, tol, coeffs=None):
+        return O.block_series_direct(op, t, alpha, V, tol, coeffs)
+
     # integrator.cpp: (u_next, records) / (u, t, records)
     def rk_step(self, op, gamma, u, h, tol, params):
         return O.exprk4s6_step(op, gamma, u, h, tol, O.ScalingShift(*params.astuple()))
@@ -103,6 +106,12 @@ class GpuImpl:
         P = self.P
         res = P.phimv(op, P.PhiRequest(t, alpha, V, tol, P.ScalingShift(*params.astuple())))
         return res.w, res.exp_v0, res.tail, res.stats
+
+    def series_direct(self, op, t, alpha, V, tol, coeffs=None):
+        P = self.P
+        req = P.BlockPhiRequest(np.atleast_1d(t), np.atleast_1d(alpha), V, tol,
+                                P.ScalingShift(1.0, 0.0, 1.0, 0.0, 61, 0))
+        return P.block_series_direct(op, req, coeffs)
 
     def _problem(self, op, gamma, u0):
         return self.P.ADRProblem(0, 0, 0.0, 0.0, float(gamma), op, np.asarray(u0, dtype=float))
