@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
                 }
                 if (vq[rr][q]) {
                   const unsigned o = unsigned(row) * ldf + c[q];
-                  Vio<V>::st(Fn + o, y[q]);
+                  Vio<V>::stcs(Fn + o, y[q]);  // next term only: evict-first
                   Vio<V>::stcs(a.E + o, en[q]);
                 }
               }
