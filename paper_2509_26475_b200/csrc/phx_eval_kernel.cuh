@@ -72,7 +72,6 @@ struct Vio<2> {
     __stcs(reinterpret_cast<double2*>(p), make_double2(x[0], x[1]));
   }
 };
-
 template <int Q, int V, int R_>
 struct Cfg {
   static constexpr int R = R_;  // rows per lane group per warp tile
@@ -658,11 +657,11 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
                 Vio<V>::ldcs(a.S + o, so[rr][q]);
                 if (has_xi) Vio<V>::ld(Dc + o, ds[rr][q]);
                 if (vwl_vec) {
-                  if (jj[q][0] >= 2) Vio<V>::ld(a.Vw + (o - unsigned(r)), vwl[rr][q]);
+                  if (jj[q][0] >= 2) Vio<V>::ldcs(a.Vw + (o - unsigned(r)), vwl[rr][q]);
                 } else {
 #pragma unroll
                   for (int e = 0; e < V; ++e)
-                    if (jj[q][e] >= 2) vwl[rr][q][e] = a.Vw[o + e - unsigned(r)];
+                    if (jj[q][e] >= 2) vwl[rr][q][e] = __ldcs(a.Vw + (o + e - unsigned(r)));
                 }
               }
             }

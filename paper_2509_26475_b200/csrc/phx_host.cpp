@@ -813,7 +813,13 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   // R rows per lane group: 2 for short rows (the per-tile pipeline overhead
   // dominates) or scalar lanes, else 1 (more resident warps)
   const double avg_nnz = double(op->nnz) / double(n);
-  const int32_t R = (QT == 1 && (V == 1 || avg_nnz < 2.5)) ? 2 : 1;
+  static const int force_r = [] {  // developer knob: PHX_FORCE_R = 1 | 2
+    const char* e = std::getenv("PHX_FORCE_R");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int32_t R = (QT == 1 && force_r >= 1 && force_r <= 2)
+                        ? force_r
+                        : ((QT == 1 && (V == 1 || avg_nnz < 2.5)) ? 2 : 1);
   const int32_t tile = 8 * (32 / std::min(GS, GF)) * R;
   // share of each phase's tiles assigned statically (the rest are grabbed
   // dynamically to absorb per-CTA speed differences); PHX_STATIC_FRAC tunes it
