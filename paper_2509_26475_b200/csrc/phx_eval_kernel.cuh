@@ -79,6 +79,10 @@ struct Cfg {
   static constexpr int B = (Q == 1 && V == 2 && R_ == 1) ? 8 : ((Q * V * R_ <= 4) ? 4 : 2);
   // resident CTAs per SM the register budget is sized for
   static constexpr int MINB = (Q * V * R_ <= 2) ? 4 : ((Q * V * R_ <= 4) ? 3 : ((Q * V <= 4) ? 2 : 1));
+  // row-local accumulator streams loaded after the gather (its batch gets the
+  // registers) for scalar lanes (C4: 116 -> 97 ms); the double2 variants load
+  // them first, hiding their latency behind the gather (measured: C2, C5)
+  static constexpr bool LATE = V == 1;
 };
 
 // Lane-group layout of one phase (S width or F width).
@@ -637,9 +641,17 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
         }
       run_tiles<DYN>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
                 [&](int base, const int* rp, const int* ci, const double* avs) {
-          // row-local streams first (independent of the CSR slice)
+          // row-local streams (independent of the CSR slice): before or after
+          // the gather (Cfg::LATE)
           double vw[R][Q][V], vwl[R][Q][V], so[R][Q][V], ds[R][Q][V], acc[R][Q][V];
           bool vq[R][Q];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e) acc[rr][q][e] = 0.0;
+          auto streams = [&]() {
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) {
             const int row = base + rr * LS.gpw + LS.g;
@@ -650,7 +662,6 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
 #pragma unroll
               for (int e = 0; e < V; ++e) {
                 vw[rr][q][e] = vwl[rr][q][e] = so[rr][q][e] = ds[rr][q][e] = 0.0;
-                acc[rr][q][e] = 0.0;
               }
               if (vq[rr][q]) {
                 Vio<V>::ldcs(a.Vw + o, vw[rr][q]);
@@ -666,7 +677,10 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
               }
             }
           }
+          };
+          if constexpr (!Cfg<Q, V, RR>::LATE) streams();
           gather_tile<Q, V, R, B, PART>(a, LS, rp, ci, avs, ldb, Dc, gtab[dpar], c, v, acc);
+          if constexpr (Cfg<Q, V, RR>::LATE) streams();
           double vn[R][Q][V], dn[R][Q][V], sn[R][Q][V];
 #pragma unroll
           for (int rr = 0; rr < R; ++rr)
@@ -848,21 +862,31 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
             double eo[R][Q][V], fs[R][Q][V], acc[R][Q][V];
             bool vq[R][Q];
 #pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-              const int row = base + rr * LF.gpw + LF.g;
+            for (int rr = 0; rr < R; ++rr)
 #pragma unroll
-              for (int q = 0; q < Q; ++q) {
-                vq[rr][q] = row < n && v[q];
-                const unsigned o = unsigned(row) * ldf + c[q];
+              for (int q = 0; q < Q; ++q)
 #pragma unroll
-                for (int e = 0; e < V; ++e) eo[rr][q][e] = fs[rr][q][e] = acc[rr][q][e] = 0.0;
-                if (vq[rr][q]) {
-                  Vio<V>::ldcs(a.E + o, eo[rr][q]);
-                  if (has_xi) Vio<V>::ld(Fc + o, fs[rr][q]);
+                for (int e = 0; e < V; ++e) acc[rr][q][e] = 0.0;
+            auto streams = [&]() {  // before or after the gather (Cfg::LATE)
+#pragma unroll
+              for (int rr = 0; rr < R; ++rr) {
+                const int row = base + rr * LF.gpw + LF.g;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                  vq[rr][q] = row < n && v[q];
+                  const unsigned o = unsigned(row) * ldf + c[q];
+#pragma unroll
+                  for (int e = 0; e < V; ++e) eo[rr][q][e] = fs[rr][q][e] = 0.0;
+                  if (vq[rr][q]) {
+                    Vio<V>::ldcs(a.E + o, eo[rr][q]);
+                    if (has_xi) Vio<V>::ld(Fc + o, fs[rr][q]);
+                  }
                 }
               }
-            }
+            };
+            if constexpr (!Cfg<Q, V, RR>::LATE) streams();
             gather_tile<Q, V, R, B, PART>(a, LF, rp, ci, avs, ldf, Fc, gtab[3 + fpar], c, v, acc);
+            if constexpr (Cfg<Q, V, RR>::LATE) streams();
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
               const int row = base + rr * LF.gpw + LF.g;
