@@ -6,15 +6,19 @@ namespace phx {
 
 namespace {
 
-bool select_kernel(int QT, int V, int R, bool part, bool dyn, EvalKernel* k) {
-  return eval_kernels_q1v1(QT, V, R, part, dyn, k) || eval_kernels_q1v2(QT, V, R, part, dyn, k) ||
-         eval_kernels_q2(QT, V, R, part, dyn, k) || eval_kernels_q4(QT, V, R, part, dyn, k) ||
-         eval_kernels_q8(QT, V, R, part, dyn, k);
+bool select_kernel(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* k) {
+  return eval_kernels_q1v1(QT, V, R, part, dyn, small, k) ||
+         eval_kernels_q1v2a(QT, V, R, part, dyn, small, k) ||
+         eval_kernels_q1v2b(QT, V, R, part, dyn, small, k) ||
+         eval_kernels_q2(QT, V, R, part, dyn, small, k) ||
+         eval_kernels_q4(QT, V, R, part, dyn, small, k) ||
+         eval_kernels_q8(QT, V, R, part, dyn, small, k);
 }
 
 }  // namespace
 
-cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, int block, int* max_blocks) {
+cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, bool small, int block,
+                           int* max_blocks) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -22,7 +26,7 @@ cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, int block,
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
   EvalKernel k{};
-  if (!select_kernel(QT, V, R, part, dyn, &k)) return cudaErrorInvalidValue;
+  if (!select_kernel(QT, V, R, part, dyn, small, &k)) return cudaErrorInvalidValue;
   int per_sm = 0;
   e = k.occ(block, &per_sm);
   if (e != cudaSuccess) return e;
@@ -34,7 +38,8 @@ cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStre
   BlockArgs copy = a;
   void* args[] = {&copy};
   EvalKernel k{};
-  if (!select_kernel(a.QT, a.vec, a.R, a.nparts > 1, a.dyn != 0, &k)) return cudaErrorInvalidValue;
+  if (!select_kernel(a.QT, a.vec, a.R, a.nparts > 1, a.dyn != 0, a.bsmall != 0, &k))
+    return cudaErrorInvalidValue;
   count_launch();
   return cudaLaunchCooperativeKernel(k.fn, grid, block, args, 0, st);
 }

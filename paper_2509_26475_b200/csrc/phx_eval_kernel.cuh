@@ -76,6 +76,8 @@ template <int Q, int V, int R_>
 struct Cfg {
   static constexpr int R = R_;  // rows per lane group per warp tile
   // gather batch: entries in flight per lane group
+  // (the kernels' BO template argument overrides it: a batch that matches the
+  // operator's row length issues no predicated-off slots -- DESIGN.md §4)
   static constexpr int B = (Q == 1 && V == 2 && R_ == 1) ? 8 : ((Q * V * R_ <= 4) ? 4 : 2);
   // resident CTAs per SM the register budget is sized for
   static constexpr int MINB = (Q * V * R_ <= 2) ? 4 : ((Q * V * R_ <= 4) ? 3 : ((Q * V <= 4) ? 2 : 1));
@@ -386,10 +388,10 @@ __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L,
     gather<Q, V, R, B, false, PART>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
 }
 
-template <int Q, int V, int RR, bool PART, bool DYN>
+template <int Q, int V, int RR, bool PART, bool DYN, int BO>
 __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs ga) {
   constexpr int R = Cfg<Q, V, RR>::R;
-  constexpr int B = Cfg<Q, V, RR>::B;
+  constexpr int B = BO > 0 ? BO : Cfg<Q, V, RR>::B;  // gather batch
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long red[2][kWarps];
   __shared__ WarpPipe pipe[kWarps];
@@ -1047,30 +1049,43 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   finish(err, err_idx, L_S, 0);
 }
 
-template <int Q, int V, int R, bool PART, bool DYN>
+template <int Q, int V, int R, bool PART, bool DYN, int BO>
 cudaError_t eval_occupancy(int block, int* per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_phimv_block<Q, V, R, PART, DYN>,
-                                                       block, 0);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      per_sm, k_phimv_block<Q, V, R, PART, DYN, BO>, block, 0);
 }
 
-template <int Q, int V, int R, bool PART, bool DYN>
+template <int Q, int V, int R, bool PART, bool DYN, int BO = 0>
 EvalKernel eval_kernel() {
-  return EvalKernel{reinterpret_cast<const void*>(k_phimv_block<Q, V, R, PART, DYN>),
-                    eval_occupancy<Q, V, R, PART, DYN>};
+  return EvalKernel{reinterpret_cast<const void*>(k_phimv_block<Q, V, R, PART, DYN, BO>),
+                    eval_occupancy<Q, V, R, PART, DYN, BO>};
 }
 
 }  // namespace
 
-// one instantiated (Q, V, R): unpartitioned static or dynamic-tail kernels,
-// partitioned kernels always with the dynamic tail
+// one instantiated (Q, V, R) with gather batch BO (0: Cfg's): unpartitioned
+// static or dynamic-tail kernels, partitioned kernels always with the
+// dynamic tail
+#define PHX_EVAL_KERNELS(q, v, r, bo)                          \
+  if (part)                                                    \
+    *out = eval_kernel<q, v, r, true, true, bo>();             \
+  else if (dyn)                                                \
+    *out = eval_kernel<q, v, r, false, true, bo>();            \
+  else                                                         \
+    *out = eval_kernel<q, v, r, false, false, bo>();
 #define PHX_EVAL_CASE(q, v, r)                                 \
   if (QT == q && V == v && R == r) {                           \
-    if (part)                                                  \
-      *out = eval_kernel<q, v, r, true, true>();               \
-    else if (dyn)                                              \
-      *out = eval_kernel<q, v, r, false, true>();              \
-    else                                                       \
-      *out = eval_kernel<q, v, r, false, false>();             \
+    PHX_EVAL_KERNELS(q, v, r, 0)                               \
+    return true;                                               \
+  }
+// ... and a second, short batch bs used for operators whose rows fit it
+#define PHX_EVAL_CASE2(q, v, r, bs)                            \
+  if (QT == q && V == v && R == r) {                           \
+    if (small) {                                               \
+      PHX_EVAL_KERNELS(q, v, r, bs)                            \
+    } else {                                                   \
+      PHX_EVAL_KERNELS(q, v, r, 0)                             \
+    }                                                          \
     return true;                                               \
   }
 

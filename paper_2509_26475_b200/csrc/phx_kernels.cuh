@@ -60,6 +60,7 @@ struct BlockArgs {
   int32_t R;       // rows per lane group per warp tile (1 or 2; 2 only when QT == 1)
   int32_t tile;    // rows per tile (row -> CTA mapping, independent of layout)
   int32_t dyn;          // 1: dynamic-tail kernel (always for partitioned runs)
+  int32_t bsmall;       // 1: the short-gather-batch variant (rows fit it)
   double static_frac;  // DYN kernels: share of a phase's CTA tiles assigned statically
   // scalars
   double xi, tol;
@@ -118,7 +119,8 @@ enum : int32_t {
 
 // launch wrappers (phx_kernels.cu)
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st);
-cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, int block, int* max_blocks);
+cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, bool small, int block,
+                           int* max_blocks);
 
 // one instantiated kernel variant and its occupancy query
 struct EvalKernel {
@@ -126,12 +128,13 @@ struct EvalKernel {
   cudaError_t (*occ)(int block, int* per_sm);
 };
 // per-file variant tables (phx_eval_q*.cu): true when the file holds the
-// variant (QT, V, R, partitioned, dynamic tail)
-bool eval_kernels_q1v1(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
-bool eval_kernels_q1v2(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
-bool eval_kernels_q2(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
-bool eval_kernels_q4(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
-bool eval_kernels_q8(int QT, int V, int R, bool part, bool dyn, EvalKernel* out);
+// variant (QT, V, R, partitioned, dynamic tail, short gather batch)
+bool eval_kernels_q1v1(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
+bool eval_kernels_q1v2a(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
+bool eval_kernels_q1v2b(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
+bool eval_kernels_q2(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
+bool eval_kernels_q4(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
+bool eval_kernels_q8(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
 
 // y = f(A x) with mode 0: A x, 1: A x - fl(xi x), 2: (A x) / div ; fused
 // per-chunk max|y| into chunkmax (bit patterns) when chunkmax != nullptr
