@@ -34,6 +34,11 @@ cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, bool small
   return cudaSuccess;
 }
 
+#ifndef PHX_X_BLOCK
+#define PHX_X_BLOCK 256
+#endif
+int eval_block_size() { return PHX_X_BLOCK; }
+
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st) {
   BlockArgs copy = a;
   void* args[] = {&copy};
@@ -41,7 +46,10 @@ cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStre
   if (!select_kernel(a.QT, a.vec, a.R, a.nparts > 1, a.dyn != 0, a.bsmall != 0, &k))
     return cudaErrorInvalidValue;
   count_launch();
-  return cudaLaunchCooperativeKernel(k.fn, grid, block, args, 0, st);
+  int per_sm = 0;  // also sets the dynamic shared memory attribute of the variant
+  const cudaError_t e = k.occ(block, &per_sm);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchCooperativeKernel(k.fn, grid, block, args, eval_pipe_bytes(), st);
 }
 
 }  // namespace phx

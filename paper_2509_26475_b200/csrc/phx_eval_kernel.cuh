@@ -26,7 +26,10 @@ namespace phx {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kBlock = 256;
+#ifndef PHX_X_BLOCK
+#define PHX_X_BLOCK 256
+#endif
+constexpr int kBlock = PHX_X_BLOCK;  // threads per CTA
 constexpr int kWarps = kBlock / 32;
 constexpr int kMaxRW = 64;  // rows per warp tile
 constexpr double DBL_MAX_D = 1.7976931348623157e308;
@@ -80,7 +83,9 @@ struct Cfg {
   // operator's row length issues no predicated-off slots -- DESIGN.md §4)
   static constexpr int B = (Q == 1 && V == 2 && R_ == 1) ? 8 : ((Q * V * R_ <= 4) ? 4 : 2);
   // resident CTAs per SM the register budget is sized for
-  static constexpr int MINB = (Q * V * R_ <= 2) ? 4 : ((Q * V * R_ <= 4) ? 3 : ((Q * V <= 4) ? 2 : 1));
+  static constexpr int MINB0 = (Q * V * R_ <= 2) ? 4 : ((Q * V * R_ <= 4) ? 3 : ((Q * V <= 4) ? 2 : 1));
+  // (the budgets above are for 256-thread CTAs)
+  static constexpr int MINB = MINB0 * 256 / kBlock > 0 ? MINB0 * 256 / kBlock : 1;
   // row-local accumulator streams loaded after the gather (its batch gets the
   // registers) for scalar lanes (C4: 116 -> 97 ms); the double2 variants load
   // them first, hiding their latency behind the gather (measured: C2, C5)
@@ -394,7 +399,9 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   constexpr int B = BO > 0 ? BO : Cfg<Q, V, RR>::B;  // gather batch
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long red[2][kWarps];
-  __shared__ WarpPipe pipe[kWarps];
+  // per-warp pipeline buffers: dynamic shared memory (kWarps * sizeof(WarpPipe))
+  extern __shared__ __align__(16) unsigned char pipe_smem[];
+  WarpPipe* pipe = reinterpret_cast<WarpPipe*>(pipe_smem);
   // gather tables [D0, D1, S, F0, F1][part] (PART only)
   __shared__ const double* gtab[5][PART ? kMaxParts : 1];
   __shared__ double gmax[2];
@@ -1049,10 +1056,16 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   finish(err, err_idx, L_S, 0);
 }
 
+constexpr size_t kPipeBytes = size_t(kWarps) * sizeof(WarpPipe);  // dynamic smem per CTA
+
 template <int Q, int V, int R, bool PART, bool DYN, int BO>
 cudaError_t eval_occupancy(int block, int* per_sm) {
+  const cudaError_t e = cudaFuncSetAttribute(k_phimv_block<Q, V, R, PART, DYN, BO>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(kPipeBytes));
+  if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      per_sm, k_phimv_block<Q, V, R, PART, DYN, BO>, block, 0);
+      per_sm, k_phimv_block<Q, V, R, PART, DYN, BO>, block, kPipeBytes);
 }
 
 template <int Q, int V, int R, bool PART, bool DYN, int BO = 0>

@@ -11,4 +11,7 @@ bool eval_kernels_q1v1(int QT, int V, int R, bool part, bool dyn, bool small, Ev
   return false;
 }
 
+// dynamic shared memory of every k_phimv_block variant (the per-warp pipes)
+size_t eval_pipe_bytes() { return kPipeBytes; }
+
 }  // namespace phx

@@ -670,7 +670,7 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     DeviceGuard guard(op->parts[size_t(q)].dev);
     PHX_CUDA(cudaStreamSynchronize(op->parts[size_t(q)].stream));
   }
-  const int block = 256;
+  const int block = phx::eval_block_size();
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const Group& g = groups[gi];
@@ -828,7 +828,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   if (QT > 8)
     throw_phx(PHX_EINVAL, std::string(who) + ": block width (p+1)*r above " +
                               std::to_string(256 * V) + " is not supported");
-  const int block = 256;
+  const int block = phx::eval_block_size();
   // rows per CTA tile: 8 warps x the larger warp tile (kernel: (32/G) * R rows,
   // R = 2 rows per lane group when QT == 1 and V == 1)
   // R rows per lane group: 2 for short rows (the per-tile pipeline overhead
@@ -841,7 +841,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   const int32_t R = (QT == 1 && force_r >= 1 && force_r <= 2)
                         ? force_r
                         : ((QT == 1 && (V == 1 || avg_nnz < 2.5)) ? 2 : 1);
-  const int32_t tile = 8 * (32 / std::min(GS, GF)) * R;
+  const int32_t tile = (block / 32) * (32 / std::min(GS, GF)) * R;
   // share of each phase's tiles assigned statically (the rest are grabbed
   // dynamically to absorb per-CTA speed differences); PHX_STATIC_FRAC tunes it
   static const double static_frac = [] {

@@ -119,6 +119,8 @@ enum : int32_t {
 
 // launch wrappers (phx_kernels.cu)
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st);
+int eval_block_size();     // threads per CTA of k_phimv_block
+size_t eval_pipe_bytes();  // its dynamic shared memory per CTA
 cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, bool small, int block,
                            int* max_blocks);
 
