@@ -64,6 +64,7 @@ def lib():
         L.orc_inf_norm.restype = C.c_double
         L.orc_inf_norm.argtypes = [dp, C.c_int64, C.c_int64, C.c_int64]
         L.orc_apply.argtypes = [C.c_int64, i64p, i32p, dp, dp, C.c_int64, dp]
+        L.orc_shifted_apply.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, dp, C.c_int64, dp]
         L.orc_basis_build.restype = C.c_void_p
         L.orc_basis_build.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int32, C.c_double, i32p]
         L.orc_basis_free.argtypes = [C.c_void_p]
@@ -205,6 +206,14 @@ def apply(op: Csr, X):
     X = np.asfortranarray(np.asarray(X, dtype=np.float64).reshape(op.n, -1))
     Y = np.empty_like(X, order="F")
     _check(lib().orc_apply(*op.args(), _d(X), X.shape[1], _d(Y)))
+    return Y
+
+
+def shifted_apply(op: Csr, xi, X):
+    """shifted_apply (linop.cpp:40-49): A X, or A X - fl(xi X) when xi != 0."""
+    X = np.asfortranarray(np.asarray(X, dtype=np.float64).reshape(op.n, -1))
+    Y = np.empty_like(X, order="F")
+    _check(lib().orc_shifted_apply(*op.args(), float(xi), _d(X), X.shape[1], _d(Y)))
     return Y
 
 

@@ -1508,6 +1508,16 @@ int orc_apply(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, 
   return guarded([&] { orc::apply_into(make_op(n, rp, ci, v), X, n, k, Y, n); });
 }
 
+// shifted_apply (linop.cpp:40-49)
+int orc_shifted_apply(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, double xi,
+                      const double* X, int64_t k, double* Y) {
+  return guarded([&] {
+    orc::Mat Xm = wrap(X, n, k, n);
+    orc::Mat Ym = orc::shifted_apply(make_op(n, rp, ci, v), xi, Xm);
+    std::copy(Ym.a.begin(), Ym.a.end(), Y);
+  });
+}
+
 // --- power basis handle (params.hpp:22-29, 50-71) ---
 void* orc_basis_build(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, int32_t m,
                       double delta, int32_t* err) {

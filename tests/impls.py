@@ -23,6 +23,9 @@ class OracleImpl:
     def apply(self, op, X):
         return O.apply(op, X)
 
+    def shifted_apply(self, op, xi, X):
+        return O.shifted_apply(op, xi, X)
+
     def select_parameters(self, op, m=61, tol=-1.0, delta=0.8):
         return O.select_parameters(op, m, tol, delta)
 
@@ -75,6 +78,9 @@ class GpuImpl:
 
     def apply(self, op, X):
         return op.apply(np.asarray(X).reshape(op.n, -1))
+
+    def shifted_apply(self, op, xi, X):
+        return op.shifted_apply(xi, np.asarray(X).reshape(op.n, -1))
 
     def select_parameters(self, op, m=61, tol=-1.0, delta=0.8):
         return self.P.select_parameters(op, m, tol, delta)

@@ -66,3 +66,16 @@ def test_adr_order_study_on_device():
     for r in out[1:]:
         assert r.order >= 3.5 and r.ok, R.rows_to_csv(out)
     assert all(r.matvecs > 0 and r.s_effective >= 1 for r in out)
+
+
+def test_reference_writer_checks(tmp_path):  # test_bench.cpp:42-73
+    row = R.ResultRow(experiment="gallery", label="identity_10", t=1.0, error=1e-16,
+                      seconds=0.01, s_effective=1, series_len_S=7, sweeps=0, matvecs=42,
+                      bound=1e-13)
+    csv = R.rows_to_csv([row])
+    assert csv.startswith("experiment,label,t,error") and "identity_10" in csv
+    assert '"matvecs": 42' in R.rows_to_json([row])
+    cfg = R.BenchConfig(out_path=str(tmp_path / "bench_rows_test.csv"), format="csv")
+    R.write_rows([row], cfg)
+    assert (tmp_path / "bench_rows_test.csv").read_text() == csv
+
