@@ -615,6 +615,49 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   double c1 = INF, c2 = mD, nS = mD;  // c2 = inf_norm(D) = ||S|| at k = 1 (S = D = Vw)
   trace(0.0, c2, nS);
 
+  // ||S||_inf for the stopping test without a row sum of S in every term:
+  // S_k = S_{k-1} + D_k/sigma, so ||S_{k-1}|| -+ c2 bound ||S_k|| (triangle
+  // inequality; widened by 1e-12 relative, far above the ~15u the rounded
+  // sums can move).  fl(tol * x) is monotone in x, so c1 + c2 > fl(tol * U)
+  // proves "continue" and c1 + c2 <= fl(tol * L) proves "stop" -- the
+  // reference's decision (phi_block.cpp:93) -- and only an inconclusive term
+  // (typically the last one or two) pays an exact pass over S, the same
+  // canonical row sums the fused epilogue computed.  With a trace requested,
+  // every term gets the exact pass (the trace records ||S||).
+  auto s_norm_exact = [&]() -> double {
+    unsigned long long m = 0;
+    unsigned c[Q];
+    bool v[Q];
+    cols(LS, c, v);
+    for (int t = cta; t < ntiles; t += ncta)
+      for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+        const int base = t * a.tile + wt * LS.RW;
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = base + rr * LS.gpw + LS.g;
+          const bool rv = row < n;
+          double as[Q][V];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            double x[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) x[e] = 0.0;
+            if (rv && v[q]) Vio<V>::ld(a.S + (unsigned(row) * ldb + c[q]), x);
+#pragma unroll
+            for (int e = 0; e < V; ++e) as[q][e] = (rv && v[q]) ? fabs(x[e]) : 0.0;
+          }
+          const double rs = group_rowsum<Q, V>(as, LS.G, LS.qp);
+          if (rv) m = umax64(m, abs_bits(rs));
+        }
+      }
+    double mx, dmy;
+    sync_step(m, m, mx, dmy);
+    return mx;
+  };
+  const bool exact_every_term = a.trace != nullptr;
+  double nSl = nS, nSu = nS;  // bounds of ||S||; equal to nS while it is exact
+  bool exact = true;
+
   // ================= S series (phi_block.cpp:93-106)
   int k = 1;
   double sigma = 1.0;
@@ -622,7 +665,22 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   double* Dn = a.D1;
   int err = kStOk, err_idx = 0;
   const bool vwl_vec = V == 2 && (r % 2) == 0;
-  while (c1 + c2 > a.tol * nS) {
+  for (;;) {
+    const double lhs = c1 + c2;
+    bool cont;
+    if (exact) {
+      cont = lhs > a.tol * nS;
+    } else if (lhs > a.tol * nSu) {
+      cont = true;
+    } else if (lhs <= a.tol * nSl) {
+      cont = false;
+    } else {
+      nS = s_norm_exact();
+      nSl = nSu = nS;
+      exact = true;
+      cont = lhs > a.tol * nS;
+    }
+    if (!cont) break;
     if (k >= 500) {
       err = kStSeriesCap;
       err_idx = 500;
@@ -631,7 +689,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
     ++k;
     c1 = c2;
     sigma *= k;
-    unsigned long long mdb = 0, msb = 0;
+    unsigned long long mdb = 0;
     {
       unsigned c[Q];
       bool v[Q];
@@ -713,7 +771,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) {
             const int row = base + rr * LS.gpw + LS.g;
-            double ad[Q][V], as[Q][V];
+            double ad[Q][V];
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
               if (vq[rr][q]) {
@@ -723,29 +781,29 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
                 Vio<V>::stcs(a.S + o, sn[rr][q]);
               }
 #pragma unroll
-              for (int e = 0; e < V; ++e) {
-                ad[q][e] = vq[rr][q] ? fabs(dn[rr][q][e]) : 0.0;
-                as[q][e] = vq[rr][q] ? fabs(sn[rr][q][e]) : 0.0;
-              }
+              for (int e = 0; e < V; ++e) ad[q][e] = vq[rr][q] ? fabs(dn[rr][q][e]) : 0.0;
             }
             const double rd = group_rowsum<Q, V>(ad, LS.G, LS.qp);
-            const double rsm = group_rowsum<Q, V>(as, LS.G, LS.qp);
-            if (row < n) {
-              mdb = umax64(mdb, abs_bits(rd));
-              msb = umax64(msb, abs_bits(rsm));
-            }
+            if (row < n) mdb = umax64(mdb, abs_bits(rd));
           }
                 });
     }
-    double maxD, maxS;
-    sync_step(mdb, msb, maxD, maxS);
+    double maxD, dmy;
+    sync_step(mdb, mdb, maxD, dmy);
     c2 = maxD / sigma;  // :103
     if (!isfinite(c2)) {
       err = kStSeriesDiverged;
       err_idx = k;
       break;
     }
-    nS = maxS;
+    nSu = (nSu + c2) * (1.0 + 1e-12);
+    nSl = (nSl - c2) * (1.0 - 1e-12);
+    exact = false;
+    if (exact_every_term) {
+      nS = s_norm_exact();
+      nSl = nSu = nS;
+      exact = true;
+    }
     trace(1.0, c2, nS);
     double* tmp = Dc;
     Dc = Dn;
@@ -838,12 +896,63 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   double fnorm, dummy;
   sync_step(mf, mf, fnorm, dummy);
 
+  // ||E||_inf for the recovery stopping test (phi_block.cpp:124), bounded
+  // like ||S|| above (E_kk = E_{kk-1} + F'_kk): an exact pass over E only for
+  // an inconclusive term or when a trace is requested
+  auto e_norm_exact = [&]() -> double {
+    unsigned long long m = 0;
+    unsigned c[Q];
+    bool v[Q];
+    cols(LF, c, v);
+    for (int t = cta; t < ntiles; t += ncta)
+      for (int wt = warp; wt < a.tile / LF.RW; wt += kWarps) {
+        const int base = t * a.tile + wt * LF.RW;
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = base + rr * LF.gpw + LF.g;
+          const bool rv = row < n;
+          double ae[Q][V];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            double x[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) x[e] = 0.0;
+            if (rv && v[q]) Vio<V>::ld(a.E + (unsigned(row) * ldf + c[q]), x);
+#pragma unroll
+            for (int e = 0; e < V; ++e) ae[q][e] = (rv && v[q]) ? fabs(x[e]) : 0.0;
+          }
+          const double rs = group_rowsum<Q, V>(ae, LF.G, LF.qp);
+          if (rv) m = umax64(m, abs_bits(rs));
+        }
+      }
+    double mx, dmy;
+    sync_step(m, m, mx, dmy);
+    return mx;
+  };
+
   // ================= recovery sweeps (phi_block.cpp:122-146)
   for (int sweep = 1; sweep < a.s_eff; ++sweep) {
     int kk = 0;
     double d1 = INF, d2 = fnorm, nE = fnorm;  // E = F
     trace(2.0, d2, nE);
-    while (d1 + d2 > a.tol * nE) {
+    double nEl = nE, nEu = nE;
+    bool eexact = true;
+    for (;;) {
+      const double lhs = d1 + d2;
+      bool cont;
+      if (eexact) {
+        cont = lhs > a.tol * nE;
+      } else if (lhs > a.tol * nEu) {
+        cont = true;
+      } else if (lhs <= a.tol * nEl) {
+        cont = false;
+      } else {
+        nE = e_norm_exact();
+        nEl = nEu = nE;
+        eexact = true;
+        cont = lhs > a.tol * nE;
+      }
+      if (!cont) break;
       if (kk >= 300) {
         err = kStRecoveryCap;
         err_idx = 300;
@@ -852,7 +961,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
       ++kk;
       d1 = d2;
       const double fac = a.single_variant ? a.t_single / (double(a.s_eff) * kk) : 0.0;
-      unsigned long long mfb = 0, meb = 0;
+      unsigned long long mfb = 0;
       {
         unsigned c[Q];
         bool v[Q];
@@ -899,7 +1008,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
               const int row = base + rr * LF.gpw + LF.g;
-              double y[Q][V], en[Q][V], ay[Q][V], ae[Q][V];
+              double y[Q][V], en[Q][V], ay[Q][V];
 #pragma unroll
               for (int q = 0; q < Q; ++q) {
 #pragma unroll
@@ -915,7 +1024,6 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
                   y[q][e] = yv;
                   en[q][e] = eo[rr][q][e] + yv;  // E += F (:138)
                   ay[q][e] = vq[rr][q] ? fabs(yv) : 0.0;
-                  ae[q][e] = vq[rr][q] ? fabs(en[q][e]) : 0.0;
                 }
                 if (vq[rr][q]) {
                   const unsigned o = unsigned(row) * ldf + c[q];
@@ -924,23 +1032,26 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
                 }
               }
               const double ry = group_rowsum<Q, V>(ay, LF.G, LF.qp);
-              const double re = group_rowsum<Q, V>(ae, LF.G, LF.qp);
-              if (row < n) {
-                mfb = umax64(mfb, abs_bits(ry));
-                meb = umax64(meb, abs_bits(re));
-              }
+              if (row < n) mfb = umax64(mfb, abs_bits(ry));
             }
                   });
       }
-      double maxF2, maxE;
-      sync_step(mfb, meb, maxF2, maxE);
+      double maxF2, dmy;
+      sync_step(mfb, mfb, maxF2, dmy);
       d2 = maxF2;
       if (!isfinite(d2)) {
         err = kStRecoveryDiverged;
         err_idx = kk;
         break;
       }
-      nE = maxE;
+      nEu = (nEu + d2) * (1.0 + 1e-12);
+      nEl = (nEl - d2) * (1.0 - 1e-12);
+      eexact = false;
+      if (exact_every_term) {
+        nE = e_norm_exact();
+        nEl = nEu = nE;
+        eexact = true;
+      }
       trace(3.0, d2, nE);
       double* tmp = Fc;
       Fc = Fn;
