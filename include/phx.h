@@ -245,6 +245,13 @@ phx_status phx_integrate(phx_op op, double gamma, const double* u0, double h, do
 const char* phx_last_error(void);
 /* Number of device kernels this process has launched through libphx. */
 int64_t phx_kernel_launches(void);
+/* How the last evaluation was launched (diagnostics): 0 one grid-wide
+ * cooperative launch, 1 a partitioned operator's cooperative launches, 2 a
+ * partitioned operator as ONE thread-block cluster with every part's blocks
+ * in shared memory (opt-in: environment PHX_CLUSTER=1, all parts on one
+ * device, 2..16 parts that fit). */
+int32_t phx_last_eval_mode(void);
+
 /* Device-event time (ms) of the last phimv_block evaluation kernel, and the
  * number of grid-wide steps it executed (S terms + promotion + recovery
  * terms + sweep ends). */

@@ -77,6 +77,7 @@ ABI_SYMBOLS = (
     "phx_kernel_launches", "phx_last_eval_stats", "phx_set_trace", "phx_get_trace",
     "phx_adr_csr", "phx_exprk4s6_step", "phx_integrate",
     "phx_mm_read_csr", "phx_mm_write_csr", "phx_op_create_mm", "phx_block_series_direct",
+    "phx_last_eval_mode",
 )
 
 
@@ -137,6 +138,7 @@ def lib():
     L.phx_block_series_direct.argtypes = [C.c_void_p, C.c_int32, dp, dp, C.c_int32, dp,
                                           C.c_int64, C.c_double, dp, C.c_int64, dp, C.c_int64]
     L.phx_last_eval_stats.argtypes = [dp, i64p]
+    L.phx_last_eval_mode.restype = C.c_int32
     L.phx_set_trace.argtypes = [C.c_int64]
     L.phx_get_trace.argtypes = [dp, C.c_int64, i64p]
     _LIB = L
@@ -452,6 +454,12 @@ def phimv(op: CsrOperator, req: PhiRequest) -> PhiResult:
     _check(lib().phx_phimv(op._h, float(req.t), float(req.alpha), V.shape[1] - 1, _d(V), op.n,
                            float(req.tol), C.byref(ss), _d(w), _d(e0), _d(tail), C.byref(rec)))
     return PhiResult(w, e0, tail, _torec(rec, lens))
+
+
+def last_eval_mode() -> int:
+    """0: one grid-wide launch, 1: partitioned cooperative launches,
+    2: partitioned operator as one thread-block cluster (shared-memory blocks)."""
+    return int(lib().phx_last_eval_mode())
 
 
 def last_eval_stats():

@@ -6,13 +6,14 @@ namespace phx {
 
 namespace {
 
-bool select_kernel(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* k) {
-  return eval_kernels_q1v1(QT, V, R, part, dyn, small, k) ||
-         eval_kernels_q1v2a(QT, V, R, part, dyn, small, k) ||
-         eval_kernels_q1v2b(QT, V, R, part, dyn, small, k) ||
-         eval_kernels_q2(QT, V, R, part, dyn, small, k) ||
-         eval_kernels_q4(QT, V, R, part, dyn, small, k) ||
-         eval_kernels_q8(QT, V, R, part, dyn, small, k);
+bool select_kernel(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* k,
+                   bool cluster = false) {
+  return eval_kernels_q1v1(QT, V, R, part, dyn, small, cluster, k) ||
+         eval_kernels_q1v2a(QT, V, R, part, dyn, small, cluster, k) ||
+         eval_kernels_q1v2b(QT, V, R, part, dyn, small, cluster, k) ||
+         eval_kernels_q2(QT, V, R, part, dyn, small, cluster, k) ||
+         eval_kernels_q4(QT, V, R, part, dyn, small, cluster, k) ||
+         eval_kernels_q8(QT, V, R, part, dyn, small, cluster, k);
 }
 
 }  // namespace
@@ -50,6 +51,44 @@ cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStre
   const cudaError_t e = k.occ(block, &per_sm);
   if (e != cudaSuccess) return e;
   return cudaLaunchCooperativeKernel(k.fn, grid, block, args, eval_pipe_bytes(), st);
+}
+
+size_t eval_cluster_smem(int32_t cl_rows, int32_t cl_nnz, int32_t tile, int32_t ldb, int32_t ldf) {
+  const size_t rpad = size_t((cl_rows + tile - 1) / tile) * size_t(tile) + 1;
+  return size_t(cl_rows) * (4 * size_t(ldb) + 3 * size_t(ldf)) * sizeof(double) +
+         size_t(cl_nnz) * (sizeof(double) + sizeof(int)) + rpad * sizeof(int);
+}
+
+// cluster mode: nparts CTAs forming one thread-block cluster (<= 8 portable,
+// <= 16 with the non-portable size), each with its part's blocks in shared
+// memory; no cooperative launch needed (a cluster is co-resident)
+cudaError_t launch_phimv_block_cluster(const BlockArgs& a, int nparts, int block, cudaStream_t st) {
+  EvalKernel k{};
+  if (!eval_kernels_cl(a.QT, a.vec, a.R, a.bsmall != 0, &k)) return cudaErrorInvalidValue;
+  block = eval_cl_block();
+  const size_t smem = eval_cluster_smem(a.cl_rows, a.cl_nnz, a.tile, a.ldb, a.ldf);
+  cudaError_t e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  if (nparts > 8) {
+    e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  BlockArgs copy = a;
+  void* args[] = {&copy};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(nparts), 1, 1);
+  cfg.blockDim = dim3(unsigned(block), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(nparts);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  return cudaLaunchKernelExC(&cfg, k.fn, args);
 }
 
 }  // namespace phx

@@ -75,6 +75,31 @@ struct Vio<2> {
     __stcs(reinterpret_cast<double2*>(p), make_double2(x[0], x[1]));
   }
 };
+// block-stream accesses with the evict-first hints when the blocks are in
+// global memory (H), plain generic accesses in cluster mode (shared memory;
+// the .global cache hints do not apply there)
+template <bool H, int V>
+__device__ __forceinline__ void ld_s(const double* p, double (&x)[V]) {
+  if constexpr (H)
+    Vio<V>::ldcs(p, x);
+  else
+    Vio<V>::ld(p, x);
+}
+template <bool H, int V>
+__device__ __forceinline__ void st_s(double* p, const double (&x)[V]) {
+  if constexpr (H)
+    Vio<V>::stcs(p, x);
+  else
+    Vio<V>::st(p, x);
+}
+template <bool H>
+__device__ __forceinline__ double ld1_s(const double* p) {
+  if constexpr (H)
+    return __ldcs(p);
+  else
+    return *p;
+}
+
 template <int Q, int V, int R_>
 struct Cfg {
   static constexpr int R = R_;  // rows per lane group per warp tile
@@ -279,11 +304,29 @@ __device__ __forceinline__ void pipelined(const BlockArgs& a, Seq& ts, int RW, W
 
 // every warp tile of a phase: the static part, then the dynamic tail from
 // counter ctr (zeroed before the phase's step began)
-template <bool DYN, class Body>
+template <bool DYN, bool CL, class Body>
 __device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, int ntiles,
                                           int warp, int cta, int ncta,
                                           unsigned long long* ctr, WarpPipe& pp, int lane,
+                                          const int* crp, const int* cci, const double* cav,
                                           Body&& body) {
+  if constexpr (CL) {
+    // cluster mode: the part's CSR lives in shared memory for the whole
+    // launch (crp padded to whole tiles); the CTA owns every tile of its part
+    (void)ctr;
+    (void)pp;
+    (void)lane;
+    (void)cta;
+    (void)ncta;
+    for (int t = 0; t < ntiles; ++t)
+      for (int wt = warp; wt < a.tile / L.RW; wt += kWarps) {
+        const int base = t * a.tile + wt * L.RW;
+        if (base >= a.n) break;  // warp-uniform
+        const int* rp = crp + base;
+        const int e0 = rp[0];
+        body(base, rp, cci + e0, cav + e0);
+      }
+  } else {
   const int tst = DYN ? static_tiles(a, ntiles, ncta) : ntiles;
   {
     TileSeq ts;
@@ -307,6 +350,7 @@ __device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, i
     ds.mval = -1;
     if (lane == 0) ds.pend = atomicAdd(ctr, 1ull);
     pipelined(a, ds, L.RW, pp, lane, body);
+  }
   }
 }
 
@@ -393,7 +437,16 @@ __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L,
     gather<Q, V, R, B, false, PART>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
 }
 
-template <int Q, int V, int RR, bool PART, bool DYN, int BO>
+// dynamic shared memory: the per-warp pipes, then (cluster mode) the part's
+// blocks Vw, D0, D1, S (cl_rows x ldb each) and F0, F1, E (cl_rows x ldf)
+constexpr size_t kPipeBytes = (size_t(kWarps) * sizeof(WarpPipe) + 15) / 16 * 16;
+
+// CL (cluster mode, implies PART): the launch is ONE thread-block cluster,
+// one CTA per part; every part's blocks live in its CTA's shared memory, the
+// gathers of other parts' rows read distributed shared memory, and the step
+// sync is a DSMEM max exchange + cluster barrier -- small operators (C1,
+// small integrator grids) whose steps are latency-bound.
+template <int Q, int V, int RR, bool PART, bool DYN, int BO, bool CL>
 __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs ga) {
   constexpr int R = Cfg<Q, V, RR>::R;
   constexpr int B = BO > 0 ? BO : Cfg<Q, V, RR>::B;  // gather batch
@@ -405,6 +458,8 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   // gather tables [D0, D1, S, F0, F1][part] (PART only)
   __shared__ const double* gtab[5][PART ? kMaxParts : 1];
   __shared__ double gmax[2];
+  __shared__ unsigned long long cl_slot[2];                  // CL: this CTA's maxima
+  __shared__ unsigned long long cl_box[2][CL ? kMaxParts : 1][2];  // CL: all parts', by step parity
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpPipe& pp = pipe[warp];
@@ -415,11 +470,14 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   // (unpartitioned: `a` aliases the kernel parameter, read from the constant
   // bank; partitioned: a local copy with the part's fields)
   BlockArgs pa;
+  const int* crp = nullptr;  // cluster mode: the part's CSR in shared memory
+  const int* cci = nullptr;
+  const double* cav = nullptr;
   int my = 0, cta = int(blockIdx.x), ncta = int(gridDim.x);
   const PartTab* T = nullptr;
   if (PART) {
     pa = ga;
-    const int per = int(gridDim.x) / ga.pcount;
+    const int per = CL ? 1 : int(gridDim.x) / ga.pcount;
     my = ga.plo + int(blockIdx.x) / per;
     cta = int(blockIdx.x) % per;
     ncta = per;
@@ -438,13 +496,49 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
     pa.E = T->E;
     pa.W = T->W;
     pa.slots = T->slots;
-    for (int q = threadIdx.x; q < ga.nparts; q += blockDim.x) {
-      const PartTab& U = ga.ptab[q];
-      gtab[0][q] = U.D0;
-      gtab[1][q] = U.D1;
-      gtab[2][q] = U.S;
-      gtab[3][q] = U.F0;
-      gtab[4][q] = U.F1;
+    if (CL) {
+      double* sm = reinterpret_cast<double*>(pipe_smem);  // no pipes in cluster mode
+      const size_t nb = size_t(ga.cl_rows) * size_t(ga.ldb), nf = size_t(ga.cl_rows) * size_t(ga.ldf);
+      pa.Vw = sm;
+      pa.D0 = sm + nb;
+      pa.D1 = sm + 2 * nb;
+      pa.S = sm + 3 * nb;
+      pa.F0 = sm + 4 * nb;
+      pa.F1 = pa.F0 + nf;
+      pa.E = pa.F1 + nf;
+      // the part's CSR: av (8-aligned) then row_ptr (padded to whole tiles) and col_idx
+      double* sav = pa.E + nf;
+      const int rpad = (ga.cl_rows + ga.tile - 1) / ga.tile * ga.tile + 1;
+      int* srp = reinterpret_cast<int*>(sav + ga.cl_nnz);
+      int* sci = srp + rpad;
+      const int nr = T->nrows, nz = T->rp[nr];
+      for (int i = threadIdx.x; i < rpad; i += blockDim.x) srp[i] = T->rp[min(i, nr)];
+      for (int e = threadIdx.x; e < nz; e += blockDim.x) {
+        sci[e] = T->ci[e];
+        sav[e] = T->av[e];
+      }
+      crp = srp;
+      cci = sci;
+      cav = sav;
+      cg::cluster_group cl = cg::this_cluster();
+      for (int q = threadIdx.x; q < ga.nparts; q += blockDim.x) {
+        gtab[0][q] = cl.map_shared_rank(pa.D0, q);
+        gtab[1][q] = cl.map_shared_rank(pa.D1, q);
+        gtab[2][q] = cl.map_shared_rank(pa.S, q);
+        gtab[3][q] = cl.map_shared_rank(pa.F0, q);
+        gtab[4][q] = cl.map_shared_rank(pa.F1, q);
+      }
+      if (threadIdx.x == 0) cl_slot[0] = cl_slot[1] = 0ull;
+      cl.sync();  // every CTA of the cluster is running before any DSMEM access
+    } else {
+      for (int q = threadIdx.x; q < ga.nparts; q += blockDim.x) {
+        const PartTab& U = ga.ptab[q];
+        gtab[0][q] = U.D0;
+        gtab[1][q] = U.D1;
+        gtab[2][q] = U.S;
+        gtab[3][q] = U.F0;
+        gtab[4][q] = U.F1;
+      }
     }
     __syncthreads();
   }
@@ -483,6 +577,33 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
         asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
         a.tstamp[q] = (ns & ((1ull << 48) - 1ull)) | (static_cast<unsigned long long>(sm) << 48);
       }
+    }
+    if (CL) {
+      // CTA maxima -> every part's box (DSMEM), cluster barrier, max of the boxes
+      publish2(ma, mb, cl_slot, red);
+      __syncthreads();
+      cg::cluster_group cl = cg::this_cluster();
+      if (int(threadIdx.x) < ga.nparts) {
+        unsigned long long* box = cl.map_shared_rank(&cl_box[step & 1][my][0], int(threadIdx.x));
+        box[0] = cl_slot[0];
+        box[1] = cl_slot[1];
+      }
+      cl.sync();
+      if (threadIdx.x == 0) {
+        unsigned long long A = 0, Bv = 0;
+        for (int q = 0; q < ga.nparts; ++q) {
+          A = umax64(A, cl_box[step & 1][q][0]);
+          Bv = umax64(Bv, cl_box[step & 1][q][1]);
+        }
+        gmax[0] = from_bits(A);
+        gmax[1] = from_bits(Bv);
+        cl_slot[0] = cl_slot[1] = 0ull;
+      }
+      __syncthreads();
+      ra = gmax[0];
+      rb = gmax[1];
+      ++step;
+      return;
     }
     publish2(ma, mb, slot, red);
     if (!PART) {
@@ -555,6 +676,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
       a.status[4] = step + extra_steps;
       a.status[5] = min(tr_len, a.trace_cap);
     }
+    if (CL) cg::this_cluster().sync();  // peers may still read this CTA's blocks
   };
   // lane column offsets (first column of each chunk) and chunk validity
   auto cols = [&](const Layout& L, unsigned (&c)[Q], bool (&v)[Q]) {
@@ -706,7 +828,8 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
           ka[q][e] = v[q] ? __ldg(a.colKa + cc) : 0.0;
           tos[q][e] = v[q] ? __ldg(a.colTos + cc) : 0.0;
         }
-      run_tiles<DYN>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+      run_tiles<DYN, CL>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+                         crp, cci, cav,
                 [&](int base, const int* rp, const int* ci, const double* avs) {
           // row-local streams (independent of the CSR slice): before or after
           // the gather (Cfg::LATE)
@@ -731,15 +854,15 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
                 vw[rr][q][e] = vwl[rr][q][e] = so[rr][q][e] = ds[rr][q][e] = 0.0;
               }
               if (vq[rr][q]) {
-                Vio<V>::ldcs(a.Vw + o, vw[rr][q]);
-                Vio<V>::ldcs(a.S + o, so[rr][q]);
+                ld_s<!CL>(a.Vw + o, vw[rr][q]);
+                ld_s<!CL>(a.S + o, so[rr][q]);
                 if (has_xi) Vio<V>::ld(Dc + o, ds[rr][q]);
                 if (vwl_vec) {
-                  if (jj[q][0] >= 2) Vio<V>::ldcs(a.Vw + (o - unsigned(r)), vwl[rr][q]);
+                  if (jj[q][0] >= 2) ld_s<!CL>(a.Vw + (o - unsigned(r)), vwl[rr][q]);
                 } else {
 #pragma unroll
                   for (int e = 0; e < V; ++e)
-                    if (jj[q][e] >= 2) vwl[rr][q][e] = __ldcs(a.Vw + (o + e - unsigned(r)));
+                    if (jj[q][e] >= 2) vwl[rr][q][e] = ld1_s<!CL>(a.Vw + (o + e - unsigned(r)));
                 }
               }
             }
@@ -776,9 +899,9 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
             for (int q = 0; q < Q; ++q) {
               if (vq[rr][q]) {
                 const unsigned o = unsigned(row) * ldb + c[q];
-                Vio<V>::stcs(a.Vw + o, vn[rr][q]);
+                st_s<!CL>(a.Vw + o, vn[rr][q]);
                 Vio<V>::st(Dn + o, dn[rr][q]);
-                Vio<V>::stcs(a.S + o, sn[rr][q]);
+                st_s<!CL>(a.S + o, sn[rr][q]);
               }
 #pragma unroll
               for (int e = 0; e < V; ++e) ad[q][e] = vq[rr][q] ? fabs(dn[rr][q][e]) : 0.0;
@@ -828,7 +951,8 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
     cols(LF, c, v);
 #pragma unroll
     for (int q = 0; q < Q; ++q) vl[q] = v[q] && int(c[q]) < r;
-    run_tiles<DYN>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+    run_tiles<DYN, CL>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+                       crp, cci, cav,
               [&](int base, const int* rp, const int* ci, const double* avs) {
         double acc[R][Q][V];
 #pragma unroll
@@ -975,7 +1099,8 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
             const int i = cc < r ? cc : cc - r;
             tosF[q][e] = v[q] ? __ldg(a.colTos + i) : 0.0;
           }
-        run_tiles<DYN>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+        run_tiles<DYN, CL>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+                       crp, cci, cav,
                   [&](int base, const int* rp, const int* ci, const double* avs) {
             double eo[R][Q][V], fs[R][Q][V], acc[R][Q][V];
             bool vq[R][Q];
@@ -996,7 +1121,7 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
 #pragma unroll
                   for (int e = 0; e < V; ++e) eo[rr][q][e] = fs[rr][q][e] = 0.0;
                   if (vq[rr][q]) {
-                    Vio<V>::ldcs(a.E + o, eo[rr][q]);
+                    ld_s<!CL>(a.E + o, eo[rr][q]);
                     if (has_xi) Vio<V>::ld(Fc + o, fs[rr][q]);
                   }
                 }
@@ -1027,8 +1152,8 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
                 }
                 if (vq[rr][q]) {
                   const unsigned o = unsigned(row) * ldf + c[q];
-                  Vio<V>::stcs(Fn + o, y[q]);  // next term only: evict-first
-                  Vio<V>::stcs(a.E + o, en[q]);
+                  st_s<!CL>(Fn + o, y[q]);  // next term only: evict-first
+                  st_s<!CL>(a.E + o, en[q]);
                 }
               }
               const double ry = group_rowsum<Q, V>(ay, LF.G, LF.qp);
@@ -1167,22 +1292,29 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   finish(err, err_idx, L_S, 0);
 }
 
-constexpr size_t kPipeBytes = size_t(kWarps) * sizeof(WarpPipe);  // dynamic smem per CTA
-
-template <int Q, int V, int R, bool PART, bool DYN, int BO>
+template <int Q, int V, int R, bool PART, bool DYN, int BO, bool CL>
 cudaError_t eval_occupancy(int block, int* per_sm) {
-  const cudaError_t e = cudaFuncSetAttribute(k_phimv_block<Q, V, R, PART, DYN, BO>,
+  const cudaError_t e = cudaFuncSetAttribute(k_phimv_block<Q, V, R, PART, DYN, BO, CL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(kPipeBytes));
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      per_sm, k_phimv_block<Q, V, R, PART, DYN, BO>, block, kPipeBytes);
+      per_sm, k_phimv_block<Q, V, R, PART, DYN, BO, CL>, block, kPipeBytes);
 }
 
-template <int Q, int V, int R, bool PART, bool DYN, int BO = 0>
+template <int Q, int V, int R, bool PART, bool DYN, int BO = 0, bool CL = false>
 EvalKernel eval_kernel() {
-  return EvalKernel{reinterpret_cast<const void*>(k_phimv_block<Q, V, R, PART, DYN, BO>),
-                    eval_occupancy<Q, V, R, PART, DYN, BO>};
+  return EvalKernel{reinterpret_cast<const void*>(k_phimv_block<Q, V, R, PART, DYN, BO, CL>),
+                    eval_occupancy<Q, V, R, PART, DYN, BO, CL>};
+}
+
+// cluster-mode variants exist for single-chunk rows (Q == 1) only
+template <int Q, int V, int R, int BO>
+EvalKernel eval_kernel_cluster() {
+  if constexpr (Q == 1)
+    return eval_kernel<Q, V, R, true, false, BO, true>();
+  else
+    return EvalKernel{nullptr, nullptr};
 }
 
 }  // namespace
@@ -1191,7 +1323,9 @@ EvalKernel eval_kernel() {
 // static or dynamic-tail kernels, partitioned kernels always with the
 // dynamic tail
 #define PHX_EVAL_KERNELS(q, v, r, bo)                          \
-  if (part)                                                    \
+  if (cluster)                                                 \
+    return false; /* cluster variants: phx_eval_cl.cu */       \
+  else if (part)                                               \
     *out = eval_kernel<q, v, r, true, true, bo>();             \
   else if (dyn)                                                \
     *out = eval_kernel<q, v, r, false, true, bo>();            \
@@ -1200,7 +1334,7 @@ EvalKernel eval_kernel() {
 #define PHX_EVAL_CASE(q, v, r)                                 \
   if (QT == q && V == v && R == r) {                           \
     PHX_EVAL_KERNELS(q, v, r, 0)                               \
-    return true;                                               \
+    return out->fn != nullptr;                                 \
   }
 // ... and a second, short batch bs used for operators whose rows fit it
 #define PHX_EVAL_CASE2(q, v, r, bs)                            \
@@ -1210,7 +1344,7 @@ EvalKernel eval_kernel() {
     } else {                                                   \
       PHX_EVAL_KERNELS(q, v, r, 0)                             \
     }                                                          \
-    return true;                                               \
+    return out->fn != nullptr;                                 \
   }
 
 }  // namespace phx

@@ -4,8 +4,9 @@
 
 namespace phx {
 
-bool eval_kernels_q1v2a(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out) {
+bool eval_kernels_q1v2a(int QT, int V, int R, bool part, bool dyn, bool small, bool cluster, EvalKernel* out) {
   (void)small;
+  (void)cluster;
   PHX_EVAL_CASE2(1, 2, 1, 5)
   return false;
 }

@@ -4,8 +4,9 @@
 
 namespace phx {
 
-bool eval_kernels_q4(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out) {
+bool eval_kernels_q4(int QT, int V, int R, bool part, bool dyn, bool small, bool cluster, EvalKernel* out) {
   (void)small;
+  (void)cluster;
   PHX_EVAL_CASE(4, 1, 1)
   PHX_EVAL_CASE(4, 2, 1)
   return false;

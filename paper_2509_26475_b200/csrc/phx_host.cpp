@@ -132,6 +132,7 @@ std::vector<double> g_trace;
 int64_t g_trace_len = 0;
 double g_last_ms = 0.0;
 int64_t g_last_steps = 0;
+int32_t g_last_mode = 0;  // 0 grid-wide launch, 1 partitioned cooperative, 2 cluster
 
 // One row part of a partitioned operator, resident on `dev`.
 struct PartDev {
@@ -671,6 +672,31 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     PHX_CUDA(cudaStreamSynchronize(op->parts[size_t(q)].stream));
   }
   const int block = phx::eval_block_size();
+  // cluster mode: all parts on one device as ONE thread-block cluster, each
+  // part's blocks in its CTA's shared memory (DSMEM gathers, cluster barrier)
+  // -- when 2..16 parts of single-chunk rows fit and PHX_CLUSTER=1
+  int64_t max_rows = 0, max_nnz = 0;
+  for (int q = 0; q < P; ++q) {
+    max_rows = std::max<int64_t>(max_rows, op->parts[size_t(q)].nrows);
+    max_nnz = std::max<int64_t>(max_nnz, op->parts[size_t(q)].nnz);
+  }
+  bool cluster = false;
+  // the cluster kernels' CTA has eval_cl_block()/32 warps: their CTA tile
+  const int32_t cl_tile = base.tile / (block / 32) * (phx::eval_cl_block() / 32);
+  {
+    // opt-in (PHX_CLUSTER=1): measured no faster than the cooperative launch
+    // on the small operators it fits (C1: 4.8 vs 4.5 us per step)
+    const char* env = std::getenv("PHX_CLUSTER");
+    const bool enabled = env && env[0] == '1';
+    int optin = 0;
+    DeviceGuard guard(op->parts[0].dev);
+    PHX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                    op->parts[0].dev));
+    cluster = enabled && groups.size() == 1 && P >= 2 && P <= 16 && base.QT == 1 &&
+              max_nnz < (int64_t(1) << 24) &&
+              phx::eval_cluster_smem(int32_t(max_rows), int32_t(max_nnz), cl_tile, ldb, ldf) <=
+                  size_t(optin);
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const Group& g = groups[gi];
@@ -696,6 +722,21 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     a.trace = (g.plo == 0 && trace_cap > 0) ? d.trace.as<double>(size_t(trace_cap)) : nullptr;
     a.trace_cap = int32_t(trace_cap);
     PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), d.stream));
+    if (cluster) {
+      a.cl_rows = int32_t(max_rows);
+      a.cl_nnz = int32_t(max_nnz);
+      a.tile = cl_tile;
+      PHX_CUDA(cudaEventCreate(&e0));
+      PHX_CUDA(cudaEventCreate(&e1));
+      PHX_CUDA(cudaEventRecord(e0, d.stream));
+      PHX_CUDA(phx::launch_phimv_block_cluster(a, P, block, d.stream));
+      PHX_CUDA(cudaEventRecord(e1, d.stream));
+      {
+        std::lock_guard<std::mutex> lk(g_trace_mu);
+        g_last_mode = 2;
+      }
+      continue;
+    }
     int max_blocks = 0;
     PHX_CUDA(phx::coop_grid_size(a.QT, a.vec, a.R, true, true, a.bsmall != 0, block, &max_blocks));
     int64_t most = 1;
@@ -709,6 +750,10 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     }
     PHX_CUDA(phx::launch_phimv_block(a, per * g.pcount, block, d.stream));
     if (gi == 0) PHX_CUDA(cudaEventRecord(e1, d.stream));
+    {
+      std::lock_guard<std::mutex> lk(g_trace_mu);
+      g_last_mode = 1;
+    }
   }
   // collect: status / sweep lengths / trace from part 0's launch, W slices
   for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -986,6 +1031,10 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(cap, ntiles)));
   PHX_CUDA(cudaEventRecord(op->ev0, st));
   PHX_CUDA(phx::launch_phimv_block(a, grid, block, st));
+  {
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    g_last_mode = 0;
+  }
   PHX_CUDA(cudaEventRecord(op->ev1, st));
   if (step_times) {
     std::vector<unsigned long long> ts(size_t(a.tstamp_cap));
@@ -1775,6 +1824,11 @@ phx_status phx_block_series_direct(phx_op op, int32_t r, const double* t, const 
                                  cudaMemcpyDeviceToHost, st));
     PHX_CUDA(cudaStreamSynchronize(st));
   });
+}
+
+int32_t phx_last_eval_mode(void) {
+  std::lock_guard<std::mutex> lk(g_trace_mu);
+  return g_last_mode;
 }
 
 phx_status phx_last_eval_stats(double* kernel_ms, int64_t* steps) {

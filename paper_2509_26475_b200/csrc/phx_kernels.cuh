@@ -61,6 +61,8 @@ struct BlockArgs {
   int32_t tile;    // rows per tile (row -> CTA mapping, independent of layout)
   int32_t dyn;          // 1: dynamic-tail kernel (always for partitioned runs)
   int32_t bsmall;       // 1: the short-gather-batch variant (rows fit it)
+  int32_t cl_rows;      // cluster mode: rows per part allocated in shared memory
+  int32_t cl_nnz;       // cluster mode: CSR entries per part allocated in shared memory
   double static_frac;  // DYN kernels: share of a phase's CTA tiles assigned statically
   // scalars
   double xi, tol;
@@ -120,6 +122,11 @@ enum : int32_t {
 // launch wrappers (phx_kernels.cu)
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st);
 int eval_block_size();     // threads per CTA of k_phimv_block
+// cluster mode (one thread-block cluster, one CTA per part, blocks in shared
+// memory): dynamic shared memory per CTA, and the launch (nparts CTAs)
+size_t eval_cluster_smem(int32_t cl_rows, int32_t cl_nnz, int32_t tile, int32_t ldb, int32_t ldf);
+
+cudaError_t launch_phimv_block_cluster(const BlockArgs& a, int nparts, int block, cudaStream_t st);
 size_t eval_pipe_bytes();  // its dynamic shared memory per CTA
 cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, bool small, int block,
                            int* max_blocks);
@@ -131,12 +138,15 @@ struct EvalKernel {
 };
 // per-file variant tables (phx_eval_q*.cu): true when the file holds the
 // variant (QT, V, R, partitioned, dynamic tail, short gather batch)
-bool eval_kernels_q1v1(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
-bool eval_kernels_q1v2a(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
-bool eval_kernels_q1v2b(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
-bool eval_kernels_q2(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
-bool eval_kernels_q4(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
-bool eval_kernels_q8(int QT, int V, int R, bool part, bool dyn, bool small, EvalKernel* out);
+bool eval_kernels_q1v1(int QT, int V, int R, bool part, bool dyn, bool small, bool cluster, EvalKernel* out);
+bool eval_kernels_q1v2a(int QT, int V, int R, bool part, bool dyn, bool small, bool cluster, EvalKernel* out);
+bool eval_kernels_q1v2b(int QT, int V, int R, bool part, bool dyn, bool small, bool cluster, EvalKernel* out);
+bool eval_kernels_q2(int QT, int V, int R, bool part, bool dyn, bool small, bool cluster, EvalKernel* out);
+bool eval_kernels_q4(int QT, int V, int R, bool part, bool dyn, bool small, bool cluster, EvalKernel* out);
+bool eval_kernels_q8(int QT, int V, int R, bool part, bool dyn, bool small, bool cluster, EvalKernel* out);
+// the cluster variants (phx_eval_cl.cu) and their CTA size
+bool eval_kernels_cl(int QT, int V, int R, bool small, EvalKernel* out);
+int eval_cl_block();
 
 // y = f(A x) with mode 0: A x, 1: A x - fl(xi x), 2: (A x) / div ; fused
 // per-chunk max|y| into chunkmax (bit patterns) when chunkmax != nullptr

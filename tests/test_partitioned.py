@@ -43,6 +43,34 @@ def test_partitioned_bitwise(cfg, size, parts):
     assert np.array_equal(tr, otr)
 
 
+@pytest.mark.parametrize("cfg,size,parts", [(1, 0, 8), (1, 0, 16), (2, 24, 8), (3, 8, 8),
+                                            (4, 512, 16), (5, 1000, 16), (1, 300, 3)])
+def test_cluster_mode_bitwise(cfg, size, parts, monkeypatch):
+    """Parts on one device that fit in shared memory run as ONE thread-block
+    cluster (opt-in PHX_CLUSTER=1: DSMEM gathers, cluster barrier): bitwise the
+    unpartitioned run, term by term."""
+    monkeypatch.setenv("PHX_CLUSTER", "1")
+    p = P()
+    wl = p.workload(cfg, size)
+    whole = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    ss = p.select_parameters(whole, 61, wl.tol)
+    ref = p.phimv_block(whole, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    part = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=parts)
+    res = p.phimv_block(part, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    assert p.last_eval_mode() == 2
+    assert res.stats.series_len_S == ref.stats.series_len_S
+    assert res.stats.series_lens_F == ref.stats.series_lens_F
+    assert np.array_equal(res.W, ref.W)
+    p.set_trace(3 * 100000)
+    p.phimv_block(part, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    tr = p.get_trace(3 * 100000)
+    p.set_trace(0)
+    oop = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    _, _, otr = O.phimv_block(oop, wl.t, wl.alpha, wl.V, wl.tol, O.ScalingShift(*ss.astuple()),
+                              trace=True)
+    assert np.array_equal(tr, otr)
+
+
 def test_partitioned_full_c2_bitwise():
     p = P()
     wl = p.workload(2, 0)
