@@ -19,7 +19,7 @@ bool select_kernel(int QT, int V, int R, bool part, bool dyn, bool small, EvalKe
 }  // namespace
 
 cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, bool small, int block,
-                           int* max_blocks) {
+                           int* max_blocks, bool lat) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -27,7 +27,8 @@ cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, bool small
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
   EvalKernel k{};
-  if (!select_kernel(QT, V, R, part, dyn, small, &k)) return cudaErrorInvalidValue;
+  if (lat ? !eval_kernels_lat(QT, V, R, small, &k) : !select_kernel(QT, V, R, part, dyn, small, &k))
+    return cudaErrorInvalidValue;
   int per_sm = 0;
   e = k.occ(block, &per_sm);
   if (e != cudaSuccess) return e;
@@ -44,7 +45,8 @@ cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStre
   BlockArgs copy = a;
   void* args[] = {&copy};
   EvalKernel k{};
-  if (!select_kernel(a.QT, a.vec, a.R, a.nparts > 1, a.dyn != 0, a.bsmall != 0, &k))
+  if (a.lat ? !eval_kernels_lat(a.QT, a.vec, a.R, a.bsmall != 0, &k)
+            : !select_kernel(a.QT, a.vec, a.R, a.nparts > 1, a.dyn != 0, a.bsmall != 0, &k))
     return cudaErrorInvalidValue;
   count_launch();
   int per_sm = 0;  // also sets the dynamic shared memory attribute of the variant

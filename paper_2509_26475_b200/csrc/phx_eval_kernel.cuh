@@ -446,8 +446,11 @@ constexpr size_t kPipeBytes = (size_t(kWarps) * sizeof(WarpPipe) + 15) / 16 * 16
 // gathers of other parts' rows read distributed shared memory, and the step
 // sync is a DSMEM max exchange + cluster barrier -- small operators (C1,
 // small integrator grids) whose steps are latency-bound.
-template <int Q, int V, int RR, bool PART, bool DYN, int BO, bool CL>
-__global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs ga) {
+// LAT (latency mode): compiled for ONE CTA per SM (register budget 255) --
+// for operators with fewer tiles than SMs, whose steps are latency-bound:
+// the gather's loads batch instead of serialising at 64 registers
+template <int Q, int V, int RR, bool PART, bool DYN, int BO, bool CL, bool LAT = false>
+__global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs ga) {
   constexpr int R = Cfg<Q, V, RR>::R;
   constexpr int B = BO > 0 ? BO : Cfg<Q, V, RR>::B;  // gather batch
   cg::grid_group grid = cg::this_grid();
@@ -1292,20 +1295,21 @@ __global__ void __launch_bounds__(kBlock, Cfg<Q, V, RR>::MINB) k_phimv_block(Blo
   finish(err, err_idx, L_S, 0);
 }
 
-template <int Q, int V, int R, bool PART, bool DYN, int BO, bool CL>
+template <int Q, int V, int R, bool PART, bool DYN, int BO, bool CL, bool LAT>
 cudaError_t eval_occupancy(int block, int* per_sm) {
-  const cudaError_t e = cudaFuncSetAttribute(k_phimv_block<Q, V, R, PART, DYN, BO, CL>,
+  const cudaError_t e = cudaFuncSetAttribute(k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(kPipeBytes));
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      per_sm, k_phimv_block<Q, V, R, PART, DYN, BO, CL>, block, kPipeBytes);
+      per_sm, k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>, block, kPipeBytes);
 }
 
-template <int Q, int V, int R, bool PART, bool DYN, int BO = 0, bool CL = false>
+template <int Q, int V, int R, bool PART, bool DYN, int BO = 0, bool CL = false, bool LAT = false>
 EvalKernel eval_kernel() {
-  return EvalKernel{reinterpret_cast<const void*>(k_phimv_block<Q, V, R, PART, DYN, BO, CL>),
-                    eval_occupancy<Q, V, R, PART, DYN, BO, CL>};
+  return EvalKernel{
+      reinterpret_cast<const void*>(k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>),
+      eval_occupancy<Q, V, R, PART, DYN, BO, CL, LAT>};
 }
 
 // cluster-mode variants exist for single-chunk rows (Q == 1) only

@@ -1013,11 +1013,23 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   int max_blocks = 0;
   a.bsmall = short_batch(op, QT, V, R) ? 1 : 0;
   PHX_CUDA(phx::coop_grid_size(QT, V, R, false, false, a.bsmall != 0, block, &max_blocks));
+  {
+    // latency mode: fewer tiles than SMs -> the one-CTA-per-SM variant (its
+    // gathers batch); PHX_LAT=0 disables it
+    int sms = 0;
+    PHX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, op->device));
+    const char* env = std::getenv("PHX_LAT");
+    const int64_t nt = (n + tile - 1) / tile;
+    a.lat = (QT == 1 && nt < sms && !(env && env[0] == '0')) ? 1 : 0;
+    if (a.lat)
+      PHX_CUDA(phx::coop_grid_size(QT, V, R, false, false, a.bsmall != 0, block, &max_blocks,
+                                   true));
+  }
   const int64_t ntiles = (n + tile - 1) / tile;
   // the dynamic-tail kernel when the CTAs get many tiles each: per-CTA speed
   // differs by up to ~20% on long steps; on short ones the tail grabs and the
   // larger kernel cost more than they balance
-  a.dyn = ntiles >= int64_t(kDynTilesPerCta) * max_blocks ? 1 : 0;
+  a.dyn = !a.lat && ntiles >= int64_t(kDynTilesPerCta) * max_blocks ? 1 : 0;
   if (a.dyn)
     PHX_CUDA(phx::coop_grid_size(QT, V, R, false, true, a.bsmall != 0, block, &max_blocks));
   // developer knob for tuning studies: PHX_GRID_FRAC = fraction (0, 1] of the

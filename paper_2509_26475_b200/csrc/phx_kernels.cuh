@@ -61,6 +61,7 @@ struct BlockArgs {
   int32_t tile;    // rows per tile (row -> CTA mapping, independent of layout)
   int32_t dyn;          // 1: dynamic-tail kernel (always for partitioned runs)
   int32_t bsmall;       // 1: the short-gather-batch variant (rows fit it)
+  int32_t lat;          // 1: the latency-mode variant (fewer tiles than SMs)
   int32_t cl_rows;      // cluster mode: rows per part allocated in shared memory
   int32_t cl_nnz;       // cluster mode: CSR entries per part allocated in shared memory
   double static_frac;  // DYN kernels: share of a phase's CTA tiles assigned statically
@@ -129,7 +130,7 @@ size_t eval_cluster_smem(int32_t cl_rows, int32_t cl_nnz, int32_t tile, int32_t 
 cudaError_t launch_phimv_block_cluster(const BlockArgs& a, int nparts, int block, cudaStream_t st);
 size_t eval_pipe_bytes();  // its dynamic shared memory per CTA
 cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, bool small, int block,
-                           int* max_blocks);
+                           int* max_blocks, bool lat = false);
 
 // one instantiated kernel variant and its occupancy query
 struct EvalKernel {
@@ -146,6 +147,8 @@ bool eval_kernels_q4(int QT, int V, int R, bool part, bool dyn, bool small, bool
 bool eval_kernels_q8(int QT, int V, int R, bool part, bool dyn, bool small, bool cluster, EvalKernel* out);
 // the cluster variants (phx_eval_cl.cu) and their CTA size
 bool eval_kernels_cl(int QT, int V, int R, bool small, EvalKernel* out);
+// latency-mode variants (phx_eval_lat.cu): unpartitioned, static, 1 CTA/SM
+bool eval_kernels_lat(int QT, int V, int R, bool small, EvalKernel* out);
 int eval_cl_block();
 
 // y = f(A x) with mode 0: A x, 1: A x - fl(xi x), 2: (A x) / div ; fused
