@@ -698,6 +698,12 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
                   size_t(optin);
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  struct EvGuard {  // the timing events are released on every exit path
+    cudaEvent_t& e;
+    ~EvGuard() {
+      if (e) cudaEventDestroy(e);
+    }
+  } g0{e0}, g1{e1};
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const Group& g = groups[gi];
     PartDev& d = op->parts[size_t(g.plo)];
@@ -780,8 +786,6 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
         PHX_CUDA(cudaMemcpy(g_trace.data(), d0.trace.p, size_t(trace_cap) * 8, cudaMemcpyDeviceToHost));
       }
       PHX_CUDA(cudaEventElapsedTime(ms_out, e0, e1));
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
     } else if (st[0] != h_status[0] || st[2] != h_status[2]) {
       throw_phx(PHX_ECUDA, "partitioned evaluation: parts disagree on the stopping decisions");
     }
