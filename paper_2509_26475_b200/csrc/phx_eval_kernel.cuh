@@ -363,6 +363,28 @@ __device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, i
 constexpr unsigned kOwnerShift = 27;
 constexpr unsigned kLocalMask = (1u << kOwnerShift) - 1u;
 
+// gather loads carry an L2 cache policy: evict_last for the fraction
+// a.gather_keep of lines -- 1 for operators whose gather reuse distance is
+// far but fits in L2 (C3: the z +- 1 planes 65,536 rows apart, while the
+// accumulator streams pass through evict-first), else 0 (default priority)
+template <int V>
+__device__ __forceinline__ void ld_gather(const double* p, double (&x)[V], unsigned long long pol) {
+  if constexpr (V == 2) {
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(x[0]), "=d"(x[1])
+                 : "l"(p), "l"(pol));
+  } else {
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(x[0]) : "l"(p), "l"(pol));
+  }
+}
+__device__ __forceinline__ unsigned long long gather_policy(float keep) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;"
+               : "=l"(pol)
+               : "f"(keep));
+  return pol;
+}
+
 template <bool PART>
 __device__ __forceinline__ const double* gather_row_ptr(const double* X,
                                                         const double* const* Xt, unsigned enc,
@@ -371,7 +393,7 @@ __device__ __forceinline__ const double* gather_row_ptr(const double* X,
   return X + enc * ld;
 }
 
-template <int Q, int V, int R, int B, bool SMEM, bool PART>
+template <int Q, int V, int R, int B, bool SMEM, bool PART, bool HINT>
 __device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const double* av_s,
                                        int e_lo, unsigned ld, const int (&rs)[R],
                                        const int (&cnt)[R], const double* X,
@@ -380,6 +402,8 @@ __device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const 
   int maxc = 0;
 #pragma unroll
   for (int rr = 0; rr < R; ++rr) maxc = max(maxc, cnt[rr]);
+  unsigned long long pol = 0;
+  if constexpr (HINT) pol = gather_policy(a.gather_keep);
   for (int u0 = 0; u0 < maxc; u0 += B) {
     double xv[B][R][Q][V];
 #pragma unroll
@@ -395,7 +419,10 @@ __device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const 
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           if (ok && vq[q]) {
-            Vio<V>::ld(xr + cq[q], xv[u][rr][q]);
+            if constexpr (HINT)
+              ld_gather<V>(xr + cq[q], xv[u][rr][q], pol);
+            else
+              Vio<V>::ld(xr + cq[q], xv[u][rr][q]);
           } else {
 #pragma unroll
             for (int e = 0; e < V; ++e) xv[u][rr][q][e] = 0.0;
@@ -417,7 +444,7 @@ __device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const 
   }
 }
 
-template <int Q, int V, int R, int B, bool PART>
+template <int Q, int V, int R, int B, bool PART, bool HINT = false>
 __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L, const int* rp,
                                             const int* ci, const double* av, unsigned ld,
                                             const double* X, const double* const* Xt,
@@ -432,9 +459,9 @@ __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L,
     cnt[rr] = rp[li + 1] - rp[li];
   }
   if (rp[L.RW] - e_lo <= kEC)
-    gather<Q, V, R, B, true, PART>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
+    gather<Q, V, R, B, true, PART, HINT>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
   else
-    gather<Q, V, R, B, false, PART>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
+    gather<Q, V, R, B, false, PART, HINT>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
 }
 
 // dynamic shared memory: the per-warp pipes, then (cluster mode) the part's
@@ -453,6 +480,11 @@ template <int Q, int V, int RR, bool PART, bool DYN, int BO, bool CL, bool LAT =
 __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs ga) {
   constexpr int R = Cfg<Q, V, RR>::R;
   constexpr int B = BO > 0 ? BO : Cfg<Q, V, RR>::B;  // gather batch
+  // L2 cache-policy gathers (a.gather_keep): the dynamic-tail (1, 2, 1)
+  // default-batch variant only -- large operators with long rows (C3); the
+  // hinted load form costs the short-row kernels (C2, C5) even at fraction 0,
+  // and cluster mode gathers shared memory
+  constexpr bool HINT = !CL && DYN && BO == 0 && Q == 1 && V == 2 && RR == 1;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long red[2][kWarps];
   // per-warp pipeline buffers: dynamic shared memory (kWarps * sizeof(WarpPipe))
@@ -872,7 +904,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
           }
           };
           if constexpr (!Cfg<Q, V, RR>::LATE) streams();
-          gather_tile<Q, V, R, B, PART>(a, LS, rp, ci, avs, ldb, Dc, gtab[dpar], c, v, acc);
+          gather_tile<Q, V, R, B, PART, HINT>(a, LS, rp, ci, avs, ldb, Dc, gtab[dpar], c, v, acc);
           if constexpr (Cfg<Q, V, RR>::LATE) streams();
           double vn[R][Q][V], dn[R][Q][V], sn[R][Q][V];
 #pragma unroll
@@ -967,7 +999,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
         // gathers S block-0 columns (left F columns live at the same column
         // index in S); a pair straddling the left/right split gathers one
         // extra column, unused
-        gather_tile<Q, V, R, B, PART>(a, LF, rp, ci, avs, ldb, a.S, gtab[2], c, vl, acc);
+        gather_tile<Q, V, R, B, PART, HINT>(a, LF, rp, ci, avs, ldb, a.S, gtab[2], c, vl, acc);
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
           const int row = base + rr * LF.gpw + LF.g;
@@ -1131,7 +1163,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
               }
             };
             if constexpr (!Cfg<Q, V, RR>::LATE) streams();
-            gather_tile<Q, V, R, B, PART>(a, LF, rp, ci, avs, ldf, Fc, gtab[3 + fpar], c, v, acc);
+            gather_tile<Q, V, R, B, PART, HINT>(a, LF, rp, ci, avs, ldf, Fc, gtab[3 + fpar], c, v, acc);
             if constexpr (Cfg<Q, V, RR>::LATE) streams();
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {

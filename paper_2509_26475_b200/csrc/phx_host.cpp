@@ -153,6 +153,7 @@ struct phx_op_s {
   int device = 0;
   int64_t n = 0, nnz = 0;
   double frac_le2 = 0.0, frac_le5 = 0.0;  // share of rows with <= 2 / <= 5 entries
+  int64_t bandwidth = 0;                   // max |col - row| over the entries
   int32_t* d_rp = nullptr;
   int32_t* d_ci = nullptr;
   double* d_av = nullptr;
@@ -186,7 +187,22 @@ constexpr int kDynTilesPerCta = 64;
 // come with a short batch (5, 2 entries) used when >= 99% of the rows fit it
 // (a longer row just takes a second batch); it issues no predicated-off
 // slots on short-row operators (C2 6.12 -> 5.75 ms, C5 -3.7%).
-void row_length_stats(phx_op op, const int64_t* row_ptr) {
+// Gather reuse distance: the operator's bandwidth max |col - row|.  A block
+// row is gathered by tiles up to `bandwidth` rows apart; when that window
+// (both sides, in block bytes) is far larger than what round-robin tiles
+// keep warm yet fits in the L2 next to the streams, the gather loads mark
+// their lines evict_last (C3: 2 x 65,536 rows x 240 B = 31 MB).
+float gather_keep(phx_op op, int64_t row_bytes) {
+  const double window = 2.0 * double(op->bandwidth) * double(row_bytes);
+  return (window >= 8e6 && window <= 96e6) ? 1.0f : 0.0f;
+}
+
+void row_length_stats(phx_op op, const int64_t* row_ptr, const int32_t* col_idx) {
+  int64_t bw = 0;  // every entry (columns need not be sorted)
+  for (int64_t i = 0; i < op->n; ++i)
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+      bw = std::max<int64_t>(bw, std::abs(int64_t(col_idx[e]) - i));
+  op->bandwidth = bw;
   int64_t le2 = 0, le5 = 0;
   for (int64_t i = 0; i < op->n; ++i) {
     const int64_t c = row_ptr[i + 1] - row_ptr[i];
@@ -923,6 +939,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
     b.R = R;
     b.tile = tile;
     b.static_frac = static_frac;
+    b.gather_keep = gather_keep(op, int64_t(w) * 8);
     b.dyn = 1;
     b.bsmall = short_batch(op, QT, V, R) ? 1 : 0;
     b.xi = xi;
@@ -962,6 +979,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.R = R;
   a.tile = tile;
   a.static_frac = static_frac;
+  a.gather_keep = gather_keep(op, int64_t(w) * 8);
   a.xi = xi;
   a.tol = tol;
   a.s_eff = int32_t(s_eff);
@@ -1190,7 +1208,7 @@ phx_status phx_op_create_csr(int64_t n, const int64_t* row_ptr, const int32_t* c
     op->device = dev;
     op->n = n;
     op->nnz = nnz;
-    row_length_stats(op, row_ptr);
+    row_length_stats(op, row_ptr, col_idx);
     try {
       PHX_CUDA(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
       PHX_CUDA(cudaEventCreate(&op->ev0));
@@ -1243,7 +1261,7 @@ phx_status phx_op_create_csr_partitioned(int64_t n, const int64_t* row_ptr,
     auto* op = new phx_op_s();
     op->n = n;
     op->nnz = nnz;
-    row_length_stats(op, row_ptr);
+    row_length_stats(op, row_ptr, col_idx);
     op->nparts = nparts;
     try {
       int cur = 0;

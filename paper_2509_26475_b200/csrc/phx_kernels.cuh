@@ -62,6 +62,7 @@ struct BlockArgs {
   int32_t dyn;          // 1: dynamic-tail kernel (always for partitioned runs)
   int32_t bsmall;       // 1: the short-gather-batch variant (rows fit it)
   int32_t lat;          // 1: the latency-mode variant (fewer tiles than SMs)
+  float gather_keep;    // L2 evict_last fraction for gather loads (0 or 1)
   int32_t cl_rows;      // cluster mode: rows per part allocated in shared memory
   int32_t cl_nnz;       // cluster mode: CSR entries per part allocated in shared memory
   double static_frac;  // DYN kernels: share of a phase's CTA tiles assigned statically
