@@ -229,13 +229,14 @@ struct DeviceGuard {
   }
 };
 
-// Parameter selection and the column-block apply run on an unpartitioned
-// operator; a partitioned one serves phimv_block with a reused ScalingShift.
+// Parameter selection and the column-block apply run on the operator's
+// whole CSR on one device: a partitioned operator keeps a selection replica
+// on part 0's device (created with it), so its ScalingShift is bitwise the
+// unpartitioned one.  (The power basis, n x 62 doubles, must then fit that
+// device: n up to ~3e8 on a 180 GB B200.)
 void require_whole(phx_op op, const char* who) {
-  if (op->nparts > 1)
-    throw_phx(PHX_EINVAL, std::string(who) +
-                              ": needs an unpartitioned operator (select parameters on the whole "
-                              "operator and reuse the ScalingShift)");
+  if (op->nparts > 1 && op->d_rp == nullptr)
+    throw_phx(PHX_EINVAL, std::string(who) + ": the partitioned operator has no selection replica");
 }
 
 // ---------------------------------------------------------------------------
@@ -1310,6 +1311,17 @@ phx_status phx_op_create_csr_partitioned(int64_t n, const int64_t* row_ptr,
       PHX_CUDA(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
       PHX_CUDA(cudaEventCreate(&op->ev0));
       PHX_CUDA(cudaEventCreate(&op->ev1));
+      // the selection replica: the whole CSR on part 0's device
+      std::vector<int32_t> rp32(size_t(n) + 1);
+      for (int64_t i = 0; i <= n; ++i) rp32[size_t(i)] = int32_t(row_ptr[i]);
+      PHX_CUDA(cudaMalloc(&op->d_rp, (size_t(n) + 1) * 4));
+      PHX_CUDA(cudaMalloc(&op->d_ci, std::max<size_t>(1, size_t(nnz)) * 4));
+      PHX_CUDA(cudaMalloc(&op->d_av, std::max<size_t>(1, size_t(nnz)) * 8));
+      PHX_CUDA(cudaMemcpy(op->d_rp, rp32.data(), (size_t(n) + 1) * 4, cudaMemcpyHostToDevice));
+      if (nnz > 0) {
+        PHX_CUDA(cudaMemcpy(op->d_ci, col_idx, size_t(nnz) * 4, cudaMemcpyHostToDevice));
+        PHX_CUDA(cudaMemcpy(op->d_av, vals, size_t(nnz) * 8, cudaMemcpyHostToDevice));
+      }
     } catch (...) {
       phx_op_destroy(op);
       throw;

@@ -82,9 +82,19 @@ def test_partitioned_full_c2_bitwise():
     assert np.array_equal(W, ref)
 
 
-def test_partitioned_rejects_selection():
+@pytest.mark.parametrize("cfg,size,parts", [(2, 32, 2), (3, 12, 3), (5, 2000, 7)])
+def test_partitioned_selection_is_the_whole_operators(cfg, size, parts):
+    """select_parameters / apply on a partitioned operator run on its selection
+    replica (the whole CSR on part 0's device): bitwise the unpartitioned
+    ScalingShift, and the evaluation with it matches end to end."""
     p = P()
-    wl = p.workload(2, 32)
-    part = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=2)
-    with pytest.raises(ValueError, match="unpartitioned"):
-        p.select_parameters(part, 61, wl.tol)
+    wl = p.workload(cfg, size)
+    whole = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    part = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=parts)
+    ss_w = p.select_parameters(whole, 61, wl.tol)
+    ss_p = p.select_parameters(part, 61, wl.tol)
+    assert ss_p.astuple() == ss_w.astuple()
+    X = np.asfortranarray(wl.V[:, :2])
+    assert np.array_equal(part.apply(X), whole.apply(X))
+    req = p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss_p)
+    assert np.array_equal(p.phimv_block(part, req).W, p.phimv_block(whole, req).W)
