@@ -244,3 +244,52 @@ def test_single_variant_with_recovery_bitwise():
     assert rec.s_effective > 1
     assert res.stats.series_lens_F == rec.series_lens_F
     assert np.array_equal(res.w, w) and np.array_equal(res.exp_v0, e0) and np.array_equal(res.tail, tail)
+
+
+def test_irregular_csr_bitwise():
+    """Legal but irregular CSR: unsorted columns, duplicate column entries,
+    empty rows, explicit zeros, one dense row (> the staged-entry capacity,
+    the global-memory gather path).  Rows accumulate in storage order on both
+    sides, so selection, the run record and W stay bitwise the oracle's."""
+    P_ = P()
+    rng = np.random.default_rng(77)
+    n = 900
+    rows = []
+    for i in range(n):
+        if i % 37 == 5:
+            rows.append([])                                        # empty row
+            continue
+        k = int(rng.integers(1, 7))
+        cols = list(rng.integers(0, n, size=k))
+        if i % 11 == 0:
+            cols.append(cols[0])                                   # duplicate entry
+        cols.append(i)
+        rng.shuffle(cols)                                          # unsorted
+        rows.append(cols)
+    rows[450] = list(rng.permutation(n)[:400]) + [450]             # one very long row
+    rp = np.zeros(n + 1, dtype=np.int64)
+    ci, av = [], []
+    for i, cols in enumerate(rows):
+        for c in cols:
+            ci.append(int(c))
+            av.append(0.0 if (len(av) % 53 == 7) else float(rng.standard_normal()) * (
+                -8.0 if c == i else 1.0))
+        rp[i + 1] = len(ci)
+    ci = np.array(ci, dtype=np.int32)
+    av = np.array(av)
+    op = P_.CsrOperator(n, rp, ci, av)
+    oop = O.csr_from_arrays(n, rp, ci, av)
+    X = O.Rng(5).matrix(n, 3)
+    assert np.array_equal(op.apply(X), O.apply(oop, X))
+    tol = 1e-12
+    ss = P_.select_parameters(op, 61, tol)
+    sso = O.select_parameters(oop, 61, tol)
+    assert ss.astuple() == sso.astuple()
+    V = O.Rng(6).matrix(n, 3)
+    t = np.array([0.1, 0.7, 1.3])
+    alpha = np.array([1.0, -0.5, 2.0])
+    Wo, ro = O.phimv_block(oop, t, alpha, V, tol, sso)
+    res = P_.phimv_block(op, P_.BlockPhiRequest(t, alpha, V, tol, ss))
+    assert (res.stats.s_effective, res.stats.series_len_S) == (ro.s_effective, ro.series_len_S)
+    assert res.stats.series_lens_F == ro.series_lens_F
+    assert np.array_equal(res.W, Wo)
