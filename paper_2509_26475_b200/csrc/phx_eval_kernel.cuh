@@ -723,6 +723,11 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   };
 
   // ================= init: Vw = V[src]*g, D = S = Vw (phi_block.cpp:76-92)
+  // Vw_1, D_1 and S_1 are the same block; instead of writing it three times,
+  // the init stores V row-major (stride p+1) into D0 and the first S term
+  // recomputes Vw_1 = fl(V[src] * g) wherever it needs it (the same single
+  // multiply, so the same bits) -- 6 block passes fewer per launch.
+  const int p1 = p + 1;
   unsigned long long m0 = 0, mv = 0;  // max |Vw| row sum; max |V| entry (finiteness)
   {
     unsigned c[Q];
@@ -751,13 +756,10 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
               }
               ax[q][e] = fabs(x[q][e]);
             }
-            if (rv && v[q]) {
-              const unsigned o = unsigned(row) * ldb + c[q];
-              Vio<V>::st(a.Vw + o, x[q]);
-              Vio<V>::st(a.D0 + o, x[q]);
-              Vio<V>::st(a.S + o, x[q]);
-            }
           }
+          if (rv)  // the row's V entries, row-major, into D0
+            for (int col = LS.lg; col < p1; col += LS.G)
+              a.D0[size_t(row) * size_t(p1) + col] = __ldg(a.V + size_t(col) * size_t(n) + row);
           const double rsum = group_rowsum<Q, V>(ax, LS.G, LS.qp);
           if (rv) m0 = umax64(m0, abs_bits(rsum));
         }
@@ -822,7 +824,149 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   double* Dn = a.D1;
   int err = kStOk, err_idx = 0;
   const bool vwl_vec = V == 2 && (r % 2) == 0;
-  for (;;) {
+  // the first term (k = 2), peeled: its D_1 = Vw_1 = S_1 comes from the
+  // row-major V in D0 (see the init); same decision and arithmetic as the loop
+  if (c1 + c2 > a.tol * nS) {
+    ++k;
+    c1 = c2;
+    sigma *= k;
+    unsigned long long mdb = 0;
+    {
+      unsigned c[Q];
+      bool v[Q];
+      cols(LS, c, v);
+      int src[Q][V], srcl[Q][V];  // V column of Vw_1's column c and of c - r
+      double gg[Q][V], kd[Q][V], ka[Q][V], tos[Q][V];
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const int cc = int(c[q]) + e;
+          const int j = v[q] ? cc / r : 0, i = v[q] ? cc - j * r : 0;
+          src[q][e] = j == 0 ? 0 : p + 1 - j;
+          srcl[q][e] = j <= 1 ? 0 : p + 2 - j;
+          gg[q][e] = v[q] ? __ldg(a.g + i) : 0.0;
+          kd[q][e] = v[q] ? __ldg(a.colKd + cc) : 0.0;
+          ka[q][e] = v[q] ? __ldg(a.colKa + cc) : 0.0;
+          tos[q][e] = v[q] ? __ldg(a.colTos + cc) : 0.0;
+        }
+      const double* const* Vt = gtab[0];  // PART: the parts' D0 (their row-major V)
+      run_tiles<DYN, CL>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+                         crp, cci, cav,
+                [&](int base, const int* rp, const int* ci, const double* avs) {
+          const int e_lo = rp[0];
+          const bool sm = rp[LS.RW] - e_lo <= kEC;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const int row = base + rr * LS.gpw + LS.g;
+            const bool rv = row < n;
+            const int li = rr * LS.gpw + LS.g;
+            const int e0 = rp[li] - e_lo, cnt = rp[li + 1] - rp[li];
+            // gather: acc = sum_e av_e * Vw_1[col_e] = av_e * fl(V[col_e][src] * g)
+            double acc[Q][V];
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int e = 0; e < V; ++e) acc[q][e] = 0.0;
+            for (int u = 0; u < cnt; ++u) {
+              const int ee = e0 + u;
+              const unsigned enc = unsigned(sm ? ci[ee] : __ldg(a.ci + e_lo + ee));
+              const double av = sm ? avs[ee] : __ldg(a.av + e_lo + ee);
+              const double* vr = gather_row_ptr<PART>(a.D0, Vt, enc, unsigned(p1));
+#pragma unroll
+              for (int q = 0; q < Q; ++q)
+                if (v[q]) {
+#pragma unroll
+                  for (int e = 0; e < V; ++e)
+                    acc[q][e] = acc[q][e] + av * (vr[src[q][e]] * gg[q][e]);
+                }
+            }
+            double ad[Q][V];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              const bool vv = rv && v[q];
+              double vn[V], dn[V], sn[V];
+              const double* vo = a.D0 + size_t(rv ? row : 0) * size_t(p1);
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                const int cc = int(c[q]) + e;
+                const double vw = vv ? vo[src[q][e]] * gg[q][e] : 0.0;  // Vw_1 = D_1 = S_1
+                const double vwl = (vv && cc >= 2 * r) ? vo[srcl[q][e]] * gg[q][e] : 0.0;
+                double g2 = 0.0;  // Vw = Vw * Kiter (:98)
+                if (cc >= 2 * r) g2 = g2 + vwl * ka[q][e];
+                g2 = g2 + vw * kd[q][e];
+                vn[e] = g2;
+                double y = acc[q][e];  // D = (A - xi I) D (:99), * t_i/s, + Vw
+                if (has_xi) y = y - a.xi * vw;
+                y = y * tos[q][e];
+                dn[e] = y + g2;
+                sn[e] = vw + dn[e] / sigma;  // S += D/sigma (:105)
+                ad[q][e] = vv ? fabs(dn[e]) : 0.0;
+              }
+              if (vv) {
+                const unsigned o = unsigned(row) * ldb + c[q];
+                st_s<!CL>(a.Vw + o, vn);
+                Vio<V>::st(Dn + o, dn);
+                st_s<!CL>(a.S + o, sn);
+              }
+            }
+            const double rd = group_rowsum<Q, V>(ad, LS.G, LS.qp);
+            if (rv) mdb = umax64(mdb, abs_bits(rd));
+          }
+                });
+    }
+    double maxD, dmy;
+    sync_step(mdb, mdb, maxD, dmy);
+    c2 = maxD / sigma;  // :103
+    if (!isfinite(c2)) {
+      err = kStSeriesDiverged;
+      err_idx = k;
+    } else {
+      nSu = (nSu + c2) * (1.0 + 1e-12);
+      nSl = (nSl - c2) * (1.0 - 1e-12);
+      exact = false;
+      if (exact_every_term) {
+        nS = s_norm_exact();
+        nSl = nSu = nS;
+        exact = true;
+      }
+      trace(1.0, c2, nS);
+      double* tmp = Dc;
+      Dc = Dn;
+      Dn = tmp;
+      dpar ^= 1;
+    }
+  } else {
+    // no S term at all (tol * ||S|| infinite): the phases below read S = Vw_1
+    unsigned c[Q];
+    bool v[Q];
+    cols(LS, c, v);
+    for (int t = cta; t < ntiles; t += ncta)
+      for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
+        const int base = t * a.tile + wt * LS.RW;
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = base + rr * LS.gpw + LS.g;
+          if (row >= n) continue;
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
+            if (v[q]) {
+              double x[V];
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                const int cc = int(c[q]) + e;
+                const int j = cc / r, i = cc - j * r;
+                const int sc = j == 0 ? 0 : p + 1 - j;
+                x[e] = a.D0[size_t(row) * size_t(p1) + sc] * __ldg(a.g + i);
+              }
+              Vio<V>::st(a.S + (unsigned(row) * ldb + c[q]), x);
+            }
+        }
+      }
+    double dmy1, dmy2;
+    sync_step(0ull, 0ull, dmy1, dmy2);
+  }
+  for (; err == kStOk;) {
     const double lhs = c1 + c2;
     bool cont;
     if (exact) {
