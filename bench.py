@@ -133,16 +133,20 @@ def max_over_ranks(x: float, dist=None, device="cpu") -> float:
 
 
 def algorithmic_bytes(wl, rec):
-    """Algorithmic HBM bytes of one k_phimv_block launch:
-    init 8n(p+1) + 24wn; each S term B_S = CSR + 48wn; promotion+assembly
-    CSR + 8n(3r+1); each recovery term B_F = CSR + 64rn (fcols = 2r);
-    each sweep end 8n(4r + 2pr)."""
+    """Algorithmic HBM bytes of one k_phimv_block launch,
+    counting only bytes the kernel moves: init 16n(p+1) (V read, V row-major
+    write -- Vw_1 = D_1 = S_1 is recomputed, not stored); the first S term
+    CSR + 8n(p+1) + 24wn (V rows gathered, Vw/D'/S written), each further
+    S term B_S = CSR + 48wn; promotion+assembly CSR + 8n(3r+1); each
+    recovery term B_F = CSR + 32 fc n; each sweep end 8n(2fc + 2pr)."""
     n, p, r = wl.n, wl.p, wl.r
     w = (p + 1) * r
     fc = r if p == 0 else 2 * r
     csr = 12 * wl.nnz + 4 * (n + 1)
-    b = 8 * n * (p + 1) + 24 * w * n
-    b += (rec.series_len_S - 1) * (csr + 48 * w * n)
+    b = 16 * n * (p + 1)
+    if rec.series_len_S >= 2:
+        b += csr + 8 * n * (p + 1) + 24 * w * n
+    b += max(0, rec.series_len_S - 2) * (csr + 48 * w * n)
     b += csr + 8 * n * (3 * r + 1)
     for lf in rec.series_lens_F:
         b += lf * (csr + 32 * fc * n)
