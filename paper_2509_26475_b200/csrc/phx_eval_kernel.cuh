@@ -203,6 +203,9 @@ struct WarpPipe {
   int rp[3][kMaxRW + 1];
   int ci[2][kEC];
   double av[2][kEC];
+  // latency mode: slot 0 still holds this tile's row_ptr and entries (set
+  // after a single-tile sequence -- the warp owns the same tile every step)
+  int cached_base, cached_rw;
 };
 
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -271,20 +274,35 @@ __device__ __forceinline__ void issue_entries(const BlockArgs& a, const int* rp,
 
 // body(base, rp, ci, av): rp = row_ptr[base .. base+RW] (clamped at n); when
 // rp[RW] - rp[0] <= kEC, ci/av hold the tile's entries from index 0.
-template <class Seq, class Body>
+template <bool CACHE, class Seq, class Body>
 __device__ __forceinline__ void pipelined(const BlockArgs& a, Seq& ts, int RW, WarpPipe& pp,
                                           int lane, Body& body) {
   const int b0 = ts.at(0, lane);
   if (b0 < 0) return;  // warp-uniform
+  int b1 = -1;
+  if constexpr (CACHE) {
+    b1 = ts.at(1, lane);
+    if (b1 < 0 && pp.cached_base == b0 && pp.cached_rw == RW) {
+      body(b0, pp.rp[0], pp.ci[0], pp.av[0]);  // no restaging round trips
+      __syncwarp();
+      return;
+    }
+  }
   __syncwarp();
   issue_rp(a, pp.rp[0], b0, RW, lane);
   cp_commit();
   cp_wait_all();
   __syncwarp();
   issue_entries(a, pp.rp[0], RW, pp.ci[0], pp.av[0], lane);
-  const int b1 = ts.at(1, lane);
+  if constexpr (!CACHE) b1 = ts.at(1, lane);
   if (b1 >= 0) issue_rp(a, pp.rp[1], b1, RW, lane);
   cp_commit();
+  if constexpr (CACHE) {
+    if (lane == 0) {  // what slot 0 holds afterwards (a single tile never leaves it)
+      pp.cached_base = b1 < 0 ? b0 : -1;
+      pp.cached_rw = RW;
+    }
+  }
   int base = b0;
   for (int s = 0; base >= 0; ++s) {
     cp_wait_all();
@@ -304,7 +322,7 @@ __device__ __forceinline__ void pipelined(const BlockArgs& a, Seq& ts, int RW, W
 
 // every warp tile of a phase: the static part, then the dynamic tail from
 // counter ctr (zeroed before the phase's step began)
-template <bool DYN, bool CL, class Body>
+template <bool DYN, bool CL, bool CACHE, class Body>
 __device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, int ntiles,
                                           int warp, int cta, int ncta,
                                           unsigned long long* ctr, WarpPipe& pp, int lane,
@@ -337,7 +355,7 @@ __device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, i
     ts.warp = warp;
     ts.cta = cta;
     ts.ncta = ncta;
-    pipelined(a, ts, L.RW, pp, lane, body);
+    pipelined<CACHE>(a, ts, L.RW, pp, lane, body);
   }
   if (DYN && tst < ntiles) {
     DynSeq ds;
@@ -349,7 +367,7 @@ __device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, i
     ds.mpos = -1;
     ds.mval = -1;
     if (lane == 0) ds.pend = atomicAdd(ctr, 1ull);
-    pipelined(a, ds, L.RW, pp, lane, body);
+    pipelined<CACHE>(a, ds, L.RW, pp, lane, body);
   }
   }
 }
@@ -498,6 +516,10 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpPipe& pp = pipe[warp];
+  if (LAT) {
+    if (lane == 0) pp.cached_base = -1;
+    __syncwarp();
+  }
 
   // Partitioned operator: this launch handles parts
   // plo .. plo+pcount-1, CTAs split evenly; a CTA rebinds the row-local
@@ -851,7 +873,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
           tos[q][e] = v[q] ? __ldg(a.colTos + cc) : 0.0;
         }
       const double* const* Vt = gtab[0];  // PART: the parts' D0 (their row-major V)
-      run_tiles<DYN, CL>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+      run_tiles<DYN, CL, LAT>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
                          crp, cci, cav,
                 [&](int base, const int* rp, const int* ci, const double* avs) {
           const int e_lo = rp[0];
@@ -1007,7 +1029,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
           ka[q][e] = v[q] ? __ldg(a.colKa + cc) : 0.0;
           tos[q][e] = v[q] ? __ldg(a.colTos + cc) : 0.0;
         }
-      run_tiles<DYN, CL>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+      run_tiles<DYN, CL, LAT>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
                          crp, cci, cav,
                 [&](int base, const int* rp, const int* ci, const double* avs) {
           // row-local streams (independent of the CSR slice): before or after
@@ -1130,7 +1152,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
     cols(LF, c, v);
 #pragma unroll
     for (int q = 0; q < Q; ++q) vl[q] = v[q] && int(c[q]) < r;
-    run_tiles<DYN, CL>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+    run_tiles<DYN, CL, LAT>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
                        crp, cci, cav,
               [&](int base, const int* rp, const int* ci, const double* avs) {
         double acc[R][Q][V];
@@ -1278,7 +1300,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
             const int i = cc < r ? cc : cc - r;
             tosF[q][e] = v[q] ? __ldg(a.colTos + i) : 0.0;
           }
-        run_tiles<DYN, CL>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
+        run_tiles<DYN, CL, LAT>(a, LF, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
                        crp, cci, cav,
                   [&](int base, const int* rp, const int* ci, const double* avs) {
             double eo[R][Q][V], fs[R][Q][V], acc[R][Q][V];
