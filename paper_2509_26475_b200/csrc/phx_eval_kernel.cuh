@@ -17,6 +17,8 @@
 // lane-local pair is the tree's first level, the butterfly the next ones.
 #include <cooperative_groups.h>
 
+#include <atomic>
+
 #pragma once
 #include "phx_kernels.cuh"
 
@@ -1493,14 +1495,32 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   finish(err, err_idx, L_S, 0);
 }
 
+// sets the variant's dynamic shared memory limit and returns its co-resident
+// CTAs per SM; both are per device and fixed, so they are cached per (device,
+// block size) -- the calls cost ~10 us each on every evaluation otherwise
 template <int Q, int V, int R, bool PART, bool DYN, int BO, bool CL, bool LAT>
 cudaError_t eval_occupancy(int block, int* per_sm) {
-  const cudaError_t e = cudaFuncSetAttribute(k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(kPipeBytes));
+  static std::atomic<long long> cache[kOccCacheDevices];  // (block << 32) | per_sm + 1
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+  const bool cacheable = dev >= 0 && dev < kOccCacheDevices;
+  if (cacheable) {
+    const long long c = cache[dev].load(std::memory_order_relaxed);
+    if (c != 0 && (c >> 32) == block) {
+      *per_sm = int(c & 0xffffffffLL) - 1;
+      return cudaSuccess;
+    }
+  }
+  e = cudaFuncSetAttribute(k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPipeBytes));
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       per_sm, k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>, block, kPipeBytes);
+  if (e == cudaSuccess && cacheable)
+    cache[dev].store((static_cast<long long>(block) << 32) | (*per_sm + 1),
+                     std::memory_order_relaxed);
+  return e;
 }
 
 template <int Q, int V, int R, bool PART, bool DYN, int BO = 0, bool CL = false, bool LAT = false>

@@ -147,6 +147,10 @@ struct PartDev {
 
 }  // namespace
 
+// control-block slots per operator: evaluations that may be in flight at once
+// (the integrator enqueues a step's four before one synchronize)
+constexpr int kCtlSlots = 4;
+
 struct phx_op_s {
   int nparts = 1;                // > 1: row-partitioned (parts[], no d_rp/d_ci/d_av)
   std::vector<PartDev> parts;
@@ -161,10 +165,10 @@ struct phx_op_s {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::mutex mu;
   // evaluation workspace
-  DevBuf Vw, D0, D1, S, F0, F1, E, W, V, coef, slots, status, lensF, FLo, FRo, trace, tstamp;
+  DevBuf Vw, D0, D1, S, F0, F1, E, W, V, FLo, FRo, trace, tstamp, ctl[kCtlSlots];
   // selection workspace
   DevBuf w0, w1, y, chunkmax, inv, partial, gcoef, spx, spy;
-  HostBuf h_small, h_chunk, h_inv, h_part, h_lens;
+  HostBuf h_small, h_chunk, h_inv, h_part, h_lens, h_ctl[kCtlSlots], h_flag;
   // fixed-seed start vectors (params.cpp:102-110), cached per operator
   std::vector<double> start1, start2;
   bool have_start2 = false;
@@ -601,6 +605,18 @@ struct EvalIn {
   bool single;
   double* h_exp_v0;
   double* h_tail;
+  int32_t slot;  // control-block slot (kCtlSlots): evaluations in flight at once
+};
+
+
+// an evaluation whose status is decoded after the caller's synchronize
+struct PendingEval {
+  const int32_t* status = nullptr;  // pinned host copy, nullptr: already decoded
+  const int32_t* lens = nullptr;
+  long s_eff = 0, nsw = 0;
+  int32_t w = 0, r = 0, fcols = 0;
+  bool single = false;
+  std::vector<int32_t> own;  // non-empty: status (8) + lens copied here
 };
 
 // Row-partitioned evaluation.  Every part runs the same
@@ -809,7 +825,11 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
   }
 }
 
-void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
+void finish_eval(const PendingEval& pe, phx_run_record* rec);
+
+// defer != nullptr: enqueue only (single-device, no trace): the caller
+// synchronizes the stream and calls finish_eval(*defer, rec)
+void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* defer = nullptr) {
   const char* who = in.single ? "phimv" : "phimv_block";
   const int64_t n = op->n;
   const int32_t r = in.r;
@@ -986,7 +1006,16 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.s_eff = int32_t(s_eff);
   a.single_variant = in.single ? 1 : 0;
   a.t_single = in.t[0];
-  double* d_coef = op->coef.as<double>(ncoef);
+  // one control block per call, uploaded and read back with one copy each:
+  // [coef ncoef doubles][slots 12 u64][status 8 i32][lensF nsw i32]
+  const size_t cb = ncoef * 8;
+  const size_t ctl_up = cb + 128;  // coefficients + zeroed slots/status
+  const size_t ctl_bytes = ctl_up + size_t(std::max<int64_t>(1, nsw)) * 4;
+  char* d_ctl = static_cast<char*>(op->ctl[in.slot].get(ctl_bytes));
+  char* h_ctl = static_cast<char*>(op->h_ctl[in.slot].get(ctl_bytes));
+  std::memcpy(h_ctl, coef.data(), cb);
+  std::memset(h_ctl + cb, 0, 128);
+  double* d_coef = reinterpret_cast<double*>(d_ctl);
   a.colKd = d_coef;
   a.colKa = d_coef + w;
   a.colTos = d_coef + 2 * w;
@@ -1007,9 +1036,9 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   a.W = in.dW ? in.dW : op->W.as<double>(size_t(n) * size_t(r));
   a.FLo = in.h_exp_v0 ? op->FLo.as<double>(size_t(n) * size_t(r)) : nullptr;
   a.FRo = in.h_tail ? op->FRo.as<double>(size_t(n) * size_t(r)) : nullptr;
-  a.slots = op->slots.as<unsigned long long>(12);  // [3][maxA, maxB, tile counter, pad]
-  a.status = op->status.as<int32_t>(8);
-  a.lensF = op->lensF.as<int32_t>(size_t(std::max<long>(1, s_eff - 1)));
+  a.slots = reinterpret_cast<unsigned long long*>(d_ctl + cb);  // [3][maxA, maxB, tile counter, pad]
+  a.status = reinterpret_cast<int32_t*>(d_ctl + cb + 96);
+  a.lensF = reinterpret_cast<int32_t*>(d_ctl + ctl_up);
   a.nparts = 1;
   static const bool step_times = std::getenv("PHX_STEP_TIMES") != nullptr;
   a.tstamp_cap = step_times ? 1 << 20 : 0;
@@ -1029,9 +1058,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
                                  size_t(p + 1), cudaMemcpyHostToDevice, st));
     a.V = dV;
   }
-  PHX_CUDA(cudaMemcpyAsync(d_coef, coef.data(), ncoef * 8, cudaMemcpyHostToDevice, st));
-  PHX_CUDA(cudaMemsetAsync(a.slots, 0, 12 * sizeof(unsigned long long), st));
-  PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), st));
+  PHX_CUDA(cudaMemcpyAsync(d_ctl, h_ctl, ctl_up, cudaMemcpyHostToDevice, st));
 
   int max_blocks = 0;
   a.bsmall = short_batch(op, QT, V, R) ? 1 : 0;
@@ -1089,11 +1116,11 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
     }
   }
 
-  h_status = op->h_small.as<int32_t>(8);
-  PHX_CUDA(cudaMemcpyAsync(h_status, a.status, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  h_lens = op->h_lens.as<int32_t>(size_t(std::max<int64_t>(1, nsw)));
-  if (nsw > 0)
-    PHX_CUDA(cudaMemcpyAsync(h_lens, a.lensF, size_t(nsw) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  // status and the recovery lengths in one read-back
+  h_status = reinterpret_cast<int32_t*>(h_ctl + cb + 96);
+  h_lens = reinterpret_cast<int32_t*>(h_ctl + ctl_up);
+  PHX_CUDA(cudaMemcpyAsync(h_status, a.status, 32 + size_t(std::max<int64_t>(0, nsw)) * 4,
+                           cudaMemcpyDeviceToHost, st));
   if (in.hW) {
     if (in.ldw == n)
       PHX_CUDA(cudaMemcpyAsync(in.hW, a.W, size_t(n) * size_t(r) * 8, cudaMemcpyDeviceToHost, st));
@@ -1105,6 +1132,17 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
     PHX_CUDA(cudaMemcpyAsync(in.h_exp_v0, a.FLo, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
   if (in.h_tail)
     PHX_CUDA(cudaMemcpyAsync(in.h_tail, a.FRo, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
+  if (defer && trace_cap == 0 && !step_times) {
+    defer->status = h_status;
+    defer->lens = h_lens;
+    defer->s_eff = s_eff;
+    defer->nsw = nsw;
+    defer->w = w;
+    defer->r = r;
+    defer->fcols = fcols;
+    defer->single = in.single;
+    return;
+  }
   PHX_CUDA(cudaStreamSynchronize(st));
   PHX_CUDA(cudaEventElapsedTime(&ms, op->ev0, op->ev1));
   {
@@ -1119,11 +1157,37 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec) {
   }
   }  // single-device path
 
+  PendingEval pe;
+  pe.status = h_status;
+  pe.lens = h_lens;
+  pe.s_eff = s_eff;
+  pe.nsw = nsw;
+  pe.w = w;
+  pe.r = r;
+  pe.fcols = fcols;
+  pe.single = in.single;
+  if (defer) {  // evaluated synchronously (partitioned / traced): keep a copy
+    pe.own.assign(h_status, h_status + 8);
+    pe.own.insert(pe.own.end(), h_lens, h_lens + std::max<long>(0, nsw));
+    pe.status = pe.lens = nullptr;
+    *defer = std::move(pe);
+    return;
+  }
+  finish_eval(pe, rec);
+}
+
+void finish_eval(const PendingEval& pe, phx_run_record* rec) {
+  if (!pe.status && pe.own.empty()) return;
+  const char* who = pe.single ? "phimv" : "phimv_block";
+  const int32_t* h_status = pe.own.empty() ? pe.status : pe.own.data();
+  const int32_t* h_lens = pe.own.empty() ? pe.lens : pe.own.data() + 8;
+  const long s_eff = pe.s_eff, nsw = pe.nsw;
+  const int32_t w = pe.w, r = pe.r, fcols = pe.fcols;
   const int32_t code = h_status[0];
   const int32_t idx = h_status[1];
   const int32_t L_S = h_status[2];
   if (code == phx::kStInputNonFinite)
-    throw_phx(PHX_EINVAL, in.single ? "phimv: V has non-finite entries"
+    throw_phx(PHX_EINVAL, pe.single ? "phimv: V has non-finite entries"
                                     : "phimv_block: inputs must be finite");
   if (code == phx::kStSeriesCap)
     throw_phx(PHX_ENUMERIC, std::string(who) + ": series did not converge within 500 terms");
@@ -1351,11 +1415,16 @@ phx_status phx_op_destroy(phx_op op) {
     cudaSetDevice(op->device);
     if (op->stream) cudaStreamSynchronize(op->stream);
     for (DevBuf* b : {&op->Vw, &op->D0, &op->D1, &op->S, &op->F0, &op->F1, &op->E, &op->W, &op->V,
-                      &op->coef, &op->slots, &op->status, &op->lensF, &op->FLo, &op->FRo,
+                      &op->FLo, &op->FRo,
                       &op->trace, &op->w0, &op->w1, &op->y, &op->chunkmax, &op->inv,
-                      &op->partial, &op->gcoef, &op->spx, &op->spy})
+                      &op->partial, &op->gcoef, &op->spx, &op->spy, &op->tstamp})
       b->release();
-    for (HostBuf* b : {&op->h_small, &op->h_chunk, &op->h_inv, &op->h_part, &op->h_lens}) b->release();
+    for (HostBuf* b : {&op->h_small, &op->h_chunk, &op->h_inv, &op->h_part, &op->h_lens, &op->h_flag})
+      b->release();
+    for (int k = 0; k < kCtlSlots; ++k) {
+      op->ctl[k].release();
+      op->h_ctl[k].release();
+    }
     if (op->d_rp) cudaFree(op->d_rp);
     if (op->d_ci) cudaFree(op->d_ci);
     if (op->d_av) cudaFree(op->d_av);
@@ -1641,6 +1710,12 @@ bool rk_step_dev(phx_op op, RkWork& w, double gamma, const double* d_u, double h
   a.gamma = gamma;
   a.h = h;
   double* dW = w.W.as<double>(size_t(2 * n));
+  // the four evaluations are enqueued back to back (one control slot each)
+  // and their statuses decoded after the step's single synchronize; an
+  // evaluation that fails leaves the later stages computing on its output,
+  // and the first failure in stage order is the error reported, as in a
+  // stage-by-stage run
+  PendingEval pend[4];
   auto call = [&](int32_t r, const double* t, const double* al, int32_t p, int k) {
     EvalIn in{};
     in.r = r;
@@ -1651,7 +1726,8 @@ bool rk_step_dev(phx_op op, RkWork& w, double gamma, const double* d_u, double h
     in.tol = tol;
     in.params = ss;
     in.dW = dW;
-    evaluate(op, in, recs ? recs + k : nullptr);
+    in.slot = k;
+    evaluate(op, in, nullptr, &pend[k]);
   };
   // g_n, f_n = A u + g_n, hf = h f_n; stage 2 alone (:38-57)
   a.mode = 0;
@@ -1701,10 +1777,11 @@ bool rk_step_dev(phx_op op, RkWork& w, double gamma, const double* d_u, double h
   a.flag = w.flag.as<int>(1);
   PHX_CUDA(cudaMemsetAsync(a.flag, 0, sizeof(int), st));
   PHX_CUDA(phx::launch_rk_stage(a, st));
-  int flag = 0;
-  PHX_CUDA(cudaMemcpyAsync(&flag, a.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int* flag = op->h_flag.as<int>(1);
+  PHX_CUDA(cudaMemcpyAsync(flag, a.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   PHX_CUDA(cudaStreamSynchronize(st));
-  return flag != 0;
+  for (int k = 0; k < 4; ++k) finish_eval(pend[k], recs ? recs + k : nullptr);
+  return *flag != 0;
 }
 
 }  // namespace

@@ -198,6 +198,7 @@ cudaError_t launch_rk_stage(const RkStageArgs& a, cudaStream_t st);
 
 // block_series_direct term (phx_kernels.cu k_series_term); r <= kSeriesMaxR
 constexpr int kSeriesMaxR = 64;
+constexpr int kOccCacheDevices = 64;  // devices whose kernel occupancy is cached
 cudaError_t launch_series_term(int32_t n, int32_t p1, int32_t r, const double* X, const double* M,
                                const double* tpow, double* G, unsigned long long* slots,
                                cudaStream_t st);

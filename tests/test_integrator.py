@@ -197,3 +197,25 @@ def test_gpu_integrate_rejects_partitioned():
     sel = P.ScalingShift(1.0, 0.0, 1.0, 0.0, 61, 0)
     with pytest.raises(ValueError, match="partitioned"):
         P.integrate(P.ADRProblem(16, 16, 1e-3, -0.5, 1000.0, op, u0), 0.01, 0.02, 1e-8, sel)
+
+
+@pytest.mark.gpu
+def test_gpu_integrate_traced_matches_untraced():
+    """A step's four evaluations are decoded after one synchronize; with the
+    stopping trace on they run synchronously instead. Same state, same records."""
+    import paper_2509_26475_b200 as P
+    rp, ci, av, u0 = adr_arrays(20, 20)
+    g = GpuImpl()
+    gop = g.op_csr(400, rp, ci, av)
+    tol = 1e-10
+    sel = g.select_parameters(gop, 61, tol)
+    h = 0.125 / 16.0
+    ua, ta, ra = g.integrate(gop, 1000.0, u0, h, 3 * h, tol, sel)
+    P.set_trace(3 * 100000)
+    try:
+        ub, tb, rb = g.integrate(gop, 1000.0, u0, h, 3 * h, tol, sel)
+    finally:
+        P.set_trace(0)
+    assert np.array_equal(ua, ub) and ta == tb
+    _recs_equal(ra, rb)
+    assert all(r.matvecs > 0 for r in rb)
