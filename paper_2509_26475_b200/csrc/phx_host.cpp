@@ -1012,7 +1012,10 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
   const size_t ctl_up = cb + 128;  // coefficients + zeroed slots/status
   const size_t ctl_bytes = ctl_up + size_t(std::max<int64_t>(1, nsw)) * 4;
   char* d_ctl = static_cast<char*>(op->ctl[in.slot].get(ctl_bytes));
-  char* h_ctl = static_cast<char*>(op->h_ctl[in.slot].get(ctl_bytes));
+  // pinned host side: the upload image, then the read-back area (kept apart:
+  // a captured step graph re-uploads the image on every replay)
+  char* h_ctl = static_cast<char*>(op->h_ctl[in.slot].get(2 * ctl_bytes));
+  char* h_back = h_ctl + ctl_bytes;
   std::memcpy(h_ctl, coef.data(), cb);
   std::memset(h_ctl + cb, 0, 128);
   double* d_coef = reinterpret_cast<double*>(d_ctl);
@@ -1117,8 +1120,8 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
   }
 
   // status and the recovery lengths in one read-back
-  h_status = reinterpret_cast<int32_t*>(h_ctl + cb + 96);
-  h_lens = reinterpret_cast<int32_t*>(h_ctl + ctl_up);
+  h_status = reinterpret_cast<int32_t*>(h_back + cb + 96);
+  h_lens = reinterpret_cast<int32_t*>(h_back + ctl_up);
   PHX_CUDA(cudaMemcpyAsync(h_status, a.status, 32 + size_t(std::max<int64_t>(0, nsw)) * 4,
                            cudaMemcpyDeviceToHost, st));
   if (in.hW) {
@@ -1692,8 +1695,11 @@ void rk_check_op(phx_op op, const char* who) {
 
 // one exprk4s6_step (integrator.cpp:29-105): d_u -> d_next (device, n each);
 // returns true when d_next has a non-finite entry
-bool rk_step_dev(phx_op op, RkWork& w, double gamma, const double* d_u, double h, double tol,
-                 const phx_scaling_shift& ss, double* d_next, phx_run_record* recs) {
+// enqueue one step on the operator's stream (no synchronize): pend receives
+// the four evaluations' pending statuses; returns the pinned host word the
+// non-finite flag is read back into
+int* rk_step_enqueue(phx_op op, RkWork& w, double gamma, const double* d_u, double h, double tol,
+                     const phx_scaling_shift& ss, double* d_next, PendingEval (&pend)[4]) {
   using C = RkCoef;
   const int64_t n = op->n;
   cudaStream_t st = op->stream;
@@ -1715,7 +1721,6 @@ bool rk_step_dev(phx_op op, RkWork& w, double gamma, const double* d_u, double h
   // evaluation that fails leaves the later stages computing on its output,
   // and the first failure in stage order is the error reported, as in a
   // stage-by-stage run
-  PendingEval pend[4];
   auto call = [&](int32_t r, const double* t, const double* al, int32_t p, int k) {
     EvalIn in{};
     in.r = r;
@@ -1779,10 +1784,67 @@ bool rk_step_dev(phx_op op, RkWork& w, double gamma, const double* d_u, double h
   PHX_CUDA(phx::launch_rk_stage(a, st));
   int* flag = op->h_flag.as<int>(1);
   PHX_CUDA(cudaMemcpyAsync(flag, a.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  PHX_CUDA(cudaStreamSynchronize(st));
+  return flag;
+}
+
+// after the step's synchronize: the evaluations' errors in stage order, the
+// records, and whether u_next left the finite range
+bool rk_step_finish(const int* flag, const PendingEval (&pend)[4], phx_run_record* recs) {
   for (int k = 0; k < 4; ++k) finish_eval(pend[k], recs ? recs + k : nullptr);
   return *flag != 0;
 }
+
+bool rk_step_dev(phx_op op, RkWork& w, double gamma, const double* d_u, double h, double tol,
+                 const phx_scaling_shift& ss, double* d_next, phx_run_record* recs) {
+  PendingEval pend[4];
+  const int* flag = rk_step_enqueue(op, w, gamma, d_u, h, tol, ss, d_next, pend);
+  PHX_CUDA(cudaStreamSynchronize(op->stream));
+  return rk_step_finish(flag, pend, recs);
+}
+
+// One integrator step captured as a CUDA graph (4 stage kernels + 4
+// persistent evaluations + the control copies), replayed for every later step
+// with the same state buffers: the step's launches cost one graph launch.
+// Every step of an integration has the same h, so the captured coefficient
+// uploads (pinned images written once at capture) are valid for all replays.
+struct StepGraph {
+  cudaGraphExec_t ex = nullptr;
+  bool failed = false;
+  PendingEval pend[4];
+  const int* flag = nullptr;
+  ~StepGraph() {
+    if (ex) cudaGraphExecDestroy(ex);
+  }
+  bool capture(phx_op op, RkWork& w, double gamma, const double* d_u, double h, double tol,
+               const phx_scaling_shift& ss, double* d_next) {
+    cudaStream_t st = op->stream;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaGraph_t g = nullptr;
+    try {
+      flag = rk_step_enqueue(op, w, gamma, d_u, h, tol, ss, d_next, pend);
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return false;
+    }
+    if (cudaStreamEndCapture(st, &g) != cudaSuccess || !g) {
+      cudaGetLastError();
+      return false;
+    }
+    const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      ex = nullptr;
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  }
+};
 
 }  // namespace
 
@@ -1832,9 +1894,35 @@ phx_status phx_integrate(phx_op op, double gamma, const double* u0, double h, do
     PHX_CUDA(cudaMemcpyAsync(cur, u0, n * 8, cudaMemcpyHostToDevice, op->stream));
     double t = 0.0;
     if (t_out) *t_out = t;
+    // steps after the first replay a captured graph per state-buffer parity
+    // (PHX_GRAPH=0 disables; traced or timed runs evaluate step by step)
+    static const bool graphs_on = [] {
+      const char* e = std::getenv("PHX_GRAPH");
+      return !(e && e[0] == '0');
+    }();
+    int64_t trace_cap;
+    {
+      std::lock_guard<std::mutex> lk(g_trace_mu);
+      trace_cap = g_trace_cap;
+    }
+    const bool graphs = graphs_on && trace_cap == 0 && std::getenv("PHX_STEP_TIMES") == nullptr;
+    StepGraph sg[2];
     for (long step = 0; step < n_steps; ++step) {
       phx_run_record* rs = (recs && 4 * int64_t(step) + 3 < recs_cap) ? recs + 4 * step : nullptr;
-      if (rk_step_dev(op, w, gamma, cur, h, tol, *params, nxt, rs)) {
+      bool bad;
+      StepGraph& G = sg[step & 1];
+      const bool fresh = G.ex == nullptr;  // capturing counts the four launches once
+      if (graphs && step >= 1 && !G.failed && (G.ex || G.capture(op, w, gamma, cur, h, tol, *params, nxt))) {
+        PHX_CUDA(cudaGraphLaunch(G.ex, op->stream));
+        if (!fresh)
+          for (int k = 0; k < 4; ++k) phx::count_launch();
+        PHX_CUDA(cudaStreamSynchronize(op->stream));
+        bad = rk_step_finish(G.flag, G.pend, rs);
+      } else {
+        if (graphs && step >= 1) G.failed = true;
+        bad = rk_step_dev(op, w, gamma, cur, h, tol, *params, nxt, rs);
+      }
+      if (bad) {
         PHX_CUDA(cudaMemcpyAsync(u_out, cur, n * 8, cudaMemcpyDeviceToHost, op->stream));
         PHX_CUDA(cudaStreamSynchronize(op->stream));
         throw_phx(PHX_ENUMERIC,
