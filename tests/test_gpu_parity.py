@@ -293,3 +293,41 @@ def test_irregular_csr_bitwise():
     assert (res.stats.s_effective, res.stats.series_len_S) == (ro.s_effective, ro.series_len_S)
     assert res.stats.series_lens_F == ro.series_lens_F
     assert np.array_equal(res.W, Wo)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 33, 257, 4099])
+def test_tiny_and_ragged_operators_bitwise(n):
+    """Operators smaller than one tile, one row past a tile, and sizes that
+    leave a partial last tile (latency mode below the SM count, the
+    persistent grid above): selection, run record and W stay the oracle's."""
+    P_ = P()
+    n_, rp, ci, av = _random_sparse(n, min(3, n), 4242 + n)
+    op = P_.CsrOperator(n_, rp, ci, av)
+    oop = O.csr_from_arrays(n_, rp, ci, av)
+    tol = 1e-12
+    ss = P_.select_parameters(op, 61, tol)
+    sso = O.select_parameters(oop, 61, tol)
+    assert ss.astuple() == sso.astuple()
+    rng = O.Rng(9 + n)
+    V = rng.matrix(n_, 3)
+    t = np.array([0.3, 1.1, 2.5])
+    alpha = np.array([0.5, 1.0, -1.5])
+    Wo, ro = O.phimv_block(oop, t, alpha, V, tol, sso)
+    res = P_.phimv_block(op, P_.BlockPhiRequest(t, alpha, V, tol, ss))
+    assert (res.stats.s_effective, res.stats.series_len_S) == (ro.s_effective, ro.series_len_S)
+    assert res.stats.series_lens_F == ro.series_lens_F
+    assert np.array_equal(res.W, Wo)
+
+
+def test_block_width_limit():
+    """(p+1)*r above the widest variant is rejected with the documented error,
+    before any device work."""
+    P_ = P()
+    n, rp, ci, av = _random_sparse(64, 3, 5)
+    op = P_.CsrOperator(n, rp, ci, av)
+    ss = P_.ScalingShift(1.0, 0.0, 1.0, 0.0, 61, 0)
+    r = 40
+    p = 12  # w = 520 > 512
+    V = np.ones((n, p + 1))
+    with pytest.raises(ValueError, match="not supported"):
+        P_.phimv_block(op, P_.BlockPhiRequest(np.full(r, 0.1), np.ones(r), V, 1e-10, ss))
