@@ -113,3 +113,35 @@ def test_random_single_bitwise(seed):
     assert res.stats.series_lens_F == rec.series_lens_F
     assert np.array_equal(res.w, w)
     assert np.array_equal(res.exp_v0, e0) and np.array_equal(res.tail, tail)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_partitioned_bitwise(seed):
+    """The row-partitioned operator (2-5 parts on one device) on the same draws:
+    selection and evaluation stay the oracle's."""
+    P_ = P()
+    parts = 2 + seed % 4
+    for attempt in range(20):  # a draw with at least 4 rows per part
+        rng = np.random.default_rng(9000 + seed + 1000 * attempt)
+        n, rp, ci, av = _draw_operator(rng)
+        if n >= 4 * parts:
+            break
+    op = P_.CsrOperator(n, rp, ci, av, parts=parts)
+    oop = O.csr_from_arrays(n, rp, ci, av)
+    p, r, t, alpha, tol, V = _draw_request(rng, n)
+    sso = O.select_parameters(oop, 61, tol)
+    ss = P_.select_parameters(op, 61, tol)
+    assert ss.astuple() == sso.astuple()
+    if sso.s * float(np.max(np.abs(t))) > 400.0:
+        t = t * (400.0 / (sso.s * float(np.max(np.abs(t)))))
+    try:
+        Wo, ro = O.phimv_block(oop, t, alpha, V, tol, sso)
+    except Exception as e:
+        with pytest.raises(Exception) as got:
+            P_.phimv_block(op, P_.BlockPhiRequest(t, alpha, V, tol, ss))
+        assert str(got.value) == str(e)
+        return
+    res = P_.phimv_block(op, P_.BlockPhiRequest(t, alpha, V, tol, ss))
+    assert (res.stats.s_effective, res.stats.series_len_S) == (ro.s_effective, ro.series_len_S)
+    assert res.stats.series_lens_F == ro.series_lens_F
+    assert np.array_equal(res.W, Wo)
