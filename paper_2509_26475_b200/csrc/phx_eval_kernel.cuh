@@ -505,6 +505,10 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   // hinted load form costs the short-row kernels (C2, C5) even at fraction 0,
   // and cluster mode gathers shared memory
   constexpr bool HINT = !CL && DYN && BO == 0 && Q == 1 && V == 2 && RR == 1;
+#ifndef PHX_LEAN
+#define PHX_LEAN 1
+#endif
+  constexpr bool LEAN = PHX_LEAN && !CL && !LAT && !PART && !DYN && Q == 1 && V == 2 && RR == 1 && BO == 5;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long red[2][kWarps];
   // per-warp pipeline buffers: dynamic shared memory (kWarps * sizeof(WarpPipe))
@@ -513,6 +517,9 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   // gather tables [D0, D1, S, F0, F1][part] (PART only)
   __shared__ const double* gtab[5][PART ? kMaxParts : 1];
   __shared__ double gmax[2];
+  // LEAN: the column coefficients Kd, Ka, t/s (w <= 64 for Q = 1, V = 2),
+  // re-read per row in the S terms instead of held in registers
+  __shared__ double s_coef[LEAN ? 3 * 64 : 1];
   __shared__ unsigned long long cl_slot[2];                  // CL: this CTA's maxima
   __shared__ unsigned long long cl_box[2][CL ? kMaxParts : 1][2];  // CL: all parts', by step parity
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
@@ -746,6 +753,14 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
     }
   };
 
+  if constexpr (LEAN) {
+    for (int k = threadIdx.x; k < a.w && k < 64; k += blockDim.x) {
+      s_coef[k] = a.colKd[k];
+      s_coef[64 + k] = a.colKa[k];
+      s_coef[128 + k] = a.colTos[k];
+    }
+    __syncthreads();
+  }
   // ================= init: Vw = V[src]*g, D = S = Vw (phi_block.cpp:76-92)
   // Vw_1, D_1 and S_1 are the same block; instead of writing it three times,
   // the init stores V row-major (stride p+1) into D0 and the first S term
@@ -1031,9 +1046,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
           ka[q][e] = v[q] ? __ldg(a.colKa + cc) : 0.0;
           tos[q][e] = v[q] ? __ldg(a.colTos + cc) : 0.0;
         }
-      run_tiles<DYN, CL, LAT>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp, lane,
-                         crp, cci, cav,
-                [&](int base, const int* rp, const int* ci, const double* avs) {
+      auto sbody = [&](int base, const int* rp, const int* ci, const double* avs) {
           // row-local streams (independent of the CSR slice): before or after
           // the gather (Cfg::LATE)
           double vw[R][Q][V], vwl[R][Q][V], so[R][Q][V], ds[R][Q][V], acc[R][Q][V];
@@ -1112,7 +1125,93 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
             const double rd = group_rowsum<Q, V>(ad, LS.G, LS.qp);
             if (row < n) mdb = umax64(mdb, abs_bits(rd));
           }
-                });
+                };
+      if constexpr (LEAN) {
+        // grid-stride warp tiles, row_ptr slice read per tile, entries
+        // gathered straight from global memory (no staging pipeline)
+        // Q = R = 1, V = 2: the same arithmetic as sbody, statement for
+        // statement, with the lane's row handled inline
+        (void)sbody;
+        const int gw = cta * kWarps + warp, nw = ncta * kWarps;
+        for (int base = gw * LS.RW; base < n; base += nw * LS.RW) {
+          const int row = base + LS.g;
+          const bool vq0 = row < n && v[0];
+          const unsigned o = unsigned(row) * ldb + c[0];
+          double vw0 = 0.0, vw1 = 0.0, so0 = 0.0, so1 = 0.0, ds0 = 0.0, ds1 = 0.0, vl0 = 0.0,
+                 vl1 = 0.0;
+          if (vq0) {
+            double t2[2];
+            ld_s<true, 2>(a.Vw + o, t2);
+            vw0 = t2[0];
+            vw1 = t2[1];
+            ld_s<true, 2>(a.S + o, t2);
+            so0 = t2[0];
+            so1 = t2[1];
+            if (has_xi) {
+              Vio<2>::ld(Dc + o, t2);
+              ds0 = t2[0];
+              ds1 = t2[1];
+            }
+            if (vwl_vec) {
+              if (jj[0][0] >= 2) {
+                ld_s<true, 2>(a.Vw + (o - unsigned(r)), t2);
+                vl0 = t2[0];
+                vl1 = t2[1];
+              }
+            } else {
+              if (jj[0][0] >= 2) vl0 = ld1_s<true>(a.Vw + (o - unsigned(r)));
+              if (jj[0][1] >= 2) vl1 = ld1_s<true>(a.Vw + (o + 1 - unsigned(r)));
+            }
+          }
+          double a0 = 0.0, a1 = 0.0;
+          if (vq0) {
+            const int e1 = __ldg(a.rp + row + 1);
+            for (int e = __ldg(a.rp + row); e < e1; ++e) {
+              double x[2];
+              Vio<2>::ld(Dc + unsigned(__ldg(a.ci + e)) * ldb + c[0], x);
+              const double w = __ldg(a.av + e);
+              a0 = a0 + w * x[0];
+              a1 = a1 + w * x[1];
+            }
+          }
+          // the lane's coefficients from shared memory (volatile: re-read per
+          // row, not hoisted into registers held across the gather)
+          const volatile double* vk = s_coef;
+          const int c0 = v[0] ? int(c[0]) : 0;
+          const double kd0 = vk[c0], kd1 = vk[c0 + 1], ka0 = vk[64 + c0], ka1 = vk[64 + c0 + 1];
+          const double ts0 = vk[128 + c0], ts1 = vk[128 + c0 + 1];
+          // columns of blocks j < 2 have Ka = +0 and Vw[c - r] not loaded
+          // (+0): 0 + (+0 * +0) = +0, so the unconditional form is bitwise
+          // the branch of the reference order (:98)
+          double g0 = 0.0, g1 = 0.0;
+          g0 = g0 + vl0 * ka0;
+          g0 = g0 + vw0 * kd0;
+          g1 = g1 + vl1 * ka1;
+          g1 = g1 + vw1 * kd1;
+          double y0 = a0, y1 = a1;
+          if (has_xi) {
+            y0 = y0 - a.xi * ds0;
+            y1 = y1 - a.xi * ds1;
+          }
+          y0 = y0 * ts0;
+          y1 = y1 * ts1;
+          const double d0 = y0 + g0, d1 = y1 + g1;
+          const double s0 = so0 + d0 / sigma, s1 = so1 + d1 / sigma;
+          __syncwarp();  // every lane has read its Vw[c - r] before any lane writes Vw
+          if (vq0) {
+            const double vn2[2] = {g0, g1}, dn2[2] = {d0, d1}, sn2[2] = {s0, s1};
+            st_s<true, 2>(a.Vw + o, vn2);
+            Vio<2>::st(Dn + o, dn2);
+            st_s<true, 2>(a.S + o, sn2);
+          }
+          const double ad[1][2] = {{vq0 ? fabs(d0) : 0.0, vq0 ? fabs(d1) : 0.0}};
+          const double rd = group_rowsum<1, 2>(ad, LS.G, LS.qp);
+          if (row < n) mdb = umax64(mdb, abs_bits(rd));
+        }
+      } else {
+        run_tiles<DYN, CL, LAT>(a, LS, ntiles, warp, cta, ncta, a.slots + 4 * (step % 3) + 2, pp,
+                                lane, crp, cci, cav, sbody);
+      }
     }
     double maxD, dmy;
     sync_step(mdb, mdb, maxD, dmy);
