@@ -160,13 +160,13 @@ __global__ void __launch_bounds__(256, 4)
 // variant 3: variant 2 with the evaluator's per-lane column coefficients
 // (Kd, Ka, t/s and the column block index j per column, from global memory,
 // held in registers) and a runtime xi test
-template <bool SMEMC>
+template <bool SMEMC, bool RT = false>
 __global__ void __launch_bounds__(256, 4)
     k_sterm_cols(int n, int terms, const int* __restrict__ rp, const int* __restrict__ ci,
                  const double* __restrict__ av, double* D0, double* D1, double* __restrict__ S,
                  double* __restrict__ Vw, const double* __restrict__ colKd,
                  const double* __restrict__ colKa, const double* __restrict__ colTos, int r,
-                 double xi, unsigned long long* __restrict__ maxd) {
+                 double xi, unsigned long long* __restrict__ maxd, int ldb_rt = W, int g_rt = G) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   const int lane = threadIdx.x & 31;
   const int g = lane / G, q = lane % G;
@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(256, 4)
     for (int base = warp_global * rows_per_warp; base < n; base += nwarps * rows_per_warp) {
       const int row = base + g;
       const bool ok = row < n;
-      const size_t o = size_t(row) * W + c;
+      const unsigned LD = RT ? unsigned(ldb_rt) : unsigned(W);
+      const unsigned o = unsigned(row) * LD + c;
       double2 vw = make_double2(0.0, 0.0), so = vw, ds = vw, vwl = vw;
       if (ok) {
         vw = __ldcs(reinterpret_cast<const double2*>(Vw + o));
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(256, 4)
       if (ok) {
         const int e1 = __ldg(rp + row + 1);
         for (int e = __ldg(rp + row); e < e1; ++e) {
-          const double2 x = *reinterpret_cast<const double2*>(D + size_t(__ldg(ci + e)) * W + c);
+          const double2 x = *reinterpret_cast<const double2*>(D + unsigned(__ldg(ci + e)) * LD + c);
           const double a = __ldg(av + e);
           a0 = a0 + a * x.x;
           a1 = a1 + a * x.y;
@@ -248,7 +249,13 @@ __global__ void __launch_bounds__(256, 4)
         __stcs(reinterpret_cast<double2*>(S + o), make_double2(so.x + d0 / sigma, so.y + d1 / sigma));
       }
       double rs = ok ? fabs(d0) + fabs(d1) : 0.0;
-      for (int k = 1; k < G; k <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, k);
+      if (RT) {
+#pragma unroll
+        for (int k = 1; k < 32; k <<= 1)
+          if (k < g_rt) rs = rs + __shfl_xor_sync(0xffffffffu, rs, k);
+      } else {
+        for (int k = 1; k < G; k <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, k);
+      }
       const unsigned long long b = __double_as_longlong(rs);
       if (ok) m = b > m ? b : m;
     }
@@ -309,8 +316,8 @@ int main(int argc, char** argv) {
   }
   int sms = 0, per = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  if (variant == 3 || variant == 4) {
-    auto kc = variant == 4 ? k_sterm_cols<true> : k_sterm_cols<false>;
+  if (variant == 3 || variant == 4 || variant == 5) {
+    auto kc = variant == 5 ? k_sterm_cols<true, true> : variant == 4 ? k_sterm_cols<true> : k_sterm_cols<false>;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kc, 256, 0));
     const int grid = sms * per;
     int terms = 29, r = 4;
@@ -331,9 +338,10 @@ int main(int argc, char** argv) {
     unsigned long long* dm3;
     CK(cudaMalloc(&dm3, 24));
     CK(cudaMemset(dm3, 0, 24));
+    int ldb_rt = W, g_rt = G;
     void* args[] = {(void*)&n, (void*)&terms, (void*)&d_rp, (void*)&d_ci, (void*)&d_av,
                     (void*)&D0, (void*)&D1, (void*)&S, (void*)&Vw, (void*)&dk, (void*)&da,
-                    (void*)&dt, (void*)&r, (void*)&xi, (void*)&dm3};
+                    (void*)&dt, (void*)&r, (void*)&xi, (void*)&dm3, (void*)&ldb_rt, (void*)&g_rt};
     for (int it = 0; it < 2; ++it)
       CK(cudaLaunchCooperativeKernel((void*)kc, grid, 256, args, 0, 0));
     cudaEvent_t a2, b2;
@@ -350,7 +358,7 @@ int main(int argc, char** argv) {
     const double bytes = 12.0 * double(nnz) + 4.0 * (n + 1) + 48.0 * W * double(n);
     std::printf("{\"variant\": \"persistent+columns%s\", \"grid\": %d, \"ctas_per_sm\": %d, "
                 "\"us_per_term\": %.2f, \"alg_GBps\": %.1f, \"frac_of_6547.5\": %.3f}\n",
-                variant == 4 ? " (smem)" : "", grid, per, per_term * 1e6, bytes / per_term / 1e9,
+                variant == 5 ? " (smem, runtime ldb/G)" : variant == 4 ? " (smem)" : "", grid, per, per_term * 1e6, bytes / per_term / 1e9,
                 bytes / per_term / 1e9 / 6547.5);
     return 0;
   }
