@@ -331,3 +331,39 @@ def test_block_width_limit():
     V = np.ones((n, p + 1))
     with pytest.raises(ValueError, match="not supported"):
         P_.phimv_block(op, P_.BlockPhiRequest(np.full(r, 0.1), np.ones(r), V, 1e-10, ss))
+
+
+@pytest.mark.parametrize("n,p,r", [(5003, 3, 4), (9001, 1, 4), (6007, 3, 8), (20011, 0, 6)])
+def test_short_row_grid_kernel_bitwise(n, p, r):
+    """Operators with 3-5 entries per row and more tiles than SMs: the static
+    gather-batch-5 kernel with its lean S-term body (grid-stride warp tiles,
+    shared-memory column coefficients), at sizes that leave a ragged last
+    warp tile."""
+    P_ = P()
+    rng = np.random.default_rng(n + 7 * p + r)
+    rp = [0]
+    ci, av = [], []
+    for i in range(n):
+        k = int(rng.integers(2, 5))
+        cols = sorted(set(rng.integers(max(0, i - 300), min(n, i + 300), size=k).tolist()) | {i})
+        vals = rng.standard_normal(len(cols))
+        vals[cols.index(i)] = -(np.abs(vals).sum() + 1.0)
+        ci += cols
+        av += (vals * 50.0).tolist()
+        rp.append(len(ci))
+    rp, ci, av = np.array(rp, dtype=np.int64), np.array(ci, dtype=np.int32), np.array(av)
+    op = P_.CsrOperator(n, rp, ci, av)
+    oop = O.csr_from_arrays(n, rp, ci, av)
+    tol = 1e-10
+    ss = P_.select_parameters(op, 61, tol)
+    sso = O.select_parameters(oop, 61, tol)
+    assert ss.astuple() == sso.astuple()
+    V = O.Rng(n).matrix(n, p + 1)
+    t = np.linspace(0.2, 1.0, r) * (2.0 / sso.s)
+    alpha = np.linspace(-1.0, 1.5, r)
+    Wo, ro = O.phimv_block(oop, t, alpha, V, tol, sso)
+    res = P_.phimv_block(op, P_.BlockPhiRequest(t, alpha, V, tol, ss))
+    assert (res.stats.s_effective, res.stats.series_len_S) == (ro.s_effective, ro.series_len_S)
+    assert res.stats.series_lens_F == ro.series_lens_F
+    assert np.array_equal(res.W, Wo)
+    assert P_.last_eval_mode() == 0
