@@ -252,6 +252,12 @@ int64_t phx_kernel_launches(void);
  * device, 2..16 parts that fit). */
 int32_t phx_last_eval_mode(void);
 
+/* The kernel variant of the last single-device evaluation (diagnostics):
+ * out[0..7] = column chunks per lane Q, columns per lane V, rows per lane
+ * group R, dynamic tail (0/1), latency mode (0/1), short-row gather batch
+ * (0/1), grid size, CTA size. */
+phx_status phx_last_eval_variant(int32_t* out8);
+
 /* Device-event time (ms) of the last phimv_block evaluation kernel, and the
  * number of grid-wide steps it executed (S terms + promotion + recovery
  * terms + sweep ends). */

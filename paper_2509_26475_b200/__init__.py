@@ -78,6 +78,7 @@ ABI_SYMBOLS = (
     "phx_adr_csr", "phx_exprk4s6_step", "phx_integrate",
     "phx_mm_read_csr", "phx_mm_write_csr", "phx_op_create_mm", "phx_block_series_direct",
     "phx_last_eval_mode",
+    "phx_last_eval_variant",
 )
 
 
@@ -139,6 +140,7 @@ def lib():
                                           C.c_int64, C.c_double, dp, C.c_int64, dp, C.c_int64]
     L.phx_last_eval_stats.argtypes = [dp, i64p]
     L.phx_last_eval_mode.restype = C.c_int32
+    L.phx_last_eval_variant.argtypes = [C.POINTER(C.c_int32)]
     L.phx_set_trace.argtypes = [C.c_int64]
     L.phx_get_trace.argtypes = [dp, C.c_int64, i64p]
     _LIB = L
@@ -460,6 +462,14 @@ def last_eval_mode() -> int:
     """0: one grid-wide launch, 1: partitioned cooperative launches,
     2: partitioned operator as one thread-block cluster (shared-memory blocks)."""
     return int(lib().phx_last_eval_mode())
+
+
+def last_eval_variant() -> dict:
+    """The kernel variant of the last single-device evaluation."""
+    out = (C.c_int32 * 8)()
+    _check(lib().phx_last_eval_variant(out))
+    keys = ("Q", "V", "R", "dynamic_tail", "latency_mode", "short_batch", "grid", "block")
+    return dict(zip(keys, (int(x) for x in out)))
 
 
 def last_eval_stats():

@@ -133,6 +133,7 @@ int64_t g_trace_len = 0;
 double g_last_ms = 0.0;
 int64_t g_last_steps = 0;
 int32_t g_last_mode = 0;  // 0 grid-wide launch, 1 partitioned cooperative, 2 cluster
+int32_t g_last_variant[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // phx_last_eval_variant
 
 // One row part of a partitioned operator, resident on `dev`.
 struct PartDev {
@@ -1099,6 +1100,8 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
   {
     std::lock_guard<std::mutex> lk(g_trace_mu);
     g_last_mode = 0;
+    const int32_t var[8] = {a.QT, a.vec, a.R, a.dyn, a.lat, a.bsmall, grid, block};
+    std::memcpy(g_last_variant, var, sizeof var);
   }
   PHX_CUDA(cudaEventRecord(op->ev1, st));
   if (step_times) {
@@ -2040,6 +2043,13 @@ phx_status phx_block_series_direct(phx_op op, int32_t r, const double* t, const 
 int32_t phx_last_eval_mode(void) {
   std::lock_guard<std::mutex> lk(g_trace_mu);
   return g_last_mode;
+}
+
+phx_status phx_last_eval_variant(int32_t* out8) {
+  if (!out8) return PHX_EINVAL;
+  std::lock_guard<std::mutex> lk(g_trace_mu);
+  std::memcpy(out8, g_last_variant, sizeof g_last_variant);
+  return PHX_OK;
 }
 
 phx_status phx_last_eval_stats(double* kernel_ms, int64_t* steps) {

@@ -333,7 +333,7 @@ def test_block_width_limit():
         P_.phimv_block(op, P_.BlockPhiRequest(np.full(r, 0.1), np.ones(r), V, 1e-10, ss))
 
 
-@pytest.mark.parametrize("n,p,r", [(5003, 3, 4), (9001, 1, 4), (6007, 3, 8), (20011, 0, 6)])
+@pytest.mark.parametrize("n,p,r", [(10007, 3, 4), (12011, 1, 4), (6007, 3, 8), (20011, 0, 6)])
 def test_short_row_grid_kernel_bitwise(n, p, r):
     """Operators with 3-5 entries per row and more tiles than SMs: the static
     gather-batch-5 kernel with its lean S-term body (grid-stride warp tiles,
@@ -367,3 +367,6 @@ def test_short_row_grid_kernel_bitwise(n, p, r):
     assert res.stats.series_lens_F == ro.series_lens_F
     assert np.array_equal(res.W, Wo)
     assert P_.last_eval_mode() == 0
+    var = P_.last_eval_variant()
+    assert (var["Q"], var["V"], var["R"]) == (1, 2, 1)
+    assert (var["dynamic_tail"], var["latency_mode"], var["short_batch"]) == (0, 0, 1)
