@@ -370,3 +370,30 @@ def test_short_row_grid_kernel_bitwise(n, p, r):
     var = P_.last_eval_variant()
     assert (var["Q"], var["V"], var["R"]) == (1, 2, 1)
     assert (var["dynamic_tail"], var["latency_mode"], var["short_batch"]) == (0, 0, 1)
+
+
+@pytest.mark.parametrize("p,r,k", [(3, 4, 8), (4, 6, 7), (2, 3, 9), (7, 8, 4), (15, 8, 3),
+                                   (3, 8, 1), (0, 5, 6)])
+def test_grid_kernel_layouts_bitwise(p, r, k):
+    """The persistent grid kernel (not latency mode) for every lane layout:
+    Q = 1..8 column chunks, V = 1 / 2 columns per lane, R = 1 / 2 rows per lane
+    group, default and short gather batches, with recovery sweeps."""
+    P_ = P()
+    n = 40000
+    n_, rp, ci, av = _random_sparse(n, k, 300 + 13 * p + r + k)
+    av = av * 20.0
+    op = P_.CsrOperator(n_, rp, ci, av)
+    oop = O.csr_from_arrays(n_, rp, ci, av)
+    tol = 1e-10
+    ss = O.select_parameters(oop, 61, tol)
+    rng = O.Rng(77 + p + r)
+    V = rng.matrix(n_, p + 1)
+    t = (0.5 + rng.uniforms(r)) * (1.5 / ss.s)
+    alpha = -1.0 + 2.0 * rng.uniforms(r)
+    Wo, ro = O.phimv_block(oop, t, alpha, V, tol, ss)
+    res = P_.phimv_block(op, P_.BlockPhiRequest(t, alpha, V, tol, P_.ScalingShift(*ss.astuple())))
+    var = P_.last_eval_variant()
+    assert var["latency_mode"] == 0 and var["grid"] > 148
+    assert res.stats.series_len_S == ro.series_len_S
+    assert res.stats.series_lens_F == ro.series_lens_F
+    assert np.array_equal(res.W, Wo)
