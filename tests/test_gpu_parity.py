@@ -397,3 +397,24 @@ def test_grid_kernel_layouts_bitwise(p, r, k):
     assert res.stats.series_len_S == ro.series_len_S
     assert res.stats.series_lens_F == ro.series_lens_F
     assert np.array_equal(res.W, Wo)
+
+
+def test_single_variant_grid_kernel_bitwise():
+    """phimv (Alg. 2: exp_v0 and the phi tail beside w) through the persistent
+    grid kernel at n = 40,000, with recovery sweeps."""
+    P_ = P()
+    n, rp, ci, av = _random_sparse(40000, 5, 4711)
+    av = av * 20.0
+    op = P_.CsrOperator(n, rp, ci, av)
+    oop = O.csr_from_arrays(n, rp, ci, av)
+    tol = 1e-12
+    ss = O.select_parameters(oop, 61, tol)
+    V = O.Rng(12).matrix(n, 4)
+    t = 3.5 / ss.s
+    w, e0, tail, rec = O.phimv(oop, t, 0.75, V, tol, ss)
+    res = P_.phimv(op, P_.PhiRequest(t, 0.75, V, tol, P_.ScalingShift(*ss.astuple())))
+    assert rec.s_effective > 1
+    assert P_.last_eval_variant()["latency_mode"] == 0
+    assert res.stats.series_lens_F == rec.series_lens_F
+    assert np.array_equal(res.w, w)
+    assert np.array_equal(res.exp_v0, e0) and np.array_equal(res.tail, tail)
