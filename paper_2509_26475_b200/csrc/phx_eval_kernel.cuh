@@ -761,6 +761,11 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
     }
     __syncthreads();
   }
+  if (master && a.tstamp != nullptr && a.tstamp_cap > kCtaStampBase) {  // diagnostics: launch start
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    a.tstamp[kCtaStampBase - 1] = ns;
+  }
   // ================= init: Vw = V[src]*g, D = S = Vw (phi_block.cpp:76-92)
   // Vw_1, D_1 and S_1 are the same block; instead of writing it three times,
   // the init stores V row-major (stride p+1) into D0 and the first S term

@@ -1108,6 +1108,9 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
     std::vector<unsigned long long> ts(size_t(a.tstamp_cap));
     PHX_CUDA(cudaMemcpyAsync(ts.data(), a.tstamp, ts.size() * 8, cudaMemcpyDeviceToHost, st));
     PHX_CUDA(cudaStreamSynchronize(st));
+    if (ts[size_t(phx::kCtaStampBase - 1)] != 0 && ts[0] != 0)
+      std::fprintf(stderr, "[phx] launch start -> first step end (us): %.1f\n",
+                   double(ts[0] - ts[size_t(phx::kCtaStampBase - 1)]) * 1e-3);
     std::fprintf(stderr, "[phx] step durations (us):");
     for (size_t q = 1; q < ts.size() && ts[q] != 0 && q < 48; ++q)
       std::fprintf(stderr, " %.1f", double(ts[q] - ts[q - 1]) * 1e-3);
