@@ -52,7 +52,7 @@ cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStre
   int per_sm = 0;  // also sets the dynamic shared memory attribute of the variant
   const cudaError_t e = k.occ(block, &per_sm);
   if (e != cudaSuccess) return e;
-  return cudaLaunchCooperativeKernel(k.fn, grid, block, args, eval_pipe_bytes(), st);
+  return cudaLaunchCooperativeKernel(k.fn, grid, block, args, k.smem, st);
 }
 
 size_t eval_cluster_smem(int32_t cl_rows, int32_t cl_nnz, int32_t tile, int32_t ldb, int32_t ldf) {

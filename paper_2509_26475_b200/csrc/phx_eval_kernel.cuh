@@ -199,16 +199,22 @@ __device__ __forceinline__ void publish2(unsigned long long a, unsigned long lon
 // registers held), so the row_ptr -> entries -> gather dependency chain costs
 // one round trip per tile instead of three.
 // ---------------------------------------------------------------------------
-constexpr int kEC = 160;  // staged CSR entries per warp tile
+#ifndef PHX_LEAN
+#define PHX_LEAN 1
+#endif
+constexpr int kEC = 160;  // staged CSR entries per warp tile (default)
 
-struct WarpPipe {
+template <int EC_>
+struct WarpPipeT {
+  static constexpr int EC = EC_;  // staged CSR entries per warp tile
   int rp[3][kMaxRW + 1];
-  int ci[2][kEC];
-  double av[2][kEC];
+  int ci[2][EC];
+  double av[2][EC];
   // latency mode: slot 0 still holds this tile's row_ptr and entries (set
   // after a single-tile sequence -- the warp owns the same tile every step)
   int cached_base, cached_rw;
 };
+using WarpPipe = WarpPipeT<kEC>;
 
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -264,10 +270,11 @@ __device__ __forceinline__ void issue_rp(const BlockArgs& a, int* dst, int base,
   for (int l = lane; l <= RW; l += 32) cp_async4(dst + l, a.rp + min(base + l, a.n));
 }
 
+template <int EC>
 __device__ __forceinline__ void issue_entries(const BlockArgs& a, const int* rp, int RW, int* ci,
                                               double* av, int lane) {
   const int e_lo = rp[0], E = rp[RW] - e_lo;
-  if (E <= kEC)
+  if (E <= EC)
     for (int e = lane; e < E; e += 32) {
       cp_async4(ci + e, a.ci + e_lo + e);
       cp_async8(av + e, a.av + e_lo + e);
@@ -276,8 +283,8 @@ __device__ __forceinline__ void issue_entries(const BlockArgs& a, const int* rp,
 
 // body(base, rp, ci, av): rp = row_ptr[base .. base+RW] (clamped at n); when
 // rp[RW] - rp[0] <= kEC, ci/av hold the tile's entries from index 0.
-template <bool CACHE, class Seq, class Body>
-__device__ __forceinline__ void pipelined(const BlockArgs& a, Seq& ts, int RW, WarpPipe& pp,
+template <bool CACHE, class Seq, class Body, class Pipe>
+__device__ __forceinline__ void pipelined(const BlockArgs& a, Seq& ts, int RW, Pipe& pp,
                                           int lane, Body& body) {
   const int b0 = ts.at(0, lane);
   if (b0 < 0) return;  // warp-uniform
@@ -295,7 +302,7 @@ __device__ __forceinline__ void pipelined(const BlockArgs& a, Seq& ts, int RW, W
   cp_commit();
   cp_wait_all();
   __syncwarp();
-  issue_entries(a, pp.rp[0], RW, pp.ci[0], pp.av[0], lane);
+  issue_entries<Pipe::EC>(a, pp.rp[0], RW, pp.ci[0], pp.av[0], lane);
   if constexpr (!CACHE) b1 = ts.at(1, lane);
   if (b1 >= 0) issue_rp(a, pp.rp[1], b1, RW, lane);
   cp_commit();
@@ -311,7 +318,7 @@ __device__ __forceinline__ void pipelined(const BlockArgs& a, Seq& ts, int RW, W
     __syncwarp();  // tile s's entries and tile s+1's row_ptr have landed
     const int nb = ts.at(s + 1, lane);
     if (nb >= 0) {
-      issue_entries(a, pp.rp[(s + 1) % 3], RW, pp.ci[(s + 1) & 1], pp.av[(s + 1) & 1], lane);
+      issue_entries<Pipe::EC>(a, pp.rp[(s + 1) % 3], RW, pp.ci[(s + 1) & 1], pp.av[(s + 1) & 1], lane);
       const int nnb = ts.at(s + 2, lane);
       if (nnb >= 0) issue_rp(a, pp.rp[(s + 2) % 3], nnb, RW, lane);
     }
@@ -324,10 +331,10 @@ __device__ __forceinline__ void pipelined(const BlockArgs& a, Seq& ts, int RW, W
 
 // every warp tile of a phase: the static part, then the dynamic tail from
 // counter ctr (zeroed before the phase's step began)
-template <bool DYN, bool CL, bool CACHE, class Body>
+template <bool DYN, bool CL, bool CACHE, class Body, class Pipe>
 __device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, int ntiles,
                                           int warp, int cta, int ncta,
-                                          unsigned long long* ctr, WarpPipe& pp, int lane,
+                                          unsigned long long* ctr, Pipe& pp, int lane,
                                           const int* crp, const int* cci, const double* cav,
                                           Body&& body) {
   if constexpr (CL) {
@@ -464,7 +471,7 @@ __device__ __forceinline__ void gather(const BlockArgs& a, const int* ci, const 
   }
 }
 
-template <int Q, int V, int R, int B, bool PART, bool HINT = false>
+template <int Q, int V, int R, int B, bool PART, bool HINT = false, int EC = kEC>
 __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L, const int* rp,
                                             const int* ci, const double* av, unsigned ld,
                                             const double* X, const double* const* Xt,
@@ -478,7 +485,7 @@ __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L,
     rs[rr] = rp[li] - e_lo;
     cnt[rr] = rp[li + 1] - rp[li];
   }
-  if (rp[L.RW] - e_lo <= kEC)
+  if (rp[L.RW] - e_lo <= EC)
     gather<Q, V, R, B, true, PART, HINT>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
   else
     gather<Q, V, R, B, false, PART, HINT>(a, ci, av, e_lo, ld, rs, cnt, X, Xt, cq, vq, acc);
@@ -487,6 +494,16 @@ __device__ __forceinline__ void gather_tile(const BlockArgs& a, const Layout& L,
 // dynamic shared memory: the per-warp pipes, then (cluster mode) the part's
 // blocks Vw, D0, D1, S (cl_rows x ldb each) and F0, F1, E (cl_rows x ldf)
 constexpr size_t kPipeBytes = (size_t(kWarps) * sizeof(WarpPipe) + 15) / 16 * 16;
+// the lean-body variant (C2's: (1,2,1), batch 5, static) stages few entries
+// per tile (<= 40 for 5-entry rows), so its pipes are smaller and the L1
+// that its gathers hit larger
+template <int Q, int V, int RR, bool PART, bool DYN, int BO, bool CL, bool LAT>
+struct PipeCfg {
+  static constexpr bool lean =
+      PHX_LEAN && !CL && !LAT && !PART && !DYN && Q == 1 && V == 2 && RR == 1 && BO == 5;
+  static constexpr int EC = lean ? 48 : kEC;
+  static constexpr size_t bytes = (size_t(kWarps) * sizeof(WarpPipeT<EC>) + 15) / 16 * 16;
+};
 
 // CL (cluster mode, implies PART): the launch is ONE thread-block cluster,
 // one CTA per part; every part's blocks live in its CTA's shared memory, the
@@ -505,15 +522,14 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   // hinted load form costs the short-row kernels (C2, C5) even at fraction 0,
   // and cluster mode gathers shared memory
   constexpr bool HINT = !CL && DYN && BO == 0 && Q == 1 && V == 2 && RR == 1;
-#ifndef PHX_LEAN
-#define PHX_LEAN 1
-#endif
-  constexpr bool LEAN = PHX_LEAN && !CL && !LAT && !PART && !DYN && Q == 1 && V == 2 && RR == 1 && BO == 5;
+  constexpr bool LEAN = PipeCfg<Q, V, RR, PART, DYN, BO, CL, LAT>::lean;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long red[2][kWarps];
   // per-warp pipeline buffers: dynamic shared memory (kWarps * sizeof(WarpPipe))
   extern __shared__ __align__(16) unsigned char pipe_smem[];
-  WarpPipe* pipe = reinterpret_cast<WarpPipe*>(pipe_smem);
+  using Pipe = WarpPipeT<PipeCfg<Q, V, RR, PART, DYN, BO, CL, LAT>::EC>;
+  constexpr int EC = Pipe::EC;
+  Pipe* pipe = reinterpret_cast<Pipe*>(pipe_smem);
   // gather tables [D0, D1, S, F0, F1][part] (PART only)
   __shared__ const double* gtab[5][PART ? kMaxParts : 1];
   __shared__ double gmax[2];
@@ -524,7 +540,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   __shared__ unsigned long long cl_box[2][CL ? kMaxParts : 1][2];  // CL: all parts', by step parity
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpPipe& pp = pipe[warp];
+  Pipe& pp = pipe[warp];
   if (LAT) {
     if (lane == 0) pp.cached_base = -1;
     __syncwarp();
@@ -899,7 +915,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
                          crp, cci, cav,
                 [&](int base, const int* rp, const int* ci, const double* avs) {
           const int e_lo = rp[0];
-          const bool sm = rp[LS.RW] - e_lo <= kEC;
+          const bool sm = rp[LS.RW] - e_lo <= EC;
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) {
             const int row = base + rr * LS.gpw + LS.g;
@@ -1090,7 +1106,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
           }
           };
           if constexpr (!Cfg<Q, V, RR>::LATE) streams();
-          gather_tile<Q, V, R, B, PART, HINT>(a, LS, rp, ci, avs, ldb, Dc, gtab[dpar], c, v, acc);
+          gather_tile<Q, V, R, B, PART, HINT, EC>(a, LS, rp, ci, avs, ldb, Dc, gtab[dpar], c, v, acc);
           if constexpr (Cfg<Q, V, RR>::LATE) streams();
           double vn[R][Q][V], dn[R][Q][V], sn[R][Q][V];
 #pragma unroll
@@ -1271,7 +1287,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
         // gathers S block-0 columns (left F columns live at the same column
         // index in S); a pair straddling the left/right split gathers one
         // extra column, unused
-        gather_tile<Q, V, R, B, PART, HINT>(a, LF, rp, ci, avs, ldb, a.S, gtab[2], c, vl, acc);
+        gather_tile<Q, V, R, B, PART, HINT, EC>(a, LF, rp, ci, avs, ldb, a.S, gtab[2], c, vl, acc);
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
           const int row = base + rr * LF.gpw + LF.g;
@@ -1435,7 +1451,7 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
               }
             };
             if constexpr (!Cfg<Q, V, RR>::LATE) streams();
-            gather_tile<Q, V, R, B, PART, HINT>(a, LF, rp, ci, avs, ldf, Fc, gtab[3 + fpar], c, v, acc);
+            gather_tile<Q, V, R, B, PART, HINT, EC>(a, LF, rp, ci, avs, ldf, Fc, gtab[3 + fpar], c, v, acc);
             if constexpr (Cfg<Q, V, RR>::LATE) streams();
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
@@ -1617,10 +1633,12 @@ cudaError_t eval_occupancy(int block, int* per_sm) {
     }
   }
   e = cudaFuncSetAttribute(k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPipeBytes));
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(PipeCfg<Q, V, R, PART, DYN, BO, CL, LAT>::bytes));
   if (e != cudaSuccess) return e;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      per_sm, k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>, block, kPipeBytes);
+      per_sm, k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>, block,
+      PipeCfg<Q, V, R, PART, DYN, BO, CL, LAT>::bytes);
   if (e == cudaSuccess && cacheable)
     cache[dev].store((static_cast<long long>(block) << 32) | (*per_sm + 1),
                      std::memory_order_relaxed);
@@ -1631,7 +1649,7 @@ template <int Q, int V, int R, bool PART, bool DYN, int BO = 0, bool CL = false,
 EvalKernel eval_kernel() {
   return EvalKernel{
       reinterpret_cast<const void*>(k_phimv_block<Q, V, R, PART, DYN, BO, CL, LAT>),
-      eval_occupancy<Q, V, R, PART, DYN, BO, CL, LAT>};
+      eval_occupancy<Q, V, R, PART, DYN, BO, CL, LAT>, PipeCfg<Q, V, R, PART, DYN, BO, CL, LAT>::bytes};
 }
 
 // cluster-mode variants exist for single-chunk rows (Q == 1) only
@@ -1640,7 +1658,7 @@ EvalKernel eval_kernel_cluster() {
   if constexpr (Q == 1)
     return eval_kernel<Q, V, R, true, false, BO, true>();
   else
-    return EvalKernel{nullptr, nullptr};
+    return EvalKernel{nullptr, nullptr, 0};
 }
 
 }  // namespace

@@ -137,6 +137,7 @@ cudaError_t coop_grid_size(int QT, int V, int R, bool part, bool dyn, bool small
 struct EvalKernel {
   const void* fn;
   cudaError_t (*occ)(int block, int* per_sm);
+  size_t smem;  // dynamic shared memory per CTA (the variant's pipes)
 };
 // per-file variant tables (phx_eval_q*.cu): true when the file holds the
 // variant (QT, V, R, partitioned, dynamic tail, short gather batch)
