@@ -501,7 +501,10 @@ template <int Q, int V, int RR, bool PART, bool DYN, int BO, bool CL, bool LAT>
 struct PipeCfg {
   static constexpr bool lean =
       PHX_LEAN && !CL && !LAT && !PART && !DYN && Q == 1 && V == 2 && RR == 1 && BO == 5;
-  static constexpr int EC = lean ? 48 : kEC;
+  // the 2-entry-row batch variant ((1,2,2), batch 2: C5's bidiagonal rows)
+  // stages at most 2 entries per row of an 8-row tile
+  static constexpr bool two = !CL && Q == 1 && V == 2 && RR == 2 && BO == 2;
+  static constexpr int EC = lean ? 48 : (two ? 32 : kEC);
   static constexpr size_t bytes = (size_t(kWarps) * sizeof(WarpPipeT<EC>) + 15) / 16 * 16;
 };
 
