@@ -15,6 +15,12 @@
 // order (oracle/phx_oracle.cpp).  Row sums use the canonical
 // pairwise tree over pow2-padded natural column order: with V = 2 the
 // lane-local pair is the tree's first level, the butterfly the next ones.
+//
+// Tiles reach a phase body through a per-warp cp.async pipeline of their CSR
+// slices (pipelined / run_tiles), sized per variant (PipeCfg).  C2's variant
+// ((1,2,1), gather batch 5, static) runs its S terms through a lean body
+// instead: grid-stride warp tiles, CSR read directly, column coefficients
+// from a shared table.
 #include <cooperative_groups.h>
 
 #include <atomic>
