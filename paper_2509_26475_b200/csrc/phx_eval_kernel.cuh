@@ -802,37 +802,70 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
     unsigned c[Q];
     bool v[Q];
     cols(LS, c, v);
-    for (int t = cta; t < ntiles; t += ncta)
-      for (int wt = warp; wt < a.tile / LS.RW; wt += kWarps) {
-        const int base = t * a.tile + wt * LS.RW;
+    // the lane's source column of V and its g_i, per column
+    int srcv[Q][V];
+    double gv[Q][V];
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const int cc = int(c[q]) + e;
+        const int j = cc / r, i = cc - j * r;
+        srcv[q][e] = j == 0 ? 0 : p + 1 - j;
+        gv[q][e] = v[q] ? __ldg(a.g + i) : 0.0;
+      }
+    // NB warp tiles per round with their V loads in flight together: the
+    // pass is one dependent load per tile otherwise, latency-bound
+    constexpr int NB = (Q * V * R <= 4) ? 4 : 1;
+    const int mwt = a.tile / (LS.RW * kWarps);  // warp tiles per CTA tile (power of two)
+    auto tile_base = [&](int k) -> int {        // this warp's k-th warp tile, -1 past the end
+      const int t = cta + (k / mwt) * ncta;
+      return t < ntiles ? t * a.tile + (warp + (k % mwt) * kWarps) * LS.RW : -1;
+    };
+    for (int k0 = 0; tile_base(k0) >= 0; k0 += NB) {
+      double vr[NB][R][Q][V];
+      int rowb[NB][R];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int base = tile_base(k0 + b);
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
           const int row = base + rr * LS.gpw + LS.g;
-          const bool rv = row < n;
-          double x[Q][V], ax[Q][V];
+          rowb[b][rr] = (base >= 0 && row < n) ? row : -1;
 #pragma unroll
-          for (int q = 0; q < Q; ++q) {
+          for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+              vr[b][rr][q][e] = (rowb[b][rr] >= 0 && v[q])
+                                    ? __ldg(a.V + size_t(srcv[q][e]) * size_t(n) + row)
+                                    : 0.0;
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const int row = rowb[b][rr];
+          const bool rv = row >= 0;
+          double ax[Q][V];
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
 #pragma unroll
             for (int e = 0; e < V; ++e) {
-              x[q][e] = 0.0;
+              double x = 0.0;
               if (rv && v[q]) {
-                const int cc = int(c[q]) + e;
-                const int j = cc / r, i = cc - j * r;
-                const int src = j == 0 ? 0 : p + 1 - j;
-                const double vraw = __ldg(a.V + size_t(src) * size_t(n) + row);
-                mv = umax64(mv, abs_bits(vraw));
-                x[q][e] = vraw * __ldg(a.g + i);
+                mv = umax64(mv, abs_bits(vr[b][rr][q][e]));
+                x = vr[b][rr][q][e] * gv[q][e];
               }
-              ax[q][e] = fabs(x[q][e]);
+              ax[q][e] = fabs(x);
             }
-          }
           if (rv)  // the row's V entries, row-major, into D0
             for (int col = LS.lg; col < p1; col += LS.G)
               a.D0[size_t(row) * size_t(p1) + col] = __ldg(a.V + size_t(col) * size_t(n) + row);
           const double rsum = group_rowsum<Q, V>(ax, LS.G, LS.qp);
           if (rv) m0 = umax64(m0, abs_bits(rsum));
         }
-      }
+    }
   }
   double mD, mSn;
   sync_step(m0, mv, mD, mSn);
