@@ -395,6 +395,7 @@ __device__ __forceinline__ void run_tiles(const BlockArgs& a, const Layout& L, i
 // per part: peer-GPU memory in a multi-GPU run).
 constexpr unsigned kOwnerShift = 27;
 constexpr unsigned kLocalMask = (1u << kOwnerShift) - 1u;
+constexpr unsigned kLocalOwner = 31u;  // owner field of a part's own rows (host: phx_host.cpp)
 
 // gather loads carry an L2 cache policy: evict_last for the fraction
 // a.gather_keep of lines -- 1 for operators whose gather reuse distance is
@@ -422,7 +423,12 @@ template <bool PART>
 __device__ __forceinline__ const double* gather_row_ptr(const double* X,
                                                         const double* const* Xt, unsigned enc,
                                                         unsigned ld) {
-  if (PART) return Xt[enc >> kOwnerShift] + size_t(enc & kLocalMask) * ld;
+  if (PART) {
+    // owner kLocalOwner: a row of this part (X, no table lookup on the
+    // dependent gather chain); else the owning part's buffer
+    const unsigned ow = enc >> kOwnerShift;
+    return (ow == kLocalOwner ? X : Xt[ow]) + size_t(enc & kLocalMask) * ld;
+  }
   return X + enc * ld;
 }
 
@@ -559,8 +565,10 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   // plo .. plo+pcount-1, CTAs split evenly; a CTA rebinds the row-local
   // fields of its part (rows are part-local from here on).
   // (unpartitioned: `a` aliases the kernel parameter, read from the constant
-  // bank; partitioned: a local copy with the part's fields)
+  // bank; partitioned: the part's copy in shared memory)
   BlockArgs pa;
+  __shared__ __align__(16) unsigned char s_pa_raw[PART ? sizeof(BlockArgs) : 16];
+  BlockArgs* const s_pa = reinterpret_cast<BlockArgs*>(s_pa_raw);
   const int* crp = nullptr;  // cluster mode: the part's CSR in shared memory
   const int* cci = nullptr;
   const double* cav = nullptr;
@@ -631,9 +639,12 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
         gtab[4][q] = U.F1;
       }
     }
+    if (threadIdx.x == 0) *s_pa = pa;
     __syncthreads();
   }
-  const BlockArgs& a = PART ? pa : ga;
+  // partitioned: the part's arguments from shared memory (a per-thread copy
+  // would live in local memory, one L1 round trip per field on every use)
+  const BlockArgs& a = PART ? *s_pa : ga;
   int dpar = 0, fpar = 0;  // D / F ping-pong parity (all parts swap in lockstep)
 
   const int n = a.n, r = a.r, p = a.p;

@@ -1354,7 +1354,10 @@ phx_status phx_op_create_csr_partitioned(int64_t n, const int64_t* row_ptr,
         for (int64_t e = e0; e < e1; ++e) {
           const int64_t col = col_idx[e];
           const int owner = int(std::upper_bound(bnd.begin(), bnd.end(), col) - bnd.begin()) - 1;
-          ci[size_t(e - e0)] = int32_t((uint32_t(owner) << 27) | uint32_t(col - bnd[size_t(owner)]));
+          // the part's own rows carry owner 31 (the kernel's kLocalOwner):
+          // gathered from the part's buffers without a part-table lookup
+          const uint32_t tag = owner == q ? 31u : uint32_t(owner);
+          ci[size_t(e - e0)] = int32_t((tag << 27) | uint32_t(col - bnd[size_t(owner)]));
         }
         DeviceGuard guard(d.dev);
         PHX_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
