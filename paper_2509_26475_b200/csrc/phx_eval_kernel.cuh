@@ -567,7 +567,8 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
   // (unpartitioned: `a` aliases the kernel parameter, read from the constant
   // bank; partitioned: the part's copy in shared memory)
   BlockArgs pa;
-  __shared__ __align__(16) unsigned char s_pa_raw[PART ? sizeof(BlockArgs) : 16];
+  constexpr bool SPA = PART && BO == 0;
+  __shared__ __align__(16) unsigned char s_pa_raw[SPA ? sizeof(BlockArgs) : 16];
   BlockArgs* const s_pa = reinterpret_cast<BlockArgs*>(s_pa_raw);
   const int* crp = nullptr;  // cluster mode: the part's CSR in shared memory
   const int* cci = nullptr;
@@ -639,12 +640,14 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv
         gtab[4][q] = U.F1;
       }
     }
-    if (threadIdx.x == 0) *s_pa = pa;
+    if (SPA && threadIdx.x == 0) *s_pa = pa;
     __syncthreads();
   }
-  // partitioned: the part's arguments from shared memory (a per-thread copy
-  // would live in local memory, one L1 round trip per field on every use)
-  const BlockArgs& a = PART ? *s_pa : ga;
+  // partitioned: the part's arguments from shared memory for the default-batch
+  // variants (C3's: the per-thread copy lives in local memory there, 463 ->
+  // 435 ms at 2 parts), the per-thread copy for the short-batch ones (C2's:
+  // 6.1 -> 7.6 ms from shared memory) -- same-box A/B, DESIGN.md §7
+  const BlockArgs& a = SPA ? *s_pa : (PART ? pa : ga);
   int dpar = 0, fpar = 0;  // D / F ping-pong parity (all parts swap in lockstep)
 
   const int n = a.n, r = a.r, p = a.p;
