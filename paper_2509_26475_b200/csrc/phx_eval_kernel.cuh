@@ -529,7 +529,13 @@ struct PipeCfg {
 // for operators with fewer tiles than SMs, whose steps are latency-bound:
 // the gather's loads batch instead of serialising at 64 registers
 template <int Q, int V, int RR, bool PART, bool DYN, int BO, bool CL, bool LAT = false>
-__global__ void __launch_bounds__(kBlock, LAT ? 1 : Cfg<Q, V, RR>::MINB) k_phimv_block(BlockArgs ga) {
+// register budget: the default-batch partitioned variants (C3's) at 3 CTAs/SM
+// (80 registers: their part tables spill heavily at 64 -- C3 at 2 parts
+// 436 -> 393 ms, same-box A/B)
+__global__ void __launch_bounds__(kBlock, LAT ? 1
+                                           : ((PART && !CL && BO == 0 && Cfg<Q, V, RR>::MINB > 3)
+                                                  ? 3
+                                                  : Cfg<Q, V, RR>::MINB)) k_phimv_block(BlockArgs ga) {
   constexpr int R = Cfg<Q, V, RR>::R;
   constexpr int B = BO > 0 ? BO : Cfg<Q, V, RR>::B;  // gather batch
   // L2 cache-policy gathers (a.gather_keep): the dynamic-tail (1, 2, 1)
