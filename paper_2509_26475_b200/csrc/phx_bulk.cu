@@ -1,0 +1,924 @@
+// The bulk-copy persistent phimv_block kernel (phi_block.cpp:48-157, Alg. 3)
+// for large operators, sm_100a.
+//
+// Same algorithm, operation order and stopping logic as k_phimv_block
+// (phx_eval_kernel.cuh; bit-for-bit the oracle), but the two phases that carry
+// almost all of the traffic -- the S-series terms (phi_block.cpp:93-106) and
+// the recovery terms (:124-139) -- run as a warp-specialised TMA-engine
+// pipeline instead of register gathers:
+//
+//   * one PRODUCER warp per CTA grabs tiles of kPlanT rows dynamically (batches
+//     of 4 positions from the step's counter, so all CTAs sweep the rows
+//     together and the gathers' L2 reuse window stays small) and, from the
+//     operator's tile plan (phx_plan.cpp), issues cp.async.bulk copies of
+//     every contiguous range the tile needs -- its row_ptr / slot / value
+//     slices, the gather window, the offset groups, single rows, and the
+//     row-local accumulator tiles -- into a ring of shared-memory stages,
+//     completing on an mbarrier (complete_tx);
+//   * eight CONSUMER warps wait on the stage's barrier, accumulate every row's
+//     entries in CSR order from shared memory (one-byte slots), run the same
+//     fused epilogue (J-term, shift, scaling, D' / S' or F' / E', |.| row
+//     sums) and stream the results to HBM with evict-first stores, then release
+//     the stage.
+//
+// Nothing a consumer reads comes from global memory, so memory-level
+// parallelism no longer depends on registers: C3's S term went from 0.47 of
+// the HBM roofline (register gathers) to 0.73 in the microbenchmark
+// (tools/microbench_c3.cu, profiles/r2_microbench_c3.jsonl).  The remaining
+// phases (init, the peeled first S term, promotion, sweep end, exact norm
+// passes: a few percent of the traffic) run as plain grid-stride loops.
+//
+// Compiled with --fmad=false: each multiply and add rounds separately.
+#include <cooperative_groups.h>
+
+#include "phx_eval_kernel.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace phx {
+namespace {
+
+constexpr int kBW = kBulkConsumers + 1;  // warps per CTA
+constexpr int kProd = kBulkConsumers;    // the producer warp
+constexpr int kPB = 4;                   // tile positions per counter grab
+
+__device__ __forceinline__ unsigned su32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx)
+               : "memory");
+}
+// global -> shared bulk copy (TMA engine), completion counted on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// CTA max of two bit patterns (kBW warps) -> one atomicMax each into the slot
+__device__ __forceinline__ void publish_b(unsigned long long a, unsigned long long b,
+                                          unsigned long long* slot,
+                                          unsigned long long (*red)[kBW]) {
+  for (int m = 16; m >= 1; m >>= 1) {
+    a = umax64(a, __shfl_xor_sync(kFull, a, m));
+    b = umax64(b, __shfl_xor_sync(kFull, b, m));
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = a;
+    red[1][warp] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ma = 0, mb = 0;
+    for (int q = 0; q < kBW; ++q) {
+      ma = umax64(ma, red[0][q]);
+      mb = umax64(mb, red[1][q]);
+    }
+    atomicMax(slot, ma);
+    atomicMax(slot + 1, mb);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
+  const BlockArgs& a = ga;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ unsigned long long bar_full[kBulkMaxStages], bar_empty[kBulkMaxStages];
+  __shared__ unsigned long long red[2][kBW];
+  __shared__ __align__(16) int pdesc[2][kPB][kPlanDesc];  // producer: descriptor batches
+  const double INF = __longlong_as_double(0x7FF0000000000000ll);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cta = int(blockIdx.x), ncta = int(gridDim.x);
+  const int NS = a.bulk_ns, SB = a.bulk_stage_bytes;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], kBulkConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int n = a.n, r = a.r, p = a.p, p1 = p + 1;
+  const int w = a.w, fc = a.fcols;
+  const unsigned ldb = unsigned(a.ldb), ldf = unsigned(a.ldf);
+  const bool has_xi = a.xi != 0.0;
+  const bool master = blockIdx.x == 0 && threadIdx.x == 0;
+  const int nblk = (n + kPlanT - 1) / kPlanT;  // row blocks = plan tiles
+  int kpipe = 0;                               // ring stages used so far (producer == consumers)
+  int step = 0, tr_len = 0;
+
+  auto trace = [&](double kind, double x, double y) {
+    if (master && a.trace != nullptr && tr_len + 3 <= a.trace_cap) {
+      a.trace[tr_len] = kind;
+      a.trace[tr_len + 1] = x;
+      a.trace[tr_len + 2] = y;
+    }
+    tr_len += 3;
+  };
+  auto sync_step = [&](unsigned long long ma, unsigned long long mb, double& ra, double& rb) {
+    unsigned long long* slot = a.slots + 4 * (step % 3);
+    publish_b(ma, mb, slot, red);
+    if (master) {
+      unsigned long long* nxt = a.slots + 4 * ((step + 1) % 3);
+      nxt[0] = 0ull;
+      nxt[1] = 0ull;
+      nxt[2] = 0ull;  // the next step's tile counter
+    }
+    grid.sync();
+    if (master && a.tstamp != nullptr && step < a.tstamp_cap) {
+      unsigned long long ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      a.tstamp[step] = ns;
+    }
+    ra = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot)));
+    rb = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot + 1)));
+    ++step;
+  };
+  auto finish = [&](int err, int idx, int L_S, int extra_steps) {
+    if (master) {
+      a.status[0] = err;
+      a.status[1] = idx;
+      a.status[2] = L_S;
+      a.status[3] = 0;
+      a.status[4] = step + extra_steps;
+      a.status[5] = min(tr_len, a.trace_cap);
+    }
+  };
+  // plain phases: row blocks of kPlanT rows round-robin over the CTAs (the
+  // same block -> CTA map in every plain phase), lane groups of G lanes over
+  // the rows of a block; body(row, valid, lg) is called warp-uniformly
+  auto plain_rows = [&](int G, auto&& body) {
+    const int gpw = 32 / G, g = lane / G, lg = lane % G;
+    for (int blk = cta; blk < nblk; blk += ncta)
+      for (int r0 = warp * gpw; r0 < kPlanT; r0 += kBW * gpw) {
+        const int row = blk * kPlanT + r0 + g;
+        body(row, row < n, lg);
+      }
+  };
+  const int GS = a.GS, GF = a.GF;
+
+  // ================= the bulk phases: S term (kind 0) / recovery term (kind 1)
+  // X: gather source (width `width`), A: stream A (Vw | E), B: stream B (S)
+  auto bulk_phase = [&](int kind, int width, const double* X, const double* A, const double* B,
+                        auto&& epi) -> unsigned long long {
+    const BulkStage L = bulk_stage(a.plan_rows, a.plan_emax, width, B != nullptr);
+    unsigned long long* ctr = a.slots + 4 * (step % 3) + 2;
+    unsigned long long mx = 0;
+    if (warp == kProd) {
+      // Batches of kPB tile positions from the step's counter.  The atomic
+      // for a batch is issued one batch ahead; its descriptors are copied
+      // (cp.async, 16 lanes x 16 B) into pdesc[nxt] while the current batch
+      // is issued, so neither latency is on the producer's path.
+      unsigned long long pfirst = 0, plast = 0;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pfirst));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(plast));
+      auto fetch = [&](int pos, int buf) {
+        const int q = pos + (lane >> 2);
+        if (lane < 4 * kPB && q < nblk)
+          cp_async16(&pdesc[buf][lane >> 2][4 * (lane & 3)],
+                     a.plan_desc + size_t(q) * kPlanDesc + 4 * (lane & 3));
+        cp_commit();
+      };
+      unsigned long long pa_ = 0, pb_ = 0;
+      if (lane == 0) pa_ = atomicAdd(ctr, (unsigned long long)kPB);
+      int posA = int(__shfl_sync(kFull, pa_, 0));
+      fetch(posA, 0);
+      if (lane == 0) pb_ = atomicAdd(ctr, (unsigned long long)kPB);
+      int cur = 0;
+      for (bool more = true; more;) {
+        const int posB = int(__shfl_sync(kFull, pb_, 0));
+        fetch(posB, cur ^ 1);
+        if (lane == 0) pb_ = atomicAdd(ctr, (unsigned long long)kPB);  // used a batch later
+        cp_wait_1();
+        __syncwarp();
+#pragma unroll 1
+        for (int j = 0; j < kPB; ++j) {
+          const int t = posA + j < nblk ? posA + j : -1;
+          const int* d = pdesc[cur][j];
+          const int s = kpipe % NS;
+          mbar_wait(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
+          unsigned char* st = ring + size_t(s) * size_t(SB);
+          unsigned long long* bf = &bar_full[s];
+          const int nsgl = t >= 0 ? d[1] : 0;
+          if (lane == 0) {
+            *reinterpret_cast<int*>(st + L.hdr) = t;
+            if (t < 0) {
+              mbar_arrive(bf);  // end of the phase: the consumers leave
+            } else {
+              const int base = t * kPlanT, rows = min(kPlanT, n - base);
+              const int ng = d[0];
+              const int e_lo = d[3], e_hi = d[4];
+              const int wlo = max(base - 1, 0), whi = min(base + rows + 1, n);
+              const int c0 = e_lo & ~15, cn = (e_hi - c0 + 15) & ~15;  // slot bytes
+              const int a0 = e_lo & ~1, an = (e_hi - a0 + 1) & ~1;    // values (16 B granules)
+              const int rn = (rows + 1 + 3) & ~3;                     // row_ptr entries
+              unsigned nrow = unsigned(whi - wlo + nsgl + (B ? 2 : 1) * rows);
+              for (int g = 0; g < ng; ++g) nrow += unsigned(d[12 + g] & 0xffff);
+              const unsigned rb = unsigned(width) * 8u;
+              mbar_arrive_tx(bf, unsigned(rn * 4 + cn + an * 8) + nrow * rb);
+              bulk_g2s(st + L.rp, a.rp + base, unsigned(rn) * 4u, bf, pfirst);
+              if (cn) bulk_g2s(st + L.sl, a.plan_slot + c0, unsigned(cn), bf, pfirst);
+              if (an) bulk_g2s(st + L.av, a.av + a0, unsigned(an) * 8u, bf, pfirst);
+              bulk_g2s(st + L.dr, X + size_t(wlo) * width, unsigned(whi - wlo) * rb, bf, plast);
+              for (int g = 0; g < ng; ++g) {
+                const int cnt = d[12 + g] & 0xffff, dst = d[12 + g] >> 16;
+                bulk_g2s(st + L.dr + dst * int(rb), X + size_t(d[8 + g]) * width, unsigned(cnt) * rb,
+                         bf, plast);
+              }
+              bulk_g2s(st + L.sa, A + size_t(base) * width, unsigned(rows) * rb, bf, pfirst);
+              if (B) bulk_g2s(st + L.sb, B + size_t(base) * width, unsigned(rows) * rb, bf, pfirst);
+            }
+          }
+          if (t >= 0 && lane < nsgl) {  // single rows, one lane each
+            const int col = __ldg(a.plan_sgl + d[2] + lane);
+            bulk_g2s(st + L.dr + (kPlanT + 2 + lane) * width * 8, X + size_t(col) * width,
+                     unsigned(width) * 8u, bf, plast);
+          }
+          __syncwarp();
+          ++kpipe;
+          if (t < 0) {
+            more = false;
+            break;
+          }
+        }
+        posA = posB;
+        cur ^= 1;
+      }
+      cp_wait_all();  // the last prefetch (positions past the end) drains
+      __syncwarp();
+      return mx;
+    }
+    // ---- consumers
+    const int G = kind == 0 ? GS : GF;
+    const int gpw = 32 / G, g = lane / G, lg = lane % G;
+    const int c = 2 * lg;
+    const bool cv = c < width;
+    for (;;) {
+      const int s = kpipe % NS;
+      mbar_wait(&bar_full[s], (kpipe / NS) & 1);
+      const unsigned char* st = ring + size_t(s) * size_t(SB);
+      const int t = *reinterpret_cast<const int*>(st + L.hdr);
+      ++kpipe;
+      if (t >= 0) {
+        const int* rps = reinterpret_cast<const int*>(st + L.rp);
+        const double* dr = reinterpret_cast<const double*>(st + L.dr);
+        const double* sa = reinterpret_cast<const double*>(st + L.sa);
+        const double* sb = reinterpret_cast<const double*>(st + L.sb);
+        const int e_lo = rps[0];
+        const unsigned char* sls = st + L.sl + (e_lo & 15);
+        const double* avs = reinterpret_cast<const double*>(st + L.av) + (e_lo & 1);
+        const int base = t * kPlanT, rows = min(kPlanT, n - base);
+        const int wlo = max(base - 1, 0);
+        for (int r0 = warp * gpw; r0 < rows; r0 += kBulkConsumers * gpw) {
+          const int rr = r0 + g;
+          const bool v = rr < rows && cv;
+          double a0 = 0.0, a1 = 0.0;
+          if (v) {
+            const int e0 = rps[rr] - e_lo, e1 = rps[rr + 1] - e_lo;
+            for (int e = e0; e < e1; ++e) {
+              const double2 x = *reinterpret_cast<const double2*>(dr + int(sls[e]) * width + c);
+              const double av = avs[e];
+              a0 = a0 + av * x.x;
+              a1 = a1 + av * x.y;
+            }
+          }
+          const double* self = dr + (base + rr - wlo) * width + c;  // the row itself (window)
+          const unsigned long long m =
+              epi(v, rr < rows, base + rr, c, a0, a1, self, sa + rr * width + c, sb + rr * width + c, lg, G);
+          mx = umax64(mx, m);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_empty[s]);
+      if (t < 0) break;
+    }
+    return mx;
+  };
+
+  // ================= init: row-major V into D0, ||Vw_1||, max|V| (phi_block.cpp:76-92)
+  unsigned long long m0 = 0, mv = 0;
+  {
+    const int c = 2 * (lane % GS);
+    int src[2];
+    double gv[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int cc = c + e;
+      const int j = cc / r, i = cc - j * r;
+      src[e] = j == 0 ? 0 : p + 1 - j;
+      gv[e] = cc < w ? __ldg(a.g + i) : 0.0;
+    }
+    plain_rows(GS, [&](int row, bool rv, int lg) {
+      double ax[1][2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double x = 0.0;
+        if (rv && c + e < w) {
+          const double vv = __ldg(a.V + size_t(src[e]) * size_t(n) + row);
+          mv = umax64(mv, abs_bits(vv));
+          x = vv * gv[e];
+        }
+        ax[0][e] = fabs(x);
+      }
+      if (rv)
+        for (int col = lg; col < p1; col += GS)
+          a.D0[size_t(row) * size_t(p1) + col] = __ldg(a.V + size_t(col) * size_t(n) + row);
+      const double rsum = group_rowsum<1, 2>(ax, GS, 1);
+      if (rv) m0 = umax64(m0, abs_bits(rsum));
+    });
+  }
+  double mD, mSn;
+  sync_step(m0, mv, mD, mSn);
+  if (!(mSn <= DBL_MAX_D)) {  // a non-finite entry of V (check_request, phi_block.cpp:25-26)
+    finish(kStInputNonFinite, 0, 1, 0);
+    return;
+  }
+  double c1 = INF, c2 = mD, nS = mD;
+  trace(0.0, c2, nS);
+
+  // exact ||S||_inf (canonical row sums) for an inconclusive stopping test
+  // (see k_phimv_block: the bounds nSl <= ||S|| <= nSu decide every other term)
+  auto s_norm_exact = [&]() -> double {
+    unsigned long long m = 0;
+    const int c = 2 * (lane % GS);
+    plain_rows(GS, [&](int row, bool rv, int) {
+      double as[1][2] = {{0.0, 0.0}};
+      if (rv && c < w) {
+        const double2 x = *reinterpret_cast<const double2*>(a.S + (unsigned(row) * ldb + c));
+        as[0][0] = fabs(x.x);
+        as[0][1] = fabs(x.y);
+      }
+      const double rs = group_rowsum<1, 2>(as, GS, 1);
+      if (rv) m = umax64(m, abs_bits(rs));
+    });
+    double mx, dmy;
+    sync_step(m, m, mx, dmy);
+    return mx;
+  };
+  const bool exact_every_term = a.trace != nullptr;
+  double nSl = nS, nSu = nS;
+  bool exact = true;
+
+  // ================= S series (phi_block.cpp:93-106)
+  int k = 1;
+  double sigma = 1.0;
+  double* Dc = a.D0;
+  double* Dn = a.D1;
+  int err = kStOk, err_idx = 0;
+  if (c1 + c2 > a.tol * nS) {
+    // the first term (k = 2), peeled: D_1 = Vw_1 = S_1 = fl(V[src] * g) from
+    // the row-major V in D0; the gathered V rows are loaded a batch at a time
+    ++k;
+    c1 = c2;
+    sigma *= k;
+    unsigned long long mdb = 0;
+    {
+      const int c = 2 * (lane % GS);
+      int src[2], srcl[2], jj[2];
+      double gg[2], kd[2], ka[2], tos[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = c + e;
+        const bool ok = cc < w;
+        const int j = ok ? cc / r : 0, i = ok ? cc - j * r : 0;
+        jj[e] = j;
+        src[e] = j == 0 ? 0 : p + 1 - j;
+        srcl[e] = j <= 1 ? 0 : p + 2 - j;
+        gg[e] = ok ? __ldg(a.g + i) : 0.0;
+        kd[e] = ok ? __ldg(a.colKd + cc) : 0.0;
+        ka[e] = ok ? __ldg(a.colKa + cc) : 0.0;
+        tos[e] = ok ? __ldg(a.colTos + cc) : 0.0;
+      }
+      plain_rows(GS, [&](int row, bool rv, int) {
+        const bool vv = rv && c < w;
+        double acc[2] = {0.0, 0.0};
+        if (vv) {
+          const int e1 = __ldg(a.rp + row + 1);
+          for (int e = __ldg(a.rp + row); e < e1; e += 8) {
+            double x0[8], x1[8], av[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              x0[u] = x1[u] = av[u] = 0.0;
+              if (e + u < e1) {
+                const double* vr = a.D0 + size_t(__ldg(a.ci + e + u)) * size_t(p1);
+                av[u] = __ldg(a.av + e + u);
+                x0[u] = vr[src[0]];
+                x1[u] = vr[src[1]];
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (e + u < e1) {
+                acc[0] = acc[0] + av[u] * (x0[u] * gg[0]);
+                acc[1] = acc[1] + av[u] * (x1[u] * gg[1]);
+              }
+          }
+        }
+        double ad[1][2], vn[2], dn[2], sn[2];
+        const double* vo = a.D0 + size_t(rv ? row : 0) * size_t(p1);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double vw = vv ? vo[src[e]] * gg[e] : 0.0;  // Vw_1 = D_1 = S_1
+          const double vwl = (vv && jj[e] >= 2) ? vo[srcl[e]] * gg[e] : 0.0;
+          double g2 = 0.0;  // Vw = Vw * Kiter (:98)
+          if (jj[e] >= 2) g2 = g2 + vwl * ka[e];
+          g2 = g2 + vw * kd[e];
+          vn[e] = g2;
+          double y = acc[e];  // D = (A - xi I) D (:99), * t_i/s, + Vw
+          if (has_xi) y = y - a.xi * vw;
+          y = y * tos[e];
+          dn[e] = y + g2;
+          sn[e] = vw + dn[e] / sigma;  // S += D/sigma (:105)
+          ad[0][e] = vv ? fabs(dn[e]) : 0.0;
+        }
+        if (vv) {
+          const unsigned o = unsigned(row) * ldb + c;
+          __stcs(reinterpret_cast<double2*>(a.Vw + o), make_double2(vn[0], vn[1]));
+          __stcs(reinterpret_cast<double2*>(Dn + o), make_double2(dn[0], dn[1]));
+          __stcs(reinterpret_cast<double2*>(a.S + o), make_double2(sn[0], sn[1]));
+        }
+        const double rd = group_rowsum<1, 2>(ad, GS, 1);
+        if (rv) mdb = umax64(mdb, abs_bits(rd));
+      });
+    }
+    double maxD, dmy;
+    sync_step(mdb, mdb, maxD, dmy);
+    c2 = maxD / sigma;  // :103
+    if (!isfinite(c2)) {
+      err = kStSeriesDiverged;
+      err_idx = k;
+    } else {
+      nSu = (nSu + c2) * (1.0 + 1e-12);
+      nSl = (nSl - c2) * (1.0 - 1e-12);
+      exact = false;
+      if (exact_every_term) {
+        nS = s_norm_exact();
+        nSl = nSu = nS;
+        exact = true;
+      }
+      trace(1.0, c2, nS);
+      double* tmp = Dc;
+      Dc = Dn;
+      Dn = tmp;
+    }
+  } else {
+    // no S term at all (tol * ||S|| infinite): the phases below read S = Vw_1
+    const int c = 2 * (lane % GS);
+    plain_rows(GS, [&](int row, bool rv, int) {
+      if (!rv || c >= w) return;
+      double x[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = c + e;
+        const int j = cc / r, i = cc - j * r;
+        const int sc = j == 0 ? 0 : p + 1 - j;
+        x[e] = a.D0[size_t(row) * size_t(p1) + sc] * __ldg(a.g + i);
+      }
+      *reinterpret_cast<double2*>(a.S + (unsigned(row) * ldb + c)) = make_double2(x[0], x[1]);
+    });
+    double dmy1, dmy2;
+    sync_step(0ull, 0ull, dmy1, dmy2);
+  }
+  // the lane's S-term column coefficients (fixed for the whole launch)
+  int jjS[2];
+  double kdS[2], kaS[2], tosS[2];
+  {
+    const int c = 2 * (lane % GS);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int cc = c + e;
+      const bool ok = cc < w;
+      jjS[e] = ok ? cc / r : 0;
+      kdS[e] = ok ? __ldg(a.colKd + cc) : 0.0;
+      kaS[e] = ok ? __ldg(a.colKa + cc) : 0.0;
+      tosS[e] = ok ? __ldg(a.colTos + cc) : 0.0;
+    }
+  }
+  const bool vwl_vec = (r % 2) == 0;
+  for (; err == kStOk;) {
+    const double lhs = c1 + c2;
+    bool cont;
+    if (exact) {
+      cont = lhs > a.tol * nS;
+    } else if (lhs > a.tol * nSu) {
+      cont = true;
+    } else if (lhs <= a.tol * nSl) {
+      cont = false;
+    } else {
+      nS = s_norm_exact();
+      nSl = nSu = nS;
+      exact = true;
+      cont = lhs > a.tol * nS;
+    }
+    if (!cont) break;
+    if (k >= 500) {
+      err = kStSeriesCap;
+      err_idx = 500;
+      break;
+    }
+    ++k;
+    c1 = c2;
+    sigma *= k;
+    double* const Dnn = Dn;
+    const double sig = sigma;
+    const unsigned long long mdb = bulk_phase(
+        0, w, Dc, a.Vw, a.S,
+        [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
+            const double* pa, const double* pb, int, int G) -> unsigned long long {
+          double ad[1][2] = {{0.0, 0.0}};
+          if (v) {
+            const double2 vw = *reinterpret_cast<const double2*>(pa);
+            const double2 so = *reinterpret_cast<const double2*>(pb);
+            double2 vl = make_double2(0.0, 0.0);
+            if (vwl_vec) {
+              if (jjS[0] >= 2) vl = *reinterpret_cast<const double2*>(pa - r);
+            } else {
+              if (jjS[0] >= 2) vl.x = pa[-r];
+              if (jjS[1] >= 2) vl.y = pa[1 - r];
+            }
+            double2 ds = make_double2(0.0, 0.0);
+            if (has_xi) ds = *reinterpret_cast<const double2*>(self);
+            const double vwv[2] = {vw.x, vw.y}, vlv[2] = {vl.x, vl.y}, sov[2] = {so.x, so.y},
+                         dsv[2] = {ds.x, ds.y}, acc[2] = {a0, a1};
+            double vn[2], dn[2], sn[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              // Vw = Vw * Kiter: ascending source column from +0 (:98)
+              double g2 = 0.0;
+              if (jjS[e] >= 2) g2 = g2 + vlv[e] * kaS[e];
+              g2 = g2 + vwv[e] * kdS[e];
+              vn[e] = g2;
+              // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
+              double y = acc[e];
+              if (has_xi) y = y - a.xi * dsv[e];
+              y = y * tosS[e];
+              dn[e] = y + g2;
+              sn[e] = sov[e] + dn[e] / sig;  // S += D/sigma (:105)
+              ad[0][e] = fabs(dn[e]);
+            }
+            const unsigned o = unsigned(row) * ldb + c;
+            __stcs(reinterpret_cast<double2*>(a.Vw + o), make_double2(vn[0], vn[1]));
+            __stcs(reinterpret_cast<double2*>(Dnn + o), make_double2(dn[0], dn[1]));
+            __stcs(reinterpret_cast<double2*>(a.S + o), make_double2(sn[0], sn[1]));
+          }
+          const double rd = group_rowsum<1, 2>(ad, G, 1);
+          return rvalid ? abs_bits(rd) : 0ull;
+        });
+    double maxD, dmy;
+    sync_step(mdb, mdb, maxD, dmy);
+    c2 = maxD / sigma;  // :103
+    if (!isfinite(c2)) {
+      err = kStSeriesDiverged;
+      err_idx = k;
+      break;
+    }
+    nSu = (nSu + c2) * (1.0 + 1e-12);
+    nSl = (nSl - c2) * (1.0 - 1e-12);
+    exact = false;
+    if (exact_every_term) {
+      nS = s_norm_exact();
+      nSl = nSu = nS;
+      exact = true;
+    }
+    trace(1.0, c2, nS);
+    double* tmp = Dc;
+    Dc = Dn;
+    Dn = tmp;
+  }
+  const int L_S = k;
+  if (err != kStOk) {
+    finish(err, err_idx, L_S, 0);
+    return;
+  }
+
+  // ================= promotion (phi_block.cpp:109-120)
+  // F_L = fl(fl(A S_L * t_i) + v0) (unshifted A), F_R = S block p
+  double* Fc = a.F0;
+  double* Fn = a.F1;
+  const bool sweeps = a.s_eff > 1;
+  unsigned long long mf = 0;
+  {
+    const int c = 2 * (lane % GF);
+    plain_rows(GF, [&](int row, bool rv, int) {
+      // gathers S block-0 columns (left F columns live at the same column
+      // index in S); a pair straddling the left/right split gathers one extra
+      // column, unused
+      const bool vl = rv && c < r;
+      double acc[2] = {0.0, 0.0};
+      if (vl) {
+        const int e1 = __ldg(a.rp + row + 1);
+        for (int e = __ldg(a.rp + row); e < e1; e += 8) {
+          double2 x[8];
+          double av[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            x[u] = make_double2(0.0, 0.0);
+            av[u] = 0.0;
+            if (e + u < e1) {
+              av[u] = __ldg(a.av + e + u);
+              x[u] = *reinterpret_cast<const double2*>(a.S + size_t(__ldg(a.ci + e + u)) * ldb + c);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (e + u < e1) {
+              acc[0] = acc[0] + av[u] * x[u].x;
+              acc[1] = acc[1] + av[u] * x[u].y;
+            }
+        }
+      }
+      double f[2], af[1][2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        f[e] = 0.0;
+        const int cc = c + e;
+        if (rv && c < fc) {
+          const int i = cc < r ? cc : cc - r;
+          const size_t srow = size_t(row) * ldb + size_t(p) * size_t(r);
+          if (cc < r) {
+            const double sc = acc[e] * __ldg(a.t + i);
+            f[e] = sc + __ldg(a.V + row);
+          } else {
+            f[e] = a.S[srow + i];
+          }
+          if (!sweeps && cc < r) {
+            // assembly W = F_L + fl(F_R * alpha) (:148-154)
+            double wv = f[e];
+            double fr = 0.0;
+            if (p > 0) {
+              fr = a.S[srow + i];
+              wv = wv + fr * __ldg(a.alpha + i);
+            }
+            a.W[size_t(i) * size_t(n) + row] = wv;
+            if (a.FLo) a.FLo[size_t(i) * size_t(n) + row] = f[e];
+            if (a.FRo) a.FRo[size_t(i) * size_t(n) + row] = fr;
+          }
+        }
+        af[0][e] = fabs(f[e]);
+      }
+      if (sweeps && rv && c < fc) {
+        const unsigned o = unsigned(row) * ldf + c;
+        *reinterpret_cast<double2*>(Fc + o) = make_double2(f[0], f[1]);
+        *reinterpret_cast<double2*>(a.E + o) = make_double2(f[0], f[1]);
+      }
+      if (sweeps) {
+        const double rf = group_rowsum<1, 2>(af, GF, 1);
+        if (rv) mf = umax64(mf, abs_bits(rf));
+      }
+    });
+  }
+  if (!sweeps) {
+    finish(kStOk, 0, L_S, 1);
+    return;
+  }
+  double fnorm, dummy;
+  sync_step(mf, mf, fnorm, dummy);
+
+  auto e_norm_exact = [&]() -> double {
+    unsigned long long m = 0;
+    const int c = 2 * (lane % GF);
+    plain_rows(GF, [&](int row, bool rv, int) {
+      double ae[1][2] = {{0.0, 0.0}};
+      if (rv && c < fc) {
+        const double2 x = *reinterpret_cast<const double2*>(a.E + (unsigned(row) * ldf + c));
+        ae[0][0] = fabs(x.x);
+        ae[0][1] = fabs(x.y);
+      }
+      const double rs = group_rowsum<1, 2>(ae, GF, 1);
+      if (rv) m = umax64(m, abs_bits(rs));
+    });
+    double mx, dmy;
+    sync_step(m, m, mx, dmy);
+    return mx;
+  };
+
+  // the lane's recovery column scale t_i / s
+  double tosF[2];
+  {
+    const int c = 2 * (lane % GF);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int cc = c + e;
+      const int i = cc < r ? cc : cc - r;
+      tosF[e] = cc < fc ? __ldg(a.colTos + i) : 0.0;
+    }
+  }
+
+  // ================= recovery sweeps (phi_block.cpp:122-146)
+  for (int sweep = 1; sweep < a.s_eff; ++sweep) {
+    int kk = 0;
+    double d1 = INF, d2 = fnorm, nE = fnorm;  // E = F
+    trace(2.0, d2, nE);
+    double nEl = nE, nEu = nE;
+    bool eexact = true;
+    for (;;) {
+      const double lhs = d1 + d2;
+      bool cont;
+      if (eexact) {
+        cont = lhs > a.tol * nE;
+      } else if (lhs > a.tol * nEu) {
+        cont = true;
+      } else if (lhs <= a.tol * nEl) {
+        cont = false;
+      } else {
+        nE = e_norm_exact();
+        nEl = nEu = nE;
+        eexact = true;
+        cont = lhs > a.tol * nE;
+      }
+      if (!cont) break;
+      if (kk >= 300) {
+        err = kStRecoveryCap;
+        err_idx = 300;
+        break;
+      }
+      ++kk;
+      d1 = d2;
+      const double fac = a.single_variant ? a.t_single / (double(a.s_eff) * kk) : 0.0;
+      const double dkk = double(kk);
+      double* const Fnn = Fn;
+      const unsigned long long mfb = bulk_phase(
+          1, fc, Fc, a.E, nullptr,
+          [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
+              const double* pa, const double*, int, int G) -> unsigned long long {
+            double ay[1][2] = {{0.0, 0.0}};
+            if (v) {
+              const double2 eo = *reinterpret_cast<const double2*>(pa);
+              double2 fs = make_double2(0.0, 0.0);
+              if (has_xi) fs = *reinterpret_cast<const double2*>(self);
+              const double eov[2] = {eo.x, eo.y}, fsv[2] = {fs.x, fs.y}, acc[2] = {a0, a1};
+              double y[2], en[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                double yv = acc[e];
+                if (has_xi) yv = yv - a.xi * fsv[e];
+                if (a.single_variant) {
+                  yv = fac * yv;  // phi_single.cpp:106
+                } else {
+                  yv = yv / dkk;        // phi_block.cpp:132
+                  yv = yv * tosF[e];  // :134-135
+                }
+                y[e] = yv;
+                en[e] = eov[e] + yv;  // E += F (:138)
+                ay[0][e] = fabs(yv);
+              }
+              const unsigned o = unsigned(row) * ldf + c;
+              __stcs(reinterpret_cast<double2*>(Fnn + o), make_double2(y[0], y[1]));
+              __stcs(reinterpret_cast<double2*>(a.E + o), make_double2(en[0], en[1]));
+            }
+            const double ry = group_rowsum<1, 2>(ay, G, 1);
+            return rvalid ? abs_bits(ry) : 0ull;
+          });
+      double maxF2, dmy;
+      sync_step(mfb, mfb, maxF2, dmy);
+      d2 = maxF2;
+      if (!isfinite(d2)) {
+        err = kStRecoveryDiverged;
+        err_idx = kk;
+        break;
+      }
+      nEu = (nEu + d2) * (1.0 + 1e-12);
+      nEl = (nEl - d2) * (1.0 - 1e-12);
+      eexact = false;
+      if (exact_every_term) {
+        nE = e_norm_exact();
+        nEl = nEu = nE;
+        eexact = true;
+      }
+      trace(3.0, d2, nE);
+      double* tmp = Fc;
+      Fc = Fn;
+      Fn = tmp;
+    }
+    if (err != kStOk) break;
+    if (master) a.lensF[sweep - 1] = kk;
+
+    // ---- sweep end (:141-145): E *= mu; Sadv = Sadv*Jexp; F refresh
+    // phase A (S layout): Sadv blocks 1..p in place, ascending source column
+    {
+      const int c = 2 * (lane % GS);
+      plain_rows(GS, [&](int row, bool rv, int) {
+        double nv[2];
+        bool wq[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cc = c + e;
+          const int j = cc < w ? cc / r : 0, i = cc - j * r;
+          wq[e] = rv && cc < w && j >= 1;
+          nv[e] = 0.0;
+          if (wq[e]) {
+            const double* srow = a.S + size_t(row) * ldb;
+            const double* cj = a.jc + size_t(i) * size_t(p + 1);
+            double accv = 0.0;
+            for (int l = 1; l <= j; ++l) accv = accv + srow[l * r + i] * __ldg(cj + (j - l));
+            nv[e] = accv;
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (wq[e]) a.S[size_t(row) * ldb + c + e] = nv[e];
+      });
+    }
+    __syncthreads();
+    // phase B (F layout): F_L = E_L*mu, F_R = E_R*mu + Sadv_p; E = F
+    const bool last = sweep == a.s_eff - 1;
+    unsigned long long mfe = 0;
+    {
+      const int c = 2 * (lane % GF);
+      plain_rows(GF, [&](int row, bool rv, int) {
+        double f[2], af[1][2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          f[e] = 0.0;
+          const int cc = c + e;
+          if (rv && c < fc) {
+            const int i = cc < r ? cc : cc - r;
+            const size_t srow = size_t(row) * ldb + size_t(p) * size_t(r);
+            const double en = a.E[size_t(row) * ldf + cc] * __ldg(a.mu + i);
+            double fv = en;
+            if (cc >= r) fv = en + a.S[srow + i];
+            f[e] = fv;
+            if (last && cc < r) {
+              double wv = fv;
+              double fr = 0.0;
+              if (p > 0) {
+                const double er = a.E[size_t(row) * ldf + r + i] * __ldg(a.mu + i);
+                fr = er + a.S[srow + i];
+                wv = wv + (a.single_variant ? __ldg(a.alpha + i) * fr : fr * __ldg(a.alpha + i));
+              }
+              a.W[size_t(i) * size_t(n) + row] = wv;
+              if (a.FLo) a.FLo[size_t(i) * size_t(n) + row] = fv;
+              if (a.FRo) a.FRo[size_t(i) * size_t(n) + row] = fr;
+            }
+          }
+          af[0][e] = (rv && c < fc) ? fabs(f[e]) : 0.0;
+        }
+        if (!last) {
+          __syncwarp();
+          if (rv && c < fc) {
+            const unsigned o = unsigned(row) * ldf + c;
+            *reinterpret_cast<double2*>(Fc + o) = make_double2(f[0], f[1]);
+            *reinterpret_cast<double2*>(a.E + o) = make_double2(f[0], f[1]);
+          }
+          const double rf = group_rowsum<1, 2>(af, GF, 1);
+          if (rv) mfe = umax64(mfe, abs_bits(rf));
+        }
+      });
+    }
+    if (!last) {
+      double dmy;
+      sync_step(mfe, mfe, fnorm, dmy);
+    }
+  }
+  finish(err, err_idx, L_S, 0);
+}
+
+}  // namespace
+
+cudaError_t bulk_occupancy(size_t smem, int* per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(k_phimv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(smem));
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_phimv_bulk, kBulkThreads, smem);
+}
+
+cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st) {
+  BlockArgs copy = a;
+  void* args[] = {&copy};
+  const size_t smem = size_t(a.bulk_ns) * size_t(a.bulk_stage_bytes);
+  cudaError_t e = cudaFuncSetAttribute(k_phimv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(smem));
+  if (e != cudaSuccess) return e;
+  count_launch();
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_phimv_bulk), grid,
+                                     kBulkThreads, args, smem, st);
+}
+
+}  // namespace phx

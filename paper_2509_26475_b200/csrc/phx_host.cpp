@@ -162,6 +162,12 @@ struct phx_op_s {
   int32_t* d_rp = nullptr;
   int32_t* d_ci = nullptr;
   double* d_av = nullptr;
+  // tile plan of the bulk-copy evaluator (phx_plan.cpp; device copies)
+  bool plan_ok = false;
+  int32_t plan_rows = 0, plan_sgl_cap = 0, plan_emax = 0;
+  int32_t* d_plan_desc = nullptr;
+  uint8_t* d_plan_slot = nullptr;
+  int32_t* d_plan_sgl = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::mutex mu;
@@ -585,6 +591,80 @@ bool finite_all(const double* x, size_t n) {
   for (size_t q = 0; q < n; ++q)
     if (!std::isfinite(x[q])) return false;
   return true;
+}
+
+// The operator's CSR on its device (int32 row_ptr / col_idx, f64 values).
+// row_ptr and the values are padded past their ends (+8 / +2): the bulk
+// evaluator copies their tile slices in whole 16-byte granules.
+void upload_csr(phx_op op, const int64_t* row_ptr, const int32_t* col_idx, const double* vals) {
+  const int64_t n = op->n, nnz = op->nnz;
+  std::vector<int32_t> rp32(size_t(n) + 1 + 8, int32_t(nnz));
+  for (int64_t i = 0; i <= n; ++i) rp32[size_t(i)] = int32_t(row_ptr[i]);
+  PHX_CUDA(cudaMalloc(&op->d_rp, rp32.size() * 4));
+  PHX_CUDA(cudaMalloc(&op->d_ci, std::max<size_t>(1, size_t(nnz)) * 4));
+  PHX_CUDA(cudaMalloc(&op->d_av, (size_t(nnz) + 2) * 8));
+  PHX_CUDA(cudaMemcpy(op->d_rp, rp32.data(), rp32.size() * 4, cudaMemcpyHostToDevice));
+  PHX_CUDA(cudaMemset(op->d_av, 0, (size_t(nnz) + 2) * 8));
+  if (nnz > 0) {
+    PHX_CUDA(cudaMemcpy(op->d_ci, col_idx, size_t(nnz) * 4, cudaMemcpyHostToDevice));
+    PHX_CUDA(cudaMemcpy(op->d_av, vals, size_t(nnz) * 8, cudaMemcpyHostToDevice));
+  }
+}
+
+// The tile plan (phx_plan.cpp) of the bulk evaluator, built once per operator
+// (an operator whose tiles do not fit the stage keeps plan_ok = false and
+// always runs k_phimv_block).
+void upload_plan(phx_op op, const int64_t* row_ptr, const int32_t* col_idx) {
+  if (op->nnz == 0) return;
+  phx::TilePlan plan;
+  if (!phx::build_tile_plan(op->n, row_ptr, col_idx, &plan)) return;
+  PHX_CUDA(cudaMalloc(&op->d_plan_desc, plan.desc.size() * 4));
+  PHX_CUDA(cudaMalloc(&op->d_plan_slot, plan.slot.size()));
+  PHX_CUDA(cudaMalloc(&op->d_plan_sgl, plan.sgl.size() * 4));
+  PHX_CUDA(cudaMemcpy(op->d_plan_desc, plan.desc.data(), plan.desc.size() * 4, cudaMemcpyHostToDevice));
+  PHX_CUDA(cudaMemcpy(op->d_plan_slot, plan.slot.data(), plan.slot.size(), cudaMemcpyHostToDevice));
+  PHX_CUDA(cudaMemcpy(op->d_plan_sgl, plan.sgl.data(), plan.sgl.size() * 4, cudaMemcpyHostToDevice));
+  op->plan_rows = plan.rows;
+  op->plan_sgl_cap = plan.sgl_cap;
+  op->plan_emax = plan.emax;
+  op->plan_ok = true;
+}
+
+// Whether an evaluation runs the bulk-copy kernel, and its ring: PHX_BULK=0
+// never, =1 whenever eligible (tests), unset: operators of >= 2^21 rows.
+// Eligible: a tile plan, double2 lanes (both widths even) and single-chunk
+// rows (w <= 64), and a ring of >= 2 stages.  Two CTAs per SM with as many
+// stages (<= 4) as fit, else one CTA with up to 4.
+struct BulkChoice {
+  bool use = false;
+  int32_t ns = 0, stage_bytes = 0, per_sm = 0;
+};
+BulkChoice bulk_choice(phx_op op, int32_t V, int32_t QS, int32_t QF, int32_t w, int32_t fcols) {
+  BulkChoice bc;
+  const char* env = std::getenv("PHX_BULK");  // read per call (tests switch it)
+  const int mode = env ? std::atoi(env) : -1;
+  if (mode == 0 || !op->plan_ok || V != 2 || QS != 1 || QF != 1) return bc;
+  if (mode != 1 && op->n < (int64_t(1) << 21)) return bc;
+  const phx::BulkStage ls = phx::bulk_stage(op->plan_rows, op->plan_emax, w, true);
+  const phx::BulkStage lf = phx::bulk_stage(op->plan_rows, op->plan_emax, fcols, false);
+  const int32_t sb = std::max(ls.bytes, lf.bytes);
+  int optin = 0;
+  PHX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->device));
+  for (int want : {2, 1})
+    for (int ns = phx::kBulkMaxStages; ns >= 2; --ns) {
+      const size_t smem = size_t(ns) * size_t(sb);
+      if (smem > size_t(optin)) continue;
+      int per = 0;
+      PHX_CUDA(phx::bulk_occupancy(smem, &per));
+      if (per >= want) {
+        bc.use = true;
+        bc.ns = ns;
+        bc.stage_bytes = sb;
+        bc.per_sm = want;
+        return bc;
+      }
+    }
+  return bc;
 }
 
 // ---------------------------------------------------------------------------
@@ -1064,6 +1144,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
   }
   PHX_CUDA(cudaMemcpyAsync(d_ctl, h_ctl, ctl_up, cudaMemcpyHostToDevice, st));
 
+  const BulkChoice bulk = bulk_choice(op, V, QS, QF, w, fcols);
   int max_blocks = 0;
   a.bsmall = short_batch(op, QT, V, R) ? 1 : 0;
   PHX_CUDA(phx::coop_grid_size(QT, V, R, false, false, a.bsmall != 0, block, &max_blocks));
@@ -1094,13 +1175,35 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
     return (f > 0.0 && f <= 1.0) ? f : 1.0;
   }();
   const int64_t cap = std::max<int64_t>(1, int64_t(double(max_blocks) * grid_frac));
-  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(cap, ntiles)));
+  int grid = int(std::max<int64_t>(1, std::min<int64_t>(cap, ntiles)));
+  if (bulk.use) {
+    // the bulk-copy kernel (phx_bulk.cu): one cooperative launch, per_sm CTAs
+    // of 8 consumer warps + 1 producer warp on every SM
+    a.plan_desc = op->d_plan_desc;
+    a.plan_slot = op->d_plan_slot;
+    a.plan_sgl = op->d_plan_sgl;
+    a.plan_rows = op->plan_rows;
+    a.plan_sgl_cap = op->plan_sgl_cap;
+    a.plan_emax = op->plan_emax;
+    a.bulk_ns = bulk.ns;
+    a.bulk_stage_bytes = bulk.stage_bytes;
+    a.dyn = 2;
+    a.lat = 0;
+    a.bsmall = 0;
+    int sms = 0;
+    PHX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, op->device));
+    grid = bulk.per_sm * sms;
+  }
   PHX_CUDA(cudaEventRecord(op->ev0, st));
-  PHX_CUDA(phx::launch_phimv_block(a, grid, block, st));
+  if (bulk.use)
+    PHX_CUDA(phx::launch_phimv_bulk(a, grid, st));
+  else
+    PHX_CUDA(phx::launch_phimv_block(a, grid, block, st));
   {
     std::lock_guard<std::mutex> lk(g_trace_mu);
     g_last_mode = 0;
-    const int32_t var[8] = {a.QT, a.vec, a.R, a.dyn, a.lat, a.bsmall, grid, block};
+    const int32_t var[8] = {a.QT, a.vec, a.R, a.dyn, a.lat, a.bsmall, grid,
+                            bulk.use ? phx::kBulkThreads : block};
     std::memcpy(g_last_variant, var, sizeof var);
   }
   PHX_CUDA(cudaEventRecord(op->ev1, st));
@@ -1287,16 +1390,8 @@ phx_status phx_op_create_csr(int64_t n, const int64_t* row_ptr, const int32_t* c
       PHX_CUDA(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
       PHX_CUDA(cudaEventCreate(&op->ev0));
       PHX_CUDA(cudaEventCreate(&op->ev1));
-      std::vector<int32_t> rp32(size_t(n) + 1);
-      for (int64_t i = 0; i <= n; ++i) rp32[size_t(i)] = int32_t(row_ptr[i]);
-      PHX_CUDA(cudaMalloc(&op->d_rp, (size_t(n) + 1) * 4));
-      PHX_CUDA(cudaMalloc(&op->d_ci, std::max<size_t>(1, size_t(nnz)) * 4));
-      PHX_CUDA(cudaMalloc(&op->d_av, std::max<size_t>(1, size_t(nnz)) * 8));
-      PHX_CUDA(cudaMemcpy(op->d_rp, rp32.data(), (size_t(n) + 1) * 4, cudaMemcpyHostToDevice));
-      if (nnz > 0) {
-        PHX_CUDA(cudaMemcpy(op->d_ci, col_idx, size_t(nnz) * 4, cudaMemcpyHostToDevice));
-        PHX_CUDA(cudaMemcpy(op->d_av, vals, size_t(nnz) * 8, cudaMemcpyHostToDevice));
-      }
+      upload_csr(op, row_ptr, col_idx, vals);
+      upload_plan(op, row_ptr, col_idx);
     } catch (...) {
       phx_op_destroy(op);
       throw;
@@ -1388,16 +1483,7 @@ phx_status phx_op_create_csr_partitioned(int64_t n, const int64_t* row_ptr,
       PHX_CUDA(cudaEventCreate(&op->ev0));
       PHX_CUDA(cudaEventCreate(&op->ev1));
       // the selection replica: the whole CSR on part 0's device
-      std::vector<int32_t> rp32(size_t(n) + 1);
-      for (int64_t i = 0; i <= n; ++i) rp32[size_t(i)] = int32_t(row_ptr[i]);
-      PHX_CUDA(cudaMalloc(&op->d_rp, (size_t(n) + 1) * 4));
-      PHX_CUDA(cudaMalloc(&op->d_ci, std::max<size_t>(1, size_t(nnz)) * 4));
-      PHX_CUDA(cudaMalloc(&op->d_av, std::max<size_t>(1, size_t(nnz)) * 8));
-      PHX_CUDA(cudaMemcpy(op->d_rp, rp32.data(), (size_t(n) + 1) * 4, cudaMemcpyHostToDevice));
-      if (nnz > 0) {
-        PHX_CUDA(cudaMemcpy(op->d_ci, col_idx, size_t(nnz) * 4, cudaMemcpyHostToDevice));
-        PHX_CUDA(cudaMemcpy(op->d_av, vals, size_t(nnz) * 8, cudaMemcpyHostToDevice));
-      }
+      upload_csr(op, row_ptr, col_idx, vals);
     } catch (...) {
       phx_op_destroy(op);
       throw;
@@ -1440,6 +1526,9 @@ phx_status phx_op_destroy(phx_op op) {
     if (op->d_rp) cudaFree(op->d_rp);
     if (op->d_ci) cudaFree(op->d_ci);
     if (op->d_av) cudaFree(op->d_av);
+    if (op->d_plan_desc) cudaFree(op->d_plan_desc);
+    if (op->d_plan_slot) cudaFree(op->d_plan_slot);
+    if (op->d_plan_sgl) cudaFree(op->d_plan_sgl);
     if (op->ev0) cudaEventDestroy(op->ev0);
     if (op->ev1) cudaEventDestroy(op->ev1);
     if (op->stream) cudaStreamDestroy(op->stream);

@@ -3,6 +3,7 @@
 // pointers.
 #pragma once
 #include <cstdint>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -104,6 +105,18 @@ struct BlockArgs {
   // plo .. plo+pcount-1; ptab (device, nparts entries) describes all parts
   int32_t nparts, plo, pcount;
   const PartTab* ptab;
+  // tile plan of the bulk-copy evaluator (k_phimv_bulk, phx_bulk.cu): per
+  // kPlanT-row tile a descriptor of its contiguous gather copies, a one-byte
+  // slot per CSR entry (its row in the stage's gathered-row array) and the
+  // single rows; the stage layout (rows, entries) and ring depth
+  const int32_t* plan_desc;
+  const uint8_t* plan_slot;
+  const int32_t* plan_sgl;
+  int32_t plan_rows;     // gathered rows per stage: window (T+2) + singles + groups
+  int32_t plan_sgl_cap;  // single rows per stage (groups start after them)
+  int32_t plan_emax;     // CSR entries per tile (max over the tiles, even)
+  int32_t bulk_ns;       // stages in the ring
+  int32_t bulk_stage_bytes;
   // diagnostics (PHX_STEP_TIMES): %globaltimer after each grid step barrier
   // at [step]; CTA arrivals (time mod 2^48 | smid << 48) at
   // [kCtaStampBase + step * ncta + cta]
@@ -120,6 +133,65 @@ enum : int32_t {
   kStRecoveryDiverged = 4,
   kStInputNonFinite = 5,  // V has a non-finite entry (detected in the init pass)
 };
+
+// ---------------------------------------------------------------------------
+// Tile plan of the bulk-copy evaluator (built once
+// per operator by build_tile_plan, phx_plan.cpp).  A tile is kPlanT
+// consecutive rows.  Its gather sources are staged in shared memory by
+// cp.async.bulk copies of CONTIGUOUS row ranges: the window [base-1,
+// base+T+1) (the tile's own rows and every column inside it), up to
+// kPlanGroups "offset groups" (the entries whose column - row offset is shared
+// by many rows of the tile: rows [base+off, base+off+T) in one copy) and a few
+// single rows.  Descriptor (kPlanDesc int32 per tile):
+//   [0] groups  [1] singles  [2] first single in plan_sgl  [3] e_lo  [4] e_hi
+//   [8+g] group g's first source row   [12+g] rows | (stage row << 16)
+constexpr int kPlanT = 32;
+constexpr int kPlanGroups = 4;
+constexpr int kPlanDesc = 16;
+constexpr int kPlanMaxSingles = 32;
+constexpr int kPlanMaxEntries = 1024;  // per tile (stage capacity)
+constexpr int kBulkConsumers = 8;      // consumer warps per CTA (+ 1 producer warp)
+constexpr int kBulkThreads = (kBulkConsumers + 1) * 32;
+constexpr int kBulkMaxStages = 4;
+
+struct TilePlan {
+  std::vector<int32_t> desc;
+  std::vector<uint8_t> slot;  // nnz + 16 (padded for 16-byte copy granules)
+  std::vector<int32_t> sgl;   // + 1
+  int32_t rows = 0, sgl_cap = 0, emax = 0;
+  bool ok = false;
+};
+// false (plan.ok == false) when some tile needs more than the stage holds
+bool build_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, TilePlan* plan);
+
+// byte layout of one stage of the bulk ring (host and device agree)
+struct BulkStage {
+  int32_t dr, sa, sb, av, sl, rp, hdr, bytes;
+};
+__host__ __device__ inline BulkStage bulk_stage(int32_t rows, int32_t emax, int32_t width, bool two) {
+  BulkStage L;
+  int32_t o = 0;
+  L.dr = o;  // gathered rows (width even: 16-byte multiples)
+  o += rows * width * 8;
+  L.sa = o;  // stream A tile (Vw | E)
+  o += kPlanT * width * 8;
+  L.sb = o;  // stream B tile (S)
+  o += two ? kPlanT * width * 8 : 0;
+  L.av = o;  // CSR values (copied from a 16-byte granule)
+  o += (emax + 2) * 8;
+  L.sl = o;  // slots
+  o += (emax + 32 + 15) / 16 * 16;
+  L.rp = o;  // row_ptr slice
+  o += (kPlanT + 4) * 4;
+  L.hdr = o;  // tile id
+  o += 16;
+  L.bytes = (o + 127) / 128 * 128;
+  return L;
+}
+
+cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st);
+// co-resident CTAs per SM of k_phimv_bulk at the given dynamic shared memory
+cudaError_t bulk_occupancy(size_t smem, int* per_sm);
 
 // launch wrappers (phx_kernels.cu)
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st);

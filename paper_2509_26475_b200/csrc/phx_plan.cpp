@@ -1,0 +1,179 @@
+// Tile plan of the bulk-copy evaluator (phx_bulk.cu): the inspector half of an
+// inspector-executor SpMM.  Built once per operator on the host (the reference
+// operator is immutable, linop.hpp:16-18), O(nnz), tiles in parallel.
+//
+// For every kPlanT-row tile the gather sources of its CSR entries are covered
+// by CONTIGUOUS row ranges that the kernel stages with one cp.async.bulk copy
+// each:
+//   - the window [base-1, base+T+1): the tile's own rows, the diagonal and
+//     every column inside it (C5's bidiagonal rows need nothing else);
+//   - up to kPlanGroups offset groups: entries whose column - row offset is
+//     shared by at least max(2, rows/4) rows of the tile (a 3D 7-point stencil
+//     has four: +-nx and +-nx*ny), staged as the rows [base+off, base+off+T);
+//   - single rows for everything else (at most kPlanMaxSingles per tile).
+// Each entry gets a one-byte slot: its row in the stage's gathered-row array
+// [window | singles | groups].  The arithmetic is untouched -- the kernel still
+// accumulates every row's entries in CSR order -- so the plan only changes
+// where the gathered values are read from.
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <thread>
+#include <vector>
+
+#include "phx_kernels.cuh"
+
+namespace phx {
+
+namespace {
+
+struct TileInfo {
+  int32_t ng = 0;
+  int32_t goff[kPlanGroups] = {0, 0, 0, 0};
+  int32_t nsgl = 0;
+  int32_t ne = 0;
+  bool ok = true;
+};
+
+// groups and singles of one tile (deterministic: groups by count desc, then
+// offset asc; singles sorted by column)
+void analyse_tile(int64_t n, const int64_t* rp, const int32_t* ci, int64_t t, TileInfo* info,
+                  std::vector<int32_t>* singles, std::vector<int64_t>& scratch) {
+  const int64_t base = t * kPlanT, rows = std::min<int64_t>(kPlanT, n - base);
+  const int64_t wlo = std::max<int64_t>(base - 1, 0), whi = std::min<int64_t>(base + rows + 1, n);
+  scratch.clear();
+  for (int64_t rr = 0; rr < rows; ++rr)
+    for (int64_t e = rp[base + rr]; e < rp[base + rr + 1]; ++e) {
+      const int64_t col = ci[e];
+      if (col >= wlo && col < whi) continue;
+      scratch.push_back(col - (base + rr));
+    }
+  info->ne = int32_t(rp[base + rows] - rp[base]);
+  std::sort(scratch.begin(), scratch.end());
+  std::vector<std::pair<int64_t, int64_t>> runs;  // (-count, offset)
+  for (size_t i = 0; i < scratch.size();) {
+    size_t j = i;
+    while (j < scratch.size() && scratch[j] == scratch[i]) ++j;
+    runs.push_back({-int64_t(j - i), scratch[i]});
+    i = j;
+  }
+  std::sort(runs.begin(), runs.end());
+  const int64_t need = std::max<int64_t>(2, rows / 4);
+  info->ng = 0;
+  for (const auto& rc : runs) {
+    if (info->ng >= kPlanGroups || -rc.first < need) break;
+    info->goff[info->ng++] = int32_t(rc.second);
+  }
+  // singles: distinct columns of the remaining out-of-window entries
+  std::vector<int32_t> sg;
+  for (int64_t rr = 0; rr < rows; ++rr)
+    for (int64_t e = rp[base + rr]; e < rp[base + rr + 1]; ++e) {
+      const int64_t col = ci[e];
+      if (col >= wlo && col < whi) continue;
+      const int64_t off = col - (base + rr);
+      bool grouped = false;
+      for (int g = 0; g < info->ng; ++g) grouped = grouped || info->goff[g] == off;
+      if (!grouped) sg.push_back(int32_t(col));
+    }
+  std::sort(sg.begin(), sg.end());
+  sg.erase(std::unique(sg.begin(), sg.end()), sg.end());
+  info->nsgl = int32_t(sg.size());
+  info->ok = info->nsgl <= kPlanMaxSingles && info->ne <= kPlanMaxEntries;
+  if (singles) *singles = std::move(sg);
+}
+
+template <class F>
+void parallel_tiles(int64_t ntiles, F&& f) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const int64_t nthr = std::min<int64_t>(int64_t(hw), std::max<int64_t>(1, ntiles / 4096));
+  std::atomic<int64_t> next{0};
+  auto work = [&] {
+    std::vector<int64_t> scratch;
+    for (;;) {
+      const int64_t t0 = next.fetch_add(1024);
+      if (t0 >= ntiles) return;
+      for (int64_t t = t0; t < std::min(ntiles, t0 + 1024); ++t) f(t, scratch);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int64_t i = 1; i < nthr; ++i) th.emplace_back(work);
+  work();
+  for (auto& x : th) x.join();
+}
+
+}  // namespace
+
+bool build_tile_plan(int64_t n, const int64_t* rp, const int32_t* ci, TilePlan* plan) {
+  plan->ok = false;
+  const int64_t ntiles = (n + kPlanT - 1) / kPlanT;
+  std::vector<TileInfo> info(static_cast<size_t>(ntiles));
+  std::atomic<bool> ok{true};
+  parallel_tiles(ntiles, [&](int64_t t, std::vector<int64_t>& scratch) {
+    if (!ok.load(std::memory_order_relaxed)) return;
+    analyse_tile(n, rp, ci, t, &info[size_t(t)], nullptr, scratch);
+    if (!info[size_t(t)].ok) ok = false;
+  });
+  if (!ok) return false;
+  int32_t ngmax = 0, smax = 0, emax = 0;
+  std::vector<int64_t> sgl_lo(size_t(ntiles) + 1, 0);
+  for (int64_t t = 0; t < ntiles; ++t) {
+    ngmax = std::max(ngmax, info[size_t(t)].ng);
+    smax = std::max(smax, info[size_t(t)].nsgl);
+    emax = std::max(emax, info[size_t(t)].ne);
+    sgl_lo[size_t(t + 1)] = sgl_lo[size_t(t)] + info[size_t(t)].nsgl;
+  }
+  if (sgl_lo[size_t(ntiles)] >= (int64_t(1) << 31)) return false;
+  const int32_t T = kPlanT;
+  const int32_t gbase = (T + 2) + smax;  // first group row of a stage
+  plan->rows = gbase + ngmax * T;
+  plan->sgl_cap = smax;
+  plan->emax = (emax + 1) / 2 * 2;
+  if (plan->rows > 256) return false;  // one-byte slots
+  const int64_t nnz = rp[n];
+  plan->desc.assign(size_t(ntiles) * kPlanDesc, 0);
+  plan->slot.assign(size_t(nnz) + 16, 0);
+  plan->sgl.assign(size_t(sgl_lo[size_t(ntiles)]) + 1, 0);
+  parallel_tiles(ntiles, [&](int64_t t, std::vector<int64_t>& scratch) {
+    TileInfo ti;
+    std::vector<int32_t> sg;
+    analyse_tile(n, rp, ci, t, &ti, &sg, scratch);
+    const int64_t base = t * T, rows = std::min<int64_t>(T, n - base);
+    const int64_t wlo = std::max<int64_t>(base - 1, 0), whi = std::min<int64_t>(base + rows + 1, n);
+    int32_t* d = plan->desc.data() + size_t(t) * kPlanDesc;
+    d[0] = ti.ng;
+    d[1] = ti.nsgl;
+    d[2] = int32_t(sgl_lo[size_t(t)]);
+    d[3] = int32_t(rp[base]);
+    d[4] = int32_t(rp[base + rows]);
+    for (int g = 0; g < ti.ng; ++g) {
+      const int64_t o0 = base + ti.goff[g];
+      const int64_t s0 = std::max<int64_t>(0, o0), s1 = std::min<int64_t>(n, o0 + rows);
+      const int64_t dst = gbase + int64_t(g) * T + (s0 - o0);
+      d[8 + g] = int32_t(s0);
+      d[12 + g] = int32_t((s1 - s0) | (dst << 16));
+    }
+    std::copy(sg.begin(), sg.end(), plan->sgl.begin() + sgl_lo[size_t(t)]);
+    for (int64_t rr = 0; rr < rows; ++rr)
+      for (int64_t e = rp[base + rr]; e < rp[base + rr + 1]; ++e) {
+        const int64_t col = ci[e];
+        int64_t sl;
+        if (col >= wlo && col < whi) {
+          sl = col - wlo;
+        } else {
+          const int64_t off = col - (base + rr);
+          int g = -1;
+          for (int q = 0; q < ti.ng; ++q)
+            if (ti.goff[q] == off) g = q;
+          if (g >= 0)
+            sl = gbase + int64_t(g) * T + rr;
+          else
+            sl = (T + 2) + (std::lower_bound(sg.begin(), sg.end(), int32_t(col)) - sg.begin());
+        }
+        plan->slot[size_t(e)] = uint8_t(sl);
+      }
+  });
+  plan->ok = true;
+  return true;
+}
+
+}  // namespace phx
