@@ -254,9 +254,26 @@ int32_t phx_last_eval_mode(void);
 
 /* The kernel variant of the last single-device evaluation (diagnostics):
  * out[0..7] = column chunks per lane Q, columns per lane V, rows per lane
- * group R, dynamic tail (0/1), latency mode (0/1), short-row gather batch
- * (0/1), grid size, CTA size. */
+ * group R, tile scheduling (0 static, 1 dynamic tail, 2 the bulk-copy kernel
+ * k_phimv_bulk), latency mode (0/1), short-row gather batch (0/1), grid size,
+ * CTA size.  The bulk-copy kernel runs when the operator has a tile plan and
+ * both block widths are even and <= 64; environment PHX_BULK=0 disables it,
+ * PHX_BULK=1 forces it for every eligible operator (read on every call). */
 phx_status phx_last_eval_variant(int32_t* out8);
+
+/* The tile plan of the bulk-copy evaluator for a host CSR matrix, built on
+ * the host exactly as phx_op_create_csr builds it (no device needed; for
+ * diagnostics and tests).  The plan covers every kPlanT = 32-row tile's
+ * gathered rows with contiguous copies -- the window [base-1, base+33), up to
+ * 4 offset groups (rows [base+off, base+off+32)) and single rows -- and gives
+ * every CSR entry a one-byte slot (its row in the stage: window rows first,
+ * then singles, then groups).  info[0..5] = ok (0/1), tiles, stage rows,
+ * single rows per stage, max entries per tile (even), total single rows.
+ * When non-null, desc (tiles x 16 int32: groups, singles, first single,
+ * e_lo, e_hi, -, -, -, group source rows[4], group rows | stage row << 16
+ * [4]), slot (nnz + 16 bytes) and sgl (total single rows + 1) are filled. */
+phx_status phx_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* info6,
+                         int32_t* desc, uint8_t* slot, int32_t* sgl);
 
 /* Device-event time (ms) of the last phimv_block evaluation kernel, and the
  * number of grid-wide steps it executed (S terms + promotion + recovery

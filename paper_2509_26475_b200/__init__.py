@@ -79,6 +79,7 @@ ABI_SYMBOLS = (
     "phx_mm_read_csr", "phx_mm_write_csr", "phx_op_create_mm", "phx_block_series_direct",
     "phx_last_eval_mode",
     "phx_last_eval_variant",
+    "phx_tile_plan",
 )
 
 
@@ -141,6 +142,9 @@ def lib():
     L.phx_last_eval_stats.argtypes = [dp, i64p]
     L.phx_last_eval_mode.restype = C.c_int32
     L.phx_last_eval_variant.argtypes = [C.POINTER(C.c_int32)]
+    L.phx_tile_plan.argtypes = [C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_uint8), C.POINTER(C.c_int32)]
     L.phx_set_trace.argtypes = [C.c_int64]
     L.phx_get_trace.argtypes = [dp, C.c_int64, i64p]
     _LIB = L
@@ -470,6 +474,30 @@ def last_eval_variant() -> dict:
     _check(lib().phx_last_eval_variant(out))
     keys = ("Q", "V", "R", "dynamic_tail", "latency_mode", "short_batch", "grid", "block")
     return dict(zip(keys, (int(x) for x in out)))
+
+
+def tile_plan(n, row_ptr, col_idx):
+    """The bulk-copy evaluator's tile plan of a host CSR (built on the host,
+    as phx_op_create_csr builds it): (info dict, desc (tiles x 16), slot
+    (nnz + 16 bytes), sgl) -- arrays None when the plan does not fit."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    info = np.zeros(6, dtype=np.int32)
+    i32 = C.POINTER(C.c_int32)
+    _check(lib().phx_tile_plan(int(n), rp.ctypes.data_as(C.POINTER(C.c_int64)),
+                               ci.ctypes.data_as(i32), info.ctypes.data_as(i32), None, None, None))
+    keys = ("ok", "tiles", "rows", "singles_cap", "emax", "singles")
+    d = dict(zip(keys, (int(x) for x in info)))
+    if not d["ok"]:
+        return d, None, None, None
+    desc = np.zeros((d["tiles"], 16), dtype=np.int32)
+    slot = np.zeros(int(rp[-1]) + 16, dtype=np.uint8)
+    sgl = np.zeros(d["singles"] + 1, dtype=np.int32)
+    _check(lib().phx_tile_plan(int(n), rp.ctypes.data_as(C.POINTER(C.c_int64)),
+                               ci.ctypes.data_as(i32), info.ctypes.data_as(i32),
+                               desc.ctypes.data_as(i32),
+                               slot.ctypes.data_as(C.POINTER(C.c_uint8)), sgl.ctypes.data_as(i32)))
+    return d, desc, slot, sgl
 
 
 def last_eval_stats():

@@ -133,6 +133,11 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
   int kpipe = 0;                               // ring stages used so far (producer == consumers)
   int step = 0, tr_len = 0;
 
+  if (master && a.tstamp != nullptr && a.tstamp_cap > kCtaStampBase) {  // diagnostics: launch start
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    a.tstamp[kCtaStampBase - 1] = ns;
+  }
   auto trace = [&](double kind, double x, double y) {
     if (master && a.trace != nullptr && tr_len + 3 <= a.trace_cap) {
       a.trace[tr_len] = kind;

@@ -2135,6 +2135,25 @@ phx_status phx_block_series_direct(phx_op op, int32_t r, const double* t, const 
   });
 }
 
+phx_status phx_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* info6,
+                         int32_t* desc, uint8_t* slot, int32_t* sgl) {
+  return guarded([&] {
+    if (!info6 || !row_ptr || n < 1) throw_phx(PHX_EINVAL, "phx_tile_plan: bad arguments");
+    phx::TilePlan plan;
+    const bool ok = phx::build_tile_plan(n, row_ptr, col_idx, &plan);
+    info6[0] = ok ? 1 : 0;
+    info6[1] = int32_t((n + phx::kPlanT - 1) / phx::kPlanT);
+    info6[2] = ok ? plan.rows : 0;
+    info6[3] = ok ? plan.sgl_cap : 0;
+    info6[4] = ok ? plan.emax : 0;
+    info6[5] = ok ? int32_t(plan.sgl.size()) - 1 : 0;
+    if (!ok) return;
+    if (desc) std::copy(plan.desc.begin(), plan.desc.end(), desc);
+    if (slot) std::copy(plan.slot.begin(), plan.slot.end(), slot);
+    if (sgl) std::copy(plan.sgl.begin(), plan.sgl.end(), sgl);
+  });
+}
+
 int32_t phx_last_eval_mode(void) {
   std::lock_guard<std::mutex> lk(g_trace_mu);
   return g_last_mode;
