@@ -2,26 +2,30 @@
 """Benchmark of the B200 phi-combination hot path (BASELINE.json metric).
 
 A step is one phimv_block evaluation (Alg. 3, phi_block.cpp:48-157) of the
-configs[1] workload — 2D advection-diffusion, n = 1,048,576, FP64 CSR, p=3,
-r=4, tol 1e-10 — with ScalingShift selected once beforehand and reused (as
-the paper prescribes).  `value` = phi-combination blocks/s over
-the whole job with V already resident in HBM; `e2e` = the same through the
-C-ABI host-buffer call (pinned V in, W out, copies inside the timed region).
+largest single-GPU stencil config, C3: 3D convection-diffusion on a 256^3
+grid, n = 16,777,216, FP64 CSR (7 nnz/row), p = 4, r = 6, tol 2^-53 -- with
+ScalingShift selected once beforehand and reused (as the paper prescribes,
+PAPER.md:740).  `value` = phi-combination blocks/s over the whole job with V
+resident in HBM; `e2e` = the same through the C-ABI host-buffer call (V in,
+W out, copies inside the timed region).  --config 2 runs C2 (1024^2) instead.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU: one process per GPU (torchrun); each rank evaluates its own
-independent block (phi blocks are independent units, weak scaling, no
-data-path collective); timing is the max over ranks.  --impl reference times
-the CPU oracle (the reference cannot be compiled here: no Eigen) on the host
-cores.
+Multi-GPU (--gpus N, with or without torchrun): ONE C3 block row-partitioned
+over N devices of this node (contiguous row parts, peer
+gathers over NVLink, per-step max-allreduce through peer mailboxes), driven
+by rank 0; strong scaling.  Under torchrun the other ranks exit at once.
+--impl reference times the CPU reference path (the oracle port -- the
+reference itself needs Eigen, absent here) on the host cores.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
 import os
+import platform
 import statistics
 import sys
 import threading
@@ -34,6 +38,9 @@ sys.path.insert(0, HERE)
 
 METRIC = "φ-combination blocks/s"
 UNIT = "blocks/s"
+NAMES = {1: "C1 1D Dirichlet Laplacian", 2: "C2 2D advection-diffusion 1024^2",
+         3: "C3 3D convection-diffusion 256^3", 4: "C4 random sparse stiff",
+         5: "C5 nonnormal upper bidiagonal"}
 
 
 def env_int(k, d):
@@ -53,23 +60,37 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(cfg):
-    """dram read+write bytes per launch of k_phimv_block from the committed
-    ncu --set full capture summary (profiles/), or None."""
+def ncu_traffic(cfg, kernel="k_phimv_bulk"):
+    """dram read+write bytes per launch of the evaluation kernel from the
+    committed ncu --set full capture summary (profiles/ncu_summary.json), or
+    None."""
     p = os.path.join(HERE, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(f"cfg{cfg}")
+        e = d.get(f"cfg{cfg}_{kernel}") or (d.get(f"cfg{cfg}") if kernel == "k_phimv_block" else None)
         return float(e["dram_bytes_per_launch"]) if e else None
     except Exception:
         return None
 
 
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
 class ClockSampler:
     """Samples SM clocks and throttle reasons via NVML during the timed region."""
 
-    def __init__(self, dev_index):
+    def __init__(self, dev_indices):
         self.samples = []
         self.reasons = set()
         self.max_mhz = None
@@ -79,8 +100,8 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.hs = [pynvml.nvmlDeviceGetHandleByIndex(i) for i in dev_indices]
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.hs[0], pynvml.NVML_CLOCK_SM)
         except Exception:
             self.nv = None
 
@@ -94,14 +115,15 @@ class ClockSampler:
             "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
         }
         while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for k, bit in names.items():
-                    if mask & bit:
-                        self.reasons.add(k)
-            except Exception:
-                pass
+            for h in self.hs:
+                try:
+                    self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for k, bit in names.items():
+                        if mask & bit:
+                            self.reasons.add(k)
+                except Exception:
+                    pass
             self._stop.wait(0.02)
 
     def __enter__(self):
@@ -132,94 +154,158 @@ def max_over_ranks(x: float, dist=None, device="cpu") -> float:
     return float(t.item())
 
 
-def algorithmic_bytes(wl, rec):
-    """Algorithmic HBM bytes of one k_phimv_block launch,
-    counting only bytes the kernel moves: init 16n(p+1) (V read, V row-major
-    write -- Vw_1 = D_1 = S_1 is recomputed, not stored); the first S term
-    CSR + 8n(p+1) + 24wn (V rows gathered, Vw/D'/S written), each further
-    S term B_S = CSR + 48wn; promotion+assembly CSR + 8n(3r+1); each
-    recovery term B_F = CSR + 32 fc n; each sweep end 8n(2fc + 2pr)."""
+def algorithmic_bytes(wl, rec, bulk=False):
+    """Algorithmic HBM bytes of one evaluation launch,
+    counting only bytes the kernel moves.
+
+    Both kernels: init 16n(p+1) (V read, V row-major write -- Vw_1 = D_1 =
+    S_1 is recomputed, not stored); the first S term CSR + 8n(p+1) + 24wn
+    (V rows gathered, Vw/D'/S written); promotion+assembly CSR + 8n(3r+1);
+    each sweep end 8n(2fc + 2pr).  Each further S term moves CSR_t + 48wn
+    and each recovery term CSR_t + 32 fc n, where CSR_t = CSR = 12 nnz +
+    4(n+1) for k_phimv_block and, for the bulk-copy kernel (which reads the
+    tile plan's one-byte slots instead of column indices), CSR_t = 9 nnz +
+    4(n+1) + 64 B per 32-row tile descriptor."""
     n, p, r = wl.n, wl.p, wl.r
     w = (p + 1) * r
     fc = r if p == 0 else 2 * r
     csr = 12 * wl.nnz + 4 * (n + 1)
+    csr_t = (9 * wl.nnz + 4 * (n + 1) + 64 * ((n + 31) // 32)) if bulk else csr
     b = 16 * n * (p + 1)
     if rec.series_len_S >= 2:
         b += csr + 8 * n * (p + 1) + 24 * w * n
-    b += max(0, rec.series_len_S - 2) * (csr + 48 * w * n)
+    b += max(0, rec.series_len_S - 2) * (csr_t + 48 * w * n)
     b += csr + 8 * n * (3 * r + 1)
     for lf in rec.series_lens_F:
-        b += lf * (csr + 32 * fc * n)
+        b += lf * (csr_t + 32 * fc * n)
     b += len(rec.series_lens_F) * 8 * n * (2 * fc + 2 * p * r)
     return b
 
 
+def golden_params(cfg, size):
+    """The oracle's ScalingShift for a full-size config from the committed
+    fixture (tests/golden/full_cfg*.json), with the oracle's W SHA-256."""
+    if size:
+        return None, None
+    p = os.path.join(HERE, "tests", "golden", f"full_cfg{cfg}.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d["params"], d.get("W_sha256")
+    except Exception:
+        return None, None
+
+
+def oracle_sample(O, op, wl, ss, terms=1, sweeps=1):
+    """One CPU timing sample of the oracle on the block: setup, `terms` S
+    terms, promotion (+ `sweeps` recovery sweeps), assembly -- phases timed."""
+    ph, rec4 = O.phimv_block_timed(op, wl.t, wl.alpha, wl.V, wl.tol, ss, terms, sweeps)
+    return ph
+
+
+def extrapolate(ph, L_S, nsweeps):
+    """Setup-free extrapolation of a sample to the whole evaluation: the
+    fixed parts (setup, promotion, assembly) and the first S term / first
+    sweep once, the remaining S terms / sweeps at the sample's steady cost
+    (terms / sweeps after the first)."""
+    t = ph["setup"] + ph["promotion"] + ph["assembly"]
+    runs, tot, first = ph["s_terms_run"], ph["s_terms"], ph["first_s_term"]
+    if runs >= 2 and L_S >= 2:
+        t += first + (tot - first) / (runs - 1) * (L_S - 2)
+    elif runs >= 1:
+        t += tot / runs * (L_S - 1)
+    runs, tot, first = ph["sweeps_run"], ph["sweeps"], ph["first_sweep"]
+    if runs >= 2 and nsweeps >= 1:
+        t += first + (tot - first) / (runs - 1) * (nsweeps - 1)
+    elif runs >= 1:
+        t += tot / runs * nsweeps
+    return t
+
+
+def oracle_setup(args, wl):
+    import oracle as O
+    op = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    gp, _ = golden_params(args.config, args.size)
+    if gp is not None:
+        ss = O.ScalingShift(*gp)
+        src = "committed oracle fixture tests/golden/full_cfg%d.json" % args.config
+    else:
+        ss = O.select_parameters(op, 61, wl.tol)
+        src = "oracle select_parameters"
+    return O, op, ss, src
+
+
 def run_reference(args):
     """CPU reference arm: the oracle (C++ restatement of the reference path;
-    the reference needs Eigen, absent here) on the host cores."""
-    rank = env_int("RANK", 0)
-    if rank != 0:
+    the reference needs Eigen, absent here) with all host threads, each step
+    a bounded sample of the block, extrapolated setup-free; one full
+    evaluation validates the extrapolation."""
+    if env_int("RANK", 0) != 0:
         return 0
-    import oracle as O
     import paper_2509_26475_b200 as P  # workload generator only (input setup)
     wl = P.workload(args.config, args.size)
-    op = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
-    ss = O.select_parameters(op, 61, wl.tol)
-    # one untimed full evaluation calibrates the per-block cost in S terms
-    t0 = time.perf_counter()
-    _, rec = O.phimv_block(op, wl.t, wl.alpha, wl.V, wl.tol, ss)
-    t_full1 = time.perf_counter() - t0
-    w = (wl.p + 1) * wl.r
-    full_units = (rec.series_len_S - 1) * w + wl.r + sum(2 * wl.r * lf for lf in rec.series_lens_F)
-    k_cap = max(1, min(args.ref_terms, rec.series_len_S - 1))
-    sample_units = k_cap * w
-    # all host threads the memory allows (each evaluation holds ~10 n x w blocks)
-    try:
-        import psutil
-        avail = psutil.virtual_memory().available
-    except Exception:
-        avail = 64 << 30
-    per = 12 * 8 * wl.n * w + (1 << 28)
-    cores = os.cpu_count() or 1
-    threads = max(1, min(cores, int(avail * 0.6 // per)))
-
-    def one_step():
-        done = [0] * threads
-
-        def work(i):
-            done[i] = O.phimv_block_prefix(op, wl.t, wl.alpha, wl.V, wl.tol, ss, k_cap)
-
-        ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    O, op, ss, src = oracle_setup(args, wl)
+    model, cores = cpu_info()
+    O.set_threads(cores)
+    nsw = int(np.ceil(ss.s * np.max(np.abs(wl.t)))) - 1  # recovery sweeps (:58-59)
+    steps = []
+    if nsw == 0:
+        # calibration: one full (threaded) evaluation, phases timed (fixed
+        # costs: setup, first S term, promotion, assembly), after a short
+        # untimed warm-up sample (threads, page allocation)
+        O.phimv_block_timed(op, wl.t, wl.alpha, wl.V, wl.tol, ss, 2, 0)
         t0 = time.perf_counter()
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-        return time.perf_counter() - t0
-
-    for _ in range(args.warmup):
-        one_step()
-    tot = 0.0
-    for _ in range(args.steps):
-        tot += one_step()
-    per_step = tot / args.steps
-    # each step: `threads` concurrent samples of k_cap S terms; a full block
-    # costs full_units/sample_units samples
-    block_time = per_step * full_units / sample_units
-    value = threads / block_time
+        ph_full, rec = O.phimv_block_timed(op, wl.t, wl.alpha, wl.V, wl.tol, ss)
+        t_full = time.perf_counter() - t0
+        L_S = rec[1]
+        fixed = (ph_full["setup"] + ph_full["first_s_term"] + ph_full["promotion"]
+                 + ph_full["assembly"])
+        # steps: S terms 2, 3, ... of sampled evaluations (setup once per
+        # sample, not a step), each timed alone; block time = fixed costs +
+        # (L_S - 2) x the step's term time
+        per_run = max(1, L_S - 2)
+        while len(steps) < args.warmup + args.steps:
+            want = min(per_run, args.warmup + args.steps - len(steps)) + 1
+            _, _, tt = O.phimv_block_timed(op, wl.t, wl.alpha, wl.V, wl.tol, ss, want, 0,
+                                           term_times=True)
+            steps += [(x, fixed + (L_S - 2) * x) for x in tt[1:want]]
+        steps = steps[args.warmup:]
+        how = (f"Each step: one steady S term (terms 2.. of sampled evaluations), timed alone; "
+               f"block time = fixed phases of the calibration (setup, first S term, promotion, "
+               f"assembly: {fixed:.2f} s) + {L_S - 2} x the step's term time")
+    else:
+        # configs with recovery sweeps: each step a sample (setup, 3 S terms,
+        # promotion, 2 sweeps, assembly), extrapolated setup-free
+        _, rec = O.phimv_block_timed(op, wl.t, wl.alpha, wl.V, wl.tol, ss, 1, 1)
+        L_S = rec[1]
+        t_full = None
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            ph = oracle_sample(O, op, wl, ss, 3, 2)
+            wall = time.perf_counter() - t0
+            if i >= args.warmup:
+                steps.append((wall, extrapolate(ph, L_S, nsw)))
+        how = ("Each step: setup + 3 S terms + promotion + 2 recovery sweeps + assembly, timed "
+               "by phase; block time extrapolated setup-free (fixed phases and the first term / "
+               "sweep once, the rest at their steady cost)")
+    per_block = statistics.mean(e for _, e in steps)
+    value = 1.0 / per_block
+    val = (f" One full evaluation (calibration) took {t_full:.2f} s: extrapolated/full = "
+           f"{per_block / t_full:.3f}." if t_full else "")
+    sample = (f"oracle port, {cores} threads (row-parallel loops; the reference is single-"
+              f"threaded), CPU '{model}' nproc={cores}. {how}; L_S={L_S}"
+              + (f", {nsw} sweeps" if nsw else "") +
+              f" (mean {per_block:.2f} s per block).{val} ScalingShift from {src}.")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "ms_per_step": 1e3 * statistics.mean(w for w, _ in steps), "higher_is_better": True,
+        "scaling": "strong" if args.gpus > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, csrc/workloads.cpp)",
         "config": config_dict(wl, args),
-        "cpu_baseline": {
-            "value": value, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": (f"{threads} concurrent single-thread oracle evaluations per step, each the "
-                       f"first {k_cap} S-series terms of the block; block cost extrapolated by "
-                       f"matvec units ({full_units}/{sample_units}); one untimed full "
-                       f"evaluation took {t_full1:.2f} s on 1 core"),
-        },
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample, "full_evaluation_s": t_full,
+                         "extrapolated_block_s": per_block},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -227,84 +313,99 @@ def run_reference(args):
 
 
 def config_dict(wl, args):
-    names = {1: "C1 1D Dirichlet Laplacian", 2: "C2 2D advection-diffusion 1024^2",
-             3: "C3 3D convection-diffusion 256^3", 4: "C4 random sparse stiff",
-             5: "C5 nonnormal upper bidiagonal"}
-    return {"workload": names.get(wl.cfg, str(wl.cfg)) + (f" (size {wl.size})" if args.size else ""),
+    par = f"row-partition x{args.gpus} (one process, peer gathers over NVLink)" if args.gpus > 1 \
+        else "1 GPU"
+    return {"workload": NAMES.get(wl.cfg, str(wl.cfg)) + (f" (size {wl.size})" if args.size else ""),
             "n": wl.n, "nnz": wl.nnz, "p": wl.p, "r": wl.r, "tol": wl.tol,
-            "block_width": (wl.p + 1) * wl.r, "parallelism": f"replicas x{args.gpus}",
+            "block_width": (wl.p + 1) * wl.r, "parallelism": par,
             "l2": "working set (Vw, D, D', S: 4 x n x w x 8 B) larger than the 126 MB L2; no flush"}
+
+
+def sha(a):
+    return hashlib.sha256(np.asfortranarray(a, dtype=np.float64).tobytes(order="F")).hexdigest()
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--size", type=int, default=0)
-    ap.add_argument("--ref-terms", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    world = env_int("WORLD_SIZE", 1)
+    if world > 1 and args.gpus == 1:
+        args.gpus = world
     if args.impl == "reference":
         return run_reference(args)
+    if env_int("RANK", 0) != 0:
+        return 0  # rank 0 drives every device of the partitioned operator
 
     import torch
     import paper_2509_26475_b200 as P
 
-    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
+    N = args.gpus
     wl = P.workload(args.config, args.size)
-    op = P.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, device=local)
+    devices = list(range(N))
+    if N == 1:
+        op = P.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, device=0)
+    else:
+        op = P.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=N, devices=devices)
+    torch.cuda.set_device(0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     params = P.select_parameters(op, 61, wl.tol)
     sel_s = time.perf_counter() - t0
 
-    stream = torch.cuda.ExternalStream(op.stream_ptr(), device=torch.device("cuda", local))
-    dV = torch.from_numpy(np.ascontiguousarray(wl.V.T)).to(f"cuda:{local}")  # (p+1, n) = col-major V
-    dW = torch.empty((wl.r, wl.n), dtype=torch.float64, device=f"cuda:{local}")
-    torch.cuda.synchronize()
+    # device-resident V / W: part q's row slices on part q's device
+    parts = [op.part_info(q) for q in range(op.parts)]
+    Vt = np.ascontiguousarray(wl.V.T)  # (p+1, n): column-major V
+    dV, dW = [], []
+    for pi in parts:
+        dev = f"cuda:{pi['device']}"
+        lo, hi = pi["row0"], pi["row0"] + pi["nrows"]
+        dV.append(torch.from_numpy(np.ascontiguousarray(Vt[:, lo:hi])).to(dev))
+        dW.append(torch.empty((wl.r, pi["nrows"]), dtype=torch.float64, device=dev))
+    streams = [torch.cuda.ExternalStream(pi["stream"], device=torch.device("cuda", pi["device"]))
+               for pi in parts]
+    for q in range(len(parts)):
+        torch.cuda.synchronize(parts[q]["device"])
 
     def step():
-        return P.phimv_block_device(op, wl.t, wl.alpha, wl.p, dV.data_ptr(), wl.tol, params,
-                                    dW.data_ptr())
+        return P.phimv_block_device_parts(op, wl.t, wl.alpha, wl.p, [x.data_ptr() for x in dV],
+                                          wl.tol, params, [x.data_ptr() for x in dW])
+
+    def sync_all():
+        for d in set(pi["device"] for pi in parts):
+            torch.cuda.synchronize(d)
 
     for _ in range(max(args.warmup, 0)):
         rec = step()
-    barrier()
-    torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    sync_all()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in parts]
     launches0 = P.kernel_launches()
     kms = []
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
+    with ClockSampler(sorted(set(pi["device"] for pi in parts))) as clk:
+        for (e0, _), s in zip(evs, streams):
+            e0.record(s)
         for _ in range(args.steps):
             rec = step()
             kms.append(P.last_eval_stats()[0])
-        ev1.record(stream)
-        torch.cuda.synchronize()
+        for (_, e1), s in zip(evs, streams):
+            e1.record(s)
+        sync_all()
     launches = P.kernel_launches() - launches0
-    elapsed = ev0.elapsed_time(ev1) / 1e3
-    barrier()
-    elapsed_max = max_over_ranks(elapsed, dist, f"cuda:{local}")
-    value = args.steps * world / elapsed_max
+    elapsed = max(e0.elapsed_time(e1) for e0, e1 in evs) / 1e3  # max over devices
+    value = args.steps / elapsed
+    var = P.last_eval_variant() if N == 1 else None
+    bulk = bool(var and var["dynamic_tail"] == 2)
+    W_dev = np.concatenate([x.cpu().numpy() for x in dW], axis=1).T  # (n, r)
 
-    # ---- e2e through the C-ABI host-buffer call: pinned V in, W out ----
+    # ---- e2e through the C-ABI host-buffer call (phx_phimv_block) ----
     L = P.lib()
-    hV = torch.from_numpy(np.ascontiguousarray(wl.V.T)).pin_memory()
-    hW = torch.empty((wl.r, wl.n), dtype=torch.float64).pin_memory()
     tt = np.ascontiguousarray(wl.t)
     aa = np.ascontiguousarray(wl.alpha)
     ss = params._c()
@@ -312,74 +413,91 @@ def main():
     crec = P._Rec(0, 0, 0, lens.ctypes.data_as(P.i32p), lens.size, 0)
     dp = C.POINTER(C.c_double)
 
-    def e2e_step():
-        code = L.phx_phimv_block(op._h, wl.r, tt.ctypes.data_as(dp), aa.ctypes.data_as(dp), wl.p,
-                                 C.cast(hV.data_ptr(), dp), wl.n, wl.tol, C.byref(ss),
-                                 C.cast(hW.data_ptr(), dp), wl.n, C.byref(crec))
-        P._check(code)
+    def e2e_run(hV, hW, nsteps):
+        def one():
+            P._check(L.phx_phimv_block(op._h, wl.r, tt.ctypes.data_as(dp), aa.ctypes.data_as(dp),
+                                       wl.p, C.cast(hV.data_ptr(), dp), wl.n, wl.tol, C.byref(ss),
+                                       C.cast(hW.data_ptr(), dp), wl.n, C.byref(crec)))
+        one()
+        sync_all()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(streams[0])
+        for _ in range(nsteps):
+            one()  # synchronous: returns after W is in host memory
+        e1.record(streams[0])
+        sync_all()
+        return nsteps / (e0.elapsed_time(e1) / 1e3)
 
-    e2e_steps = max(5, args.steps // 2)
-    for _ in range(2):
-        e2e_step()
-    barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_el = e0.elapsed_time(e1) / 1e3
-    e2e_value = e2e_steps * world / max_over_ranks(e2e_el, dist, f"cuda:{local}")
+    e2e_steps = max(3, args.steps // 2)
+    hV = torch.from_numpy(Vt).pin_memory()
+    hW = torch.empty((wl.r, wl.n), dtype=torch.float64).pin_memory()
+    e2e_value = e2e_run(hV, hW, e2e_steps)
+    W_host = hW.numpy().T.copy()
+    hVp = torch.from_numpy(Vt.copy())  # pageable: how an Eigen caller passes V
+    hWp = torch.empty((wl.r, wl.n), dtype=torch.float64)
+    e2e_pageable = e2e_run(hVp, hWp, e2e_steps)
 
-    # ---- roofline of the dominant (only) kernel, k_phimv_block ----
+    # ---- roofline of the dominant (only) kernel ----
     peak, peak_src = measured_peak()
     prec = P.RunRecord(rec.s_effective, rec.series_len_S, rec.series_lens_F, rec.matvecs)
-    alg = algorithmic_bytes(wl, prec)
+    alg = algorithmic_bytes(wl, prec, bulk)
     kernel_s = statistics.mean(kms) / 1e3
     achieved = alg / kernel_s / 1e9
-    traffic = ncu_traffic(args.config)
+    kname = "k_phimv_bulk" if bulk else "k_phimv_block"
+    traffic = ncu_traffic(args.config, kname) if N == 1 else None
+
+    # ---- parity at full size: the oracle's committed SHA-256 of W ----
+    _, want_sha = golden_params(args.config, args.size)
+    got_sha = sha(W_dev)
+    parity = {"W_sha256": got_sha, "oracle_fixture_sha256": want_sha,
+              "bitwise_equal_to_oracle": (want_sha == got_sha) if want_sha else None,
+              "host_api_W_equal": bool(np.array_equal(W_dev, W_host))}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import oracle as O
-        oop = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
-        oss = O.ScalingShift(*params.astuple())
-        t0 = time.perf_counter()
-        Wo, ro = O.phimv_block(oop, wl.t, wl.alpha, wl.V, wl.tol, oss)
-        dt = time.perf_counter() - t0
-        same = bool(np.array_equal(Wo, dW.cpu().numpy().T))
-        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": (f"one full oracle phimv_block of the same block (1 thread, "
-                          f"{dt:.2f} s); GPU W bitwise-equal to it: {same}")}
+    if N == 1 and not args.no_cpu_baseline:
+        O, oop, oss, src = oracle_setup(args, wl)
+        model, cores = cpu_info()
+        O.set_threads(cores)
+        ph = oracle_sample(O, oop, wl, oss, 3, 2 if rec.series_lens_F else 0)
+        tot = extrapolate(ph, rec.series_len_S, len(rec.series_lens_F))
+        spent = sum(v for k, v in ph.items() if not k.endswith("_run"))
+        cpu = {"value": 1.0 / tot, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": (f"oracle port on {cores} threads (row-parallel), CPU '{model}': setup + "
+                          f"{int(ph['s_terms_run'])} S terms + promotion"
+                          + (" + 2 recovery sweeps" if rec.series_lens_F else "") +
+                          f" + assembly timed by phase ({spent:.1f} s), extrapolated setup-free "
+                          f"to L_S={rec.series_len_S}: {tot:.1f} s per block")}
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": elapsed_max / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded generators, csrc/workloads.cpp)",
-            "config": config_dict(wl, args),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_phimv_block", "peak_source": peak_src,
-                         "alg_bytes_per_launch": alg, "kernel_ms": kernel_s * 1e3},
-            "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": int(wl.n * (wl.p + 1) * 8),
-                    "d2h_bytes_per_step": int(wl.n * wl.r * 8)},
-            "gpu_launches": int(launches),
-            "clocks": clk.summary(),
-            "selection_s": sel_s,
-            "run_record": {"s_effective": rec.s_effective, "series_len_S": rec.series_len_S,
-                           "n_sweeps": len(rec.series_lens_F), "matvecs": rec.matvecs},
-            "params": {"s": params.s, "xi": params.xi, "s0": params.s0, "r": params.r},
-        }
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if N > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, csrc/workloads.cpp)",
+        "config": config_dict(wl, args),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": kname,
+                     "peak_source": peak_src, "alg_bytes_per_launch": alg,
+                     "kernel_ms": kernel_s * 1e3,
+                     "timing": "CUDA events around the launch on the operator's stream "
+                               "(phx_last_eval_stats), mean over the timed steps"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": int(wl.n * (wl.p + 1) * 8),
+                "d2h_bytes_per_step": int(wl.n * wl.r * 8),
+                "host_buffers": "pinned (cudaHostAlloc)",
+                "pageable_value": e2e_pageable},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "selection_s": sel_s,
+        "parity": parity,
+        "run_record": {"s_effective": rec.s_effective, "series_len_S": rec.series_len_S,
+                       "n_sweeps": len(rec.series_lens_F), "matvecs": rec.matvecs},
+        "params": {"s": params.s, "xi": params.xi, "s0": params.s0, "r": params.r},
+        "kernel_variant": var,
+    }
+    print(json.dumps(line), flush=True)
     op.close()
     return 0
 

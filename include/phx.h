@@ -163,6 +163,23 @@ phx_status phx_phimv_block_device(phx_op op, int32_t r, const double* t, const d
                                   const phx_scaling_shift* params, double* d_W,
                                   phx_run_record* rec);
 
+/* Row parts of a (partitioned) operator: part q holds rows
+ * [row0, row0 + nrows) on `device`, evaluated on `stream`.  An unpartitioned
+ * operator is one part.  Any output pointer may be null. */
+phx_status phx_op_part_info(phx_op op, int32_t q, int64_t* row0, int64_t* nrows, int32_t* device,
+                            void** stream);
+
+/* The distributed device-resident form of phx_phimv_block_device: part q's
+ * rows of V (nrows_q x (p+1)) and of W (nrows_q x r) live on part q's device,
+ * column-major with leading dimension nrows_q (phx_op_part_info).  No copies:
+ * every part reads its V slice and writes its W slice in place.  (On a
+ * partitioned operator phx_phimv_block_device scatters V's rows from, and
+ * gathers W's rows to, the operator's first device with peer copies.) */
+phx_status phx_phimv_block_device_parts(phx_op op, int32_t r, const double* t, const double* alpha,
+                                        int32_t p, const double* const* d_V_parts, double tol,
+                                        const phx_scaling_shift* params, double* const* d_W_parts,
+                                        phx_run_record* rec);
+
 /* Single-combination evaluator phimv (phi_single.hpp:44, phi_single.cpp:38-127):
  * w = sum_j alpha^j phi_j(tA) v_j with the single variant's operation order.
  * exp_v0 / tail (n values each) may be NULL. */

@@ -79,9 +79,11 @@ def lib():
         L.orc_phimv_block.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int64, dp, dp, C.c_int32, dp,
                                       C.c_int64, C.c_double, C.POINTER(ScalingShiftC), dp,
                                       C.c_int64, i64p, i32p, C.c_int64, dp, C.c_int64, i64p]
-        L.orc_phimv_block_prefix.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int64, dp, dp,
-                                             C.c_int32, dp, C.c_int64, C.c_double,
-                                             C.POINTER(ScalingShiftC), C.c_int32, i32p]
+        L.orc_phimv_block_timed.argtypes = [C.c_int64, i64p, i32p, dp, C.c_int64, dp, dp,
+                                            C.c_int32, dp, C.c_int64, C.c_double,
+                                            C.POINTER(ScalingShiftC), C.c_int32, C.c_int32, dp,
+                                            i64p, dp]
+        L.orc_set_threads.argtypes = [C.c_int32]
         L.orc_phimv.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, C.c_double, C.c_int32, dp,
                                 C.c_int64, C.c_double, C.POINTER(ScalingShiftC), dp, dp, dp, i64p,
                                 i32p, C.c_int64]
@@ -341,17 +343,34 @@ def phimv_block(op: Csr, t, alpha, V, tol, params: ScalingShift, trace=False, le
     return W, _rec(rec4, lens)
 
 
-def phimv_block_prefix(op: Csr, t, alpha, V, tol, params: ScalingShift, max_s_terms: int):
-    """Timing sample: the evaluation stopped after max_s_terms S terms."""
+def set_threads(threads: int):
+    """Row-parallel loops for the CPU timing arms (results stay bitwise those
+    of one thread; the reference is single-threaded: 1 is its configuration)."""
+    lib().orc_set_threads(int(threads))
+
+
+def phimv_block_timed(op: Csr, t, alpha, V, tol, params: ScalingShift, max_s_terms: int = 0,
+                      max_sweeps: int = 0, term_times: bool = False):
+    """Timing sample: the evaluation with its phases timed, optionally stopped
+    after max_s_terms S terms / max_sweeps recovery sweeps.  Returns
+    (phases dict, RunRecord-like tuple[, per-S-term seconds])."""
     t = np.ascontiguousarray(t, dtype=np.float64)
     alpha = np.ascontiguousarray(alpha, dtype=np.float64)
     V = np.asfortranarray(np.asarray(V, dtype=np.float64).reshape(op.n, -1))
-    done = C.c_int32()
+    ph = np.zeros(9)
+    rec4 = np.zeros(4, dtype=np.int64)
+    tt = np.zeros(max(1, max_s_terms if max_s_terms > 0 else 512))
     pc = params.c()
-    _check(lib().orc_phimv_block_prefix(*op.args(), t.size, _d(t), _d(alpha), V.shape[1] - 1,
-                                        _d(V), op.n, tol, C.byref(pc), int(max_s_terms),
-                                        C.byref(done)))
-    return done.value
+    _check(lib().orc_phimv_block_timed(*op.args(), t.size, _d(t), _d(alpha), V.shape[1] - 1,
+                                       _d(V), op.n, tol, C.byref(pc), int(max_s_terms),
+                                       int(max_sweeps), _d(ph), rec4.ctypes.data_as(
+                                           C.POINTER(C.c_int64)), _d(tt) if term_times else None))
+    keys = ("setup", "s_terms", "s_terms_run", "promotion", "sweeps", "sweeps_run", "assembly",
+            "first_s_term", "first_sweep")
+    out = dict(zip(keys, ph.tolist())), tuple(int(x) for x in rec4)
+    if term_times:
+        return out + (tt[: int(ph[2])].copy(),)
+    return out
 
 
 def phimv(op: Csr, t, alpha, V, tol, params: ScalingShift, lens_cap=1 << 16):

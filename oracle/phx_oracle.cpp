@@ -35,6 +35,7 @@
 // ============================================================================
 #include <algorithm>
 #include <cfloat>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -78,17 +79,42 @@ struct Op {
   const double* v = nullptr;
 };
 
+// Row-parallel loops for the CPU timing arms (bench.py): orc_set_threads(T)
+// splits every n-sized loop of phimv_block into T contiguous row ranges.
+// Rows are independent and the maxima order-free, so results are bitwise
+// those of one thread (the reference itself is single-threaded; T = 1 is
+// its configuration and the default).
+static int g_threads = 1;
+template <class F>
+static void pfor(long n, F&& f) {
+  const long T = (n < 65536) ? 1 : long(g_threads);
+  if (T <= 1) {
+    f(0L, n);
+    return;
+  }
+  const long chunk = (n + T - 1) / T;
+  std::vector<std::thread> th;
+  for (long q = 1; q < T; ++q) {
+    const long lo = q * chunk, hi = std::min(n, lo + chunk);
+    if (lo < hi) th.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  f(0L, std::min(n, chunk));
+  for (auto& x : th) x.join();
+}
+
 // LinearOperator::apply (linop.cpp:10-24) for a CSR ApplyFn.
 static void apply_into(const Op& op, const double* X, long ldx, long k, double* Y,
                        long ldy) {
   for (long c = 0; c < k; ++c) {
     const double* x = X + size_t(c) * size_t(ldx);
     double* y = Y + size_t(c) * size_t(ldy);
-    for (long i = 0; i < op.n; ++i) {
-      double acc = 0.0;
-      for (int64_t e = op.rp[i]; e < op.rp[i + 1]; ++e) acc = acc + op.v[e] * x[op.ci[e]];
-      y[i] = acc;
-    }
+    pfor(op.n, [&](long lo, long hi) {
+      for (long i = lo; i < hi; ++i) {
+        double acc = 0.0;
+        for (int64_t e = op.rp[i]; e < op.rp[i + 1]; ++e) acc = acc + op.v[e] * x[op.ci[e]];
+        y[i] = acc;
+      }
+    });
   }
 }
 
@@ -141,13 +167,21 @@ static double tree_abs(const double* x, long lo, long len, long w) {
 // inf_norm (linop.cpp:51-54): max_i sum_c |X_ic|; 0 for an empty matrix.
 static double inf_norm(const double* X, long rows, long cols, long ld) {
   if (rows == 0 || cols == 0) return 0.0;
-  std::vector<double> row(static_cast<size_t>(cols));
   const long len = pow2ceil(cols);
+  std::vector<double> part(size_t(std::max(1, g_threads)) + 1, 0.0);
+  std::vector<long> starts;
+  pfor(rows, [&](long lo, long hi) {
+    std::vector<double> row(static_cast<size_t>(cols));
+    double m = 0.0;
+    for (long i = lo; i < hi; ++i) {
+      for (long c = 0; c < cols; ++c) row[size_t(c)] = X[size_t(i) + size_t(c) * size_t(ld)];
+      m = nan_max(m, tree_abs(row.data(), 0, len, cols));
+    }
+    const long chunk = rows < 65536 ? rows : (rows + g_threads - 1) / g_threads;
+    part[size_t(lo / std::max(1L, chunk))] = m;
+  });
   double m = 0.0;
-  for (long i = 0; i < rows; ++i) {
-    for (long c = 0; c < cols; ++c) row[size_t(c)] = X[size_t(i) + size_t(c) * size_t(ld)];
-    m = nan_max(m, tree_abs(row.data(), 0, len, cols));
-  }
+  for (double x : part) m = nan_max(m, x);
   return m;
 }
 static double inf_norm(const Mat& X) { return inf_norm(X.a.data(), X.rows, X.cols, X.rows); }
@@ -565,9 +599,23 @@ struct BlockResult {
   RunRecord rec;
 };
 
+// phases (timing arms only): [setup, S terms, S terms run, promotion,
+// sweeps, sweeps run, assembly, first S term, first sweep] seconds / counts.  max_s_terms / max_sweeps
+// > 0 stop the S series / the recovery after that many (a timing SAMPLE:
+// W is then not the evaluation's result).
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, const Mat& V,
                                double req_tol, const ScalingShift& params, Trace tr,
-                               int max_s_terms = 0) {
+                               int max_s_terms = 0, int max_sweeps = 0,
+                               double* phases = nullptr, double* term_times = nullptr) {
+  double tp = now_s();
+  auto lap = [&](int slot) {
+    const double x = now_s();
+    if (phases) phases[slot] += x - tp;
+    tp = x;
+  };
   // check_request (phi_block.cpp:15-27)
   if (t.empty()) throw std::invalid_argument("phimv_block: at least one abscissa required");
   if (alpha.size() != t.size()) throw std::invalid_argument("phimv_block: t and alpha lengths differ");
@@ -617,9 +665,18 @@ static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, con
       const double g = mu[size_t(i)] / double(s);
       const double* vs = V.col(src);
       double* dst = Vw.col(j * r + i);
-      for (long q = 0; q < n; ++q) dst[q] = vs[q] * g;
+      pfor(n, [&](long lo, long hi) {
+        for (long q = lo; q < hi; ++q) dst[q] = vs[q] * g;
+      });
     }
   }
+  const size_t nw = size_t(n) * size_t(w);
+  // elementwise pass over a whole block, row-parallel
+  auto each = [&](auto&& f) {
+    pfor(long(nw), [&](long lo, long hi) {
+      for (long q = lo; q < hi; ++q) f(size_t(q));
+    });
+  };
 
   Mat S = Vw, D = Vw;
   int k = 1;
@@ -628,16 +685,12 @@ static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, con
   double c2 = inf_norm(D);
   double nS = inf_norm(S);
   tr.add(0, c2, nS);
-  Mat Vn(n, w);
+  Mat Vn(n, w), Dn(n, w);
+  lap(0);
   while (c1 + c2 > tol * nS) {  // :93
-    if (max_s_terms > 0 && k - 1 >= max_s_terms) {
-      // timing sample only (bench.py reference arm): stop after a prefix
-      rec.series_len_S = k;
-      BlockResult early;
-      early.rec = std::move(rec);
-      return early;
-    }
+    if (max_s_terms > 0 && k - 1 >= max_s_terms) break;  // timing sample only
     if (k >= kSeriesCap) no_convergence("phimv_block", "series", kSeriesCap);
+    const double t_term = now_s();
     ++k;
     c1 = c2;
     sigma *= k;
@@ -647,38 +700,55 @@ static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, con
         const long c = j * r + i;
         const double* self = Vw.col(c);
         double* out = Vn.col(c);
+        const double ka = Ka[size_t(i)], kd = Kd[size_t(i)];
         if (j >= 2) {
-          const double* lo = Vw.col(c - r);
-          for (long q = 0; q < n; ++q) {
-            double acc = 0.0;
-            acc = acc + lo[q] * Ka[size_t(i)];
-            acc = acc + self[q] * Kd[size_t(i)];
-            out[q] = acc;
-          }
+          const double* lw = Vw.col(c - r);
+          pfor(n, [&](long lo, long hi) {
+            for (long q = lo; q < hi; ++q) {
+              double acc = 0.0;
+              acc = acc + lw[q] * ka;
+              acc = acc + self[q] * kd;
+              out[q] = acc;
+            }
+          });
         } else {
-          for (long q = 0; q < n; ++q) {
-            double acc = 0.0;
-            acc = acc + self[q] * Kd[size_t(i)];
-            out[q] = acc;
-          }
+          pfor(n, [&](long lo, long hi) {
+            for (long q = lo; q < hi; ++q) {
+              double acc = 0.0;
+              acc = acc + self[q] * kd;
+              out[q] = acc;
+            }
+          });
         }
       }
     std::swap(Vw, Vn);
-    D = shifted_apply(op, xi, D);  // :99
+    // D = shifted_apply(op, xi, D) (:99; linop.cpp:40-49), into a second block
+    apply_into(op, D.a.data(), n, w, Dn.a.data(), n);
+    if (xi != 0.0) each([&](size_t q) { Dn.a[q] = Dn.a[q] - xi * D.a[q]; });
+    std::swap(D, Dn);
     rec.matvecs += (p + 1) * r;
     for (int j = 0; j <= p; ++j)  // :101
       for (long i = 0; i < r; ++i) {
         double* dc = D.col(j * r + i);
-        for (long q = 0; q < n; ++q) dc[q] = dc[q] * tos[size_t(i)];
+        const double ts = tos[size_t(i)];
+        pfor(n, [&](long lo, long hi) {
+          for (long q = lo; q < hi; ++q) dc[q] = dc[q] * ts;
+        });
       }
-    for (size_t q = 0; q < D.a.size(); ++q) D.a[q] = D.a[q] + Vw.a[q];  // :102
-    c2 = inf_norm(D) / sigma;                                          // :103
+    each([&](size_t q) { D.a[q] = D.a[q] + Vw.a[q]; });  // :102
+    c2 = inf_norm(D) / sigma;                            // :103
     if (!std::isfinite(c2)) diverged("phimv_block", "series", k);
-    for (size_t q = 0; q < S.a.size(); ++q) S.a[q] = S.a[q] + D.a[q] / sigma;  // :105
+    each([&](size_t q) { S.a[q] = S.a[q] + D.a[q] / sigma; });  // :105
     nS = inf_norm(S);
     tr.add(1, c2, nS);
+    if (phases) {
+      phases[2] += 1.0;
+      if (phases[2] == 1.0) phases[7] = now_s() - tp;  // the first S term alone
+    }
+    if (term_times) term_times[k - 2] = now_s() - t_term;
   }
   rec.series_len_S = k;
+  lap(1);
 
   // promotion (:109-120)
   const long fcols = p == 0 ? r : 2 * r;
@@ -688,7 +758,8 @@ static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, con
   {
     Mat FL(n, r);
     std::copy(F.col(0), F.col(0) + size_t(n) * size_t(r), FL.col(0));
-    Mat AF = apply(op, FL);
+    Mat AF(n, r);
+    apply_into(op, FL.a.data(), n, r, AF.a.data(), n);
     rec.matvecs += r;
     for (long i = 0; i < r; ++i) {
       double* a = AF.col(i);
@@ -701,10 +772,19 @@ static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, con
     }
   }
 
+  lap(3);
   // recovery sweeps (:122-146)
   Mat& Sadv = S;
-  Mat E(n, fcols);
+  Mat E(n, fcols), Fn(n, fcols);
+  const size_t nf = size_t(n) * size_t(fcols);
+  auto eachf = [&](auto&& f) {
+    pfor(long(nf), [&](long lo, long hi) {
+      for (long q = lo; q < hi; ++q) f(size_t(q));
+    });
+  };
   for (long sweep = 1; sweep < s; ++sweep) {
+    if (max_sweeps > 0 && sweep > max_sweeps) break;  // timing sample only
+    if (phases) phases[5] += 1.0;
     E = F;
     int kk = 0;
     double d1 = std::numeric_limits<double>::infinity();
@@ -715,21 +795,28 @@ static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, con
       if (kk >= kRecoveryCap) no_convergence("phimv_block", "recovery sweep", kRecoveryCap);
       ++kk;
       d1 = d2;
-      F = shifted_apply(op, xi, F);
-      for (size_t q = 0; q < F.a.size(); ++q) F.a[q] = F.a[q] / double(kk);
+      // F = shifted_apply(op, xi, F) (linop.cpp:40-49), into a second block
+      apply_into(op, F.a.data(), n, fcols, Fn.a.data(), n);
+      if (xi != 0.0) eachf([&](size_t q) { Fn.a[q] = Fn.a[q] - xi * F.a[q]; });
+      std::swap(F, Fn);
+      const double dkk = double(kk);
+      eachf([&](size_t q) { F.a[q] = F.a[q] / dkk; });
       rec.matvecs += fcols;
       for (long c = 0; c < fcols; ++c) {
         const double sc = tos[size_t(c % r)];
         double* fc = F.col(c);
-        for (long q = 0; q < n; ++q) fc[q] = fc[q] * sc;
+        pfor(n, [&](long lo, long hi) {
+          for (long q = lo; q < hi; ++q) fc[q] = fc[q] * sc;
+        });
       }
       d2 = inf_norm(F);
       if (!std::isfinite(d2)) diverged("phimv_block", "recovery sweep", kk);
-      for (size_t q = 0; q < E.a.size(); ++q) E.a[q] = E.a[q] + F.a[q];
+      eachf([&](size_t q) { E.a[q] = E.a[q] + F.a[q]; });
       nE = inf_norm(E);
       tr.add(3, d2, nE);
     }
     rec.series_lens_F.push_back(kk);
+    if (phases && phases[5] == 1.0) phases[8] = -1.0;  // marker: first sweep's end below
     for (long c = 0; c < fcols; ++c) {  // :141-142
       const double sc = mu[size_t(c % r)];
       double* ec = E.col(c);
@@ -754,7 +841,9 @@ static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, con
         for (long q = 0; q < n; ++q) fr[q] = er[q] + sp[q];
       }
     std::copy(E.col(0), E.col(0) + size_t(n) * size_t(r), F.col(0));  // :145
+    if (phases && phases[8] == -1.0) phases[8] = now_s() - tp;  // the first sweep alone
   }
+  lap(4);
 
   BlockResult out;  // :148-154
   out.W = Mat(n, r);
@@ -765,6 +854,7 @@ static BlockResult phimv_block(const Op& op, const Vec& t, const Vec& alpha, con
       out.W(q, i) = wv;
     }
   out.rec = std::move(rec);
+  lap(6);
   return out;
 }
 
@@ -1592,22 +1682,31 @@ int orc_phimv_block(int64_t n, const int64_t* rp, const int32_t* ci, const doubl
   });
 }
 
-// Timing sample for the CPU reference arm: the same evaluation, stopped after
-// max_s_terms S-series terms (no promotion/recovery).  Returns the terms done.
-int orc_phimv_block_prefix(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
-                           int64_t r, const double* t, const double* alpha, int32_t p,
-                           const double* V, int64_t ldv, double tol,
-                           const orc_scaling_shift* params, int32_t max_s_terms,
-                           int32_t* terms_done) {
+// Timing sample for the CPU arms of bench.py: the same evaluation with its
+// phases timed (phases7[9]: setup, S terms, S terms run, promotion, sweeps,
+// sweeps run, assembly, first S term, first sweep), optionally stopped after max_s_terms S terms and
+// max_sweeps recovery sweeps (0: all).  rec4 as in orc_phimv_block;
+// term_times (optional, >= the S terms run): each S term's wall time.
+int orc_phimv_block_timed(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                          int64_t r, const double* t, const double* alpha, int32_t p,
+                          const double* V, int64_t ldv, double tol,
+                          const orc_scaling_shift* params, int32_t max_s_terms,
+                          int32_t max_sweeps, double* phases7, int64_t* rec4,
+                          double* term_times) {
   return guarded([&] {
     orc::Vec tv(t, t + r), av(alpha, alpha + r);
     orc::Mat Vm = wrap(V, n, p + 1, ldv);
     orc::Trace trc;
-    orc::BlockResult res =
-        orc::phimv_block(make_op(n, rp, ci, v), tv, av, Vm, tol, *params, trc, max_s_terms);
-    *terms_done = res.rec.series_len_S - 1;
+    for (int q = 0; q < 9; ++q) phases7[q] = 0.0;
+    orc::BlockResult res = orc::phimv_block(make_op(n, rp, ci, v), tv, av, Vm, tol, *params, trc,
+                                            max_s_terms, max_sweeps, phases7, term_times);
+    fill_rec(res.rec, rec4, nullptr, 0);
   });
 }
+
+// threads of the row-parallel loops (bench.py CPU arms); 1 = the reference's
+// configuration
+void orc_set_threads(int32_t threads) { orc::g_threads = threads < 1 ? 1 : threads; }
 
 int orc_phimv(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, double t, double alpha,
               int32_t p, const double* V, int64_t ldv, double tol, const orc_scaling_shift* params,

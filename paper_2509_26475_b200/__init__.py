@@ -79,7 +79,7 @@ ABI_SYMBOLS = (
     "phx_mm_read_csr", "phx_mm_write_csr", "phx_op_create_mm", "phx_block_series_direct",
     "phx_last_eval_mode",
     "phx_last_eval_variant",
-    "phx_tile_plan",
+    "phx_tile_plan", "phx_op_part_info", "phx_phimv_block_device_parts",
 )
 
 
@@ -145,6 +145,11 @@ def lib():
     L.phx_tile_plan.argtypes = [C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                 C.POINTER(C.c_uint8), C.POINTER(C.c_int32)]
+    L.phx_op_part_info.argtypes = [C.c_void_p, C.c_int32, i64p, i64p, i32p,
+                                   C.POINTER(C.c_void_p)]
+    L.phx_phimv_block_device_parts.argtypes = [C.c_void_p, C.c_int32, dp, dp, C.c_int32,
+                                               C.POINTER(C.c_void_p), C.c_double, C.POINTER(_SS),
+                                               C.POINTER(C.c_void_p), C.POINTER(_Rec)]
     L.phx_set_trace.argtypes = [C.c_int64]
     L.phx_get_trace.argtypes = [dp, C.c_int64, i64p]
     _LIB = L
@@ -302,6 +307,16 @@ class CsrOperator:
         except Exception:
             pass
 
+    def part_info(self, q: int) -> dict:
+        """Part q's rows [row0, row0 + nrows), its device and stream
+        (phx_op_part_info; an unpartitioned operator is one part)."""
+        row0, nrows, dev = C.c_int64(), C.c_int64(), C.c_int32()
+        st = C.c_void_p()
+        _check(lib().phx_op_part_info(self._h, int(q), C.byref(row0), C.byref(nrows),
+                                      C.byref(dev), C.byref(st)))
+        return {"row0": row0.value, "nrows": nrows.value, "device": dev.value,
+                "stream": int(st.value or 0)}
+
     def apply(self, X):
         X = np.asarray(X, dtype=np.float64)
         vec = X.ndim == 1
@@ -442,6 +457,22 @@ def phimv_block_device(op: CsrOperator, t, alpha, p, d_V_ptr: int, tol, params: 
     _check(lib().phx_phimv_block_device(op._h, t.size, _d(t), _d(alpha), int(p),
                                         C.c_void_p(d_V_ptr), float(tol), C.byref(ss),
                                         C.c_void_p(d_W_ptr), C.byref(rec)))
+    return _torec(rec, lens)
+
+
+def phimv_block_device_parts(op: CsrOperator, t, alpha, p, d_V_ptrs, tol, params: ScalingShift,
+                             d_W_ptrs) -> RunRecord:
+    """Distributed device-resident evaluation (phx_phimv_block_device_parts):
+    d_V_ptrs[q] / d_W_ptrs[q] are part q's row slices on its device,
+    column-major with leading dimension part_info(q)["nrows"]."""
+    t = np.ascontiguousarray(np.atleast_1d(t), dtype=np.float64)
+    alpha = np.ascontiguousarray(np.atleast_1d(alpha), dtype=np.float64)
+    rec, lens = _mkrec(_lens_cap(params, t))
+    ss = params._c()
+    vp = (C.c_void_p * len(d_V_ptrs))(*[C.c_void_p(int(x)) for x in d_V_ptrs])
+    wp = (C.c_void_p * len(d_W_ptrs))(*[C.c_void_p(int(x)) for x in d_W_ptrs])
+    _check(lib().phx_phimv_block_device_parts(op._h, t.size, _d(t), _d(alpha), int(p), vp,
+                                              float(tol), C.byref(ss), wp, C.byref(rec)))
     return _torec(rec, lens)
 
 

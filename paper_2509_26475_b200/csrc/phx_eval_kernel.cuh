@@ -52,6 +52,18 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsig
   return a > b ? a : b;
 }
 
+// system-scope loads of the cross-part mailboxes (another GPU writes them)
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <int V>
 struct Vio;
 // ld/st: default caching (gather sources and their producers);
@@ -755,18 +767,20 @@ __global__ void __launch_bounds__(kBlock, LAT ? 1
             mbx->a = A;
             mbx->b = Bv;
           }
+          // release at system scope: the mailboxes may be peer-GPU memory
+          // (NVLink), so the (a, b) writes above must be visible to another
+          // device before it sees gen
           __threadfence_system();
           for (int q = 0; q < ga.nparts; ++q)
-            atomicExch(&(ga.ptab[q].mbox + buf + my)->gen, gen);
+            atomicExch_system(&(ga.ptab[q].mbox + buf + my)->gen, gen);
         }
         unsigned long long A = 0, Bv = 0;
         for (int q = 0; q < ga.nparts; ++q) {
           const MailBox* mbx = T->mbox + (step & 1) * ga.nparts + q;
-          while (atomicAdd(const_cast<unsigned*>(&mbx->gen), 0u) < gen) {
+          while (ld_acquire_sys(&mbx->gen) < gen) {
           }
-          __threadfence_system();
-          A = umax64(A, __ldcg(&mbx->a));
-          Bv = umax64(Bv, __ldcg(&mbx->b));
+          A = umax64(A, ld_relaxed_sys(&mbx->a));
+          Bv = umax64(Bv, ld_relaxed_sys(&mbx->b));
         }
         gmax[0] = from_bits(A);
         gmax[1] = from_bits(Bv);

@@ -687,6 +687,10 @@ struct EvalIn {
   double* h_exp_v0;
   double* h_tail;
   int32_t slot;  // control-block slot (kCtlSlots): evaluations in flight at once
+  // partitioned operators: per-part device slices (V: nrows x (p+1), W:
+  // nrows x r, column-major with leading dimension nrows, on the part's device)
+  const double* const* dVp = nullptr;
+  double* const* dWp = nullptr;
 };
 
 
@@ -715,8 +719,12 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
   const int32_t r = base.r, p = base.p, ldb = base.ldb, ldf = base.ldf;
   if (in.single || in.h_exp_v0 || in.h_tail)
     throw_phx(PHX_EINVAL, "phimv: the single-combination evaluator needs an unpartitioned operator");
-  if (!in.hV || !in.hW)
-    throw_phx(PHX_EINVAL, "phimv_block: a partitioned operator takes host V and W buffers");
+  // V in / W out: host buffers (H2D / D2H per part), one device block on the
+  // operator's device (peer copies of each part's rows over NVLink), or the
+  // parts' own device slices (no copies: the distributed device-resident form)
+  const bool host_io = in.hV && in.hW, dev_io = in.dV && in.dW, parts_io = in.dVp && in.dWp;
+  if (!(host_io || dev_io || parts_io))
+    throw_phx(PHX_EINVAL, "phimv_block: V and W must both be host, device or per-part buffers");
   const size_t ncoef = coef.size();
   std::vector<phx::PartTab> tab(static_cast<size_t>(P));
   for (int q = 0; q < P; ++q) {
@@ -729,7 +737,7 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     T.rp = d.rp;
     T.ci = d.ci;
     T.av = d.av;
-    double* dV = d.V.as<double>(nr * size_t(p + 1));
+    double* dV = parts_io ? const_cast<double*>(in.dVp[q]) : d.V.as<double>(nr * size_t(p + 1));
     T.V = dV;
     T.Vw = d.Vw.as<double>(nr * size_t(ldb));
     T.D0 = d.D0.as<double>(nr * size_t(ldb));
@@ -738,14 +746,18 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     T.F0 = d.F0.as<double>(nr * size_t(ldf));
     T.F1 = d.F1.as<double>(nr * size_t(ldf));
     T.E = d.E.as<double>(nr * size_t(ldf));
-    T.W = d.W.as<double>(nr * size_t(r));
+    T.W = parts_io ? in.dWp[q] : d.W.as<double>(nr * size_t(r));
     T.slots = d.slots.as<unsigned long long>(12);
     T.arrive = d.arrive.as<unsigned>(3);
     T.mbox = d.mbox.as<phx::MailBox>(2 * size_t(P));  // [step parity][part]
     T.row0 = int32_t(d.row0);
     T.nrows = int32_t(d.nrows);
-    PHX_CUDA(cudaMemcpy2DAsync(dV, nr * 8, in.hV + d.row0, size_t(in.ldv) * 8, nr * 8,
-                               size_t(p + 1), cudaMemcpyHostToDevice, d.stream));
+    if (host_io)
+      PHX_CUDA(cudaMemcpy2DAsync(dV, nr * 8, in.hV + d.row0, size_t(in.ldv) * 8, nr * 8,
+                                 size_t(p + 1), cudaMemcpyHostToDevice, d.stream));
+    else if (dev_io)  // peer copy of the part's rows (UVA)
+      PHX_CUDA(cudaMemcpy2DAsync(dV, nr * 8, in.dV + d.row0, size_t(op->n) * 8, nr * 8,
+                                 size_t(p + 1), cudaMemcpyDefault, d.stream));
     PHX_CUDA(cudaMemsetAsync(T.slots, 0, 12 * sizeof(unsigned long long), d.stream));
     PHX_CUDA(cudaMemsetAsync(T.arrive, 0, 3 * sizeof(unsigned), d.stream));
     PHX_CUDA(cudaMemsetAsync(T.mbox, 0, 2 * size_t(P) * sizeof(phx::MailBox), d.stream));
@@ -811,13 +823,26 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
               phx::eval_cluster_smem(int32_t(max_rows), int32_t(max_nnz), cl_tile, ldb, ldf) <=
                   size_t(optin);
   }
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // per launch group: start / end events on its device (the evaluation's
+  // time is the slowest group's)
+  struct EvPair {
+    int dev = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+  };
   struct EvGuard {  // the timing events are released on every exit path
-    cudaEvent_t& e;
+    std::vector<EvPair>& v;
     ~EvGuard() {
-      if (e) cudaEventDestroy(e);
+      for (EvPair& x : v) {
+        cudaSetDevice(x.dev);
+        if (x.e0) cudaEventDestroy(x.e0);
+        if (x.e1) cudaEventDestroy(x.e1);
+      }
     }
-  } g0{e0}, g1{e1};
+  };
+  std::vector<EvPair> evs(groups.size());
+  EvGuard evguard{evs};
+  int dev_prev = 0;
+  PHX_CUDA(cudaGetDevice(&dev_prev));
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     const Group& g = groups[gi];
     PartDev& d = op->parts[size_t(g.plo)];
@@ -842,15 +867,17 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     a.trace = (g.plo == 0 && trace_cap > 0) ? d.trace.as<double>(size_t(trace_cap)) : nullptr;
     a.trace_cap = int32_t(trace_cap);
     PHX_CUDA(cudaMemsetAsync(a.status, 0, 8 * sizeof(int32_t), d.stream));
+    EvPair& ev = evs[gi];
+    ev.dev = d.dev;
+    PHX_CUDA(cudaEventCreate(&ev.e0));
+    PHX_CUDA(cudaEventCreate(&ev.e1));
     if (cluster) {
       a.cl_rows = int32_t(max_rows);
       a.cl_nnz = int32_t(max_nnz);
       a.tile = cl_tile;
-      PHX_CUDA(cudaEventCreate(&e0));
-      PHX_CUDA(cudaEventCreate(&e1));
-      PHX_CUDA(cudaEventRecord(e0, d.stream));
+      PHX_CUDA(cudaEventRecord(ev.e0, d.stream));
       PHX_CUDA(phx::launch_phimv_block_cluster(a, P, block, d.stream));
-      PHX_CUDA(cudaEventRecord(e1, d.stream));
+      PHX_CUDA(cudaEventRecord(ev.e1, d.stream));
       {
         std::lock_guard<std::mutex> lk(g_trace_mu);
         g_last_mode = 2;
@@ -863,13 +890,9 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     for (int q = g.plo; q < g.plo + g.pcount; ++q)
       most = std::max<int64_t>(most, (op->parts[size_t(q)].nrows + a.tile - 1) / a.tile);
     const int per = int(std::max<int64_t>(1, std::min<int64_t>(max_blocks / g.pcount, most)));
-    if (gi == 0) {
-      PHX_CUDA(cudaEventCreate(&e0));
-      PHX_CUDA(cudaEventCreate(&e1));
-      PHX_CUDA(cudaEventRecord(e0, d.stream));
-    }
+    PHX_CUDA(cudaEventRecord(ev.e0, d.stream));
     PHX_CUDA(phx::launch_phimv_block(a, per * g.pcount, block, d.stream));
-    if (gi == 0) PHX_CUDA(cudaEventRecord(e1, d.stream));
+    PHX_CUDA(cudaEventRecord(ev.e1, d.stream));
     {
       std::lock_guard<std::mutex> lk(g_trace_mu);
       g_last_mode = 1;
@@ -882,9 +905,13 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     DeviceGuard guard(d0.dev);
     for (int q = g.plo; q < g.plo + g.pcount; ++q) {
       PartDev& d = op->parts[size_t(q)];
-      PHX_CUDA(cudaMemcpy2DAsync(in.hW + d.row0, size_t(in.ldw) * 8, d.W.p, size_t(d.nrows) * 8,
-                                 size_t(d.nrows) * 8, size_t(r), cudaMemcpyDeviceToHost,
-                                 d0.stream));
+      if (host_io)
+        PHX_CUDA(cudaMemcpy2DAsync(in.hW + d.row0, size_t(in.ldw) * 8, d.W.p, size_t(d.nrows) * 8,
+                                   size_t(d.nrows) * 8, size_t(r), cudaMemcpyDeviceToHost,
+                                   d0.stream));
+      else if (dev_io)
+        PHX_CUDA(cudaMemcpy2DAsync(in.dW + d.row0, size_t(op->n) * 8, d.W.p, size_t(d.nrows) * 8,
+                                   size_t(d.nrows) * 8, size_t(r), cudaMemcpyDefault, d0.stream));
     }
     int32_t st[8];
     PHX_CUDA(cudaMemcpyAsync(st, d0.status.p, sizeof(st), cudaMemcpyDeviceToHost, d0.stream));
@@ -899,11 +926,14 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
         g_trace_len = st[5];
         PHX_CUDA(cudaMemcpy(g_trace.data(), d0.trace.p, size_t(trace_cap) * 8, cudaMemcpyDeviceToHost));
       }
-      PHX_CUDA(cudaEventElapsedTime(ms_out, e0, e1));
     } else if (st[0] != h_status[0] || st[2] != h_status[2]) {
       throw_phx(PHX_ECUDA, "partitioned evaluation: parts disagree on the stopping decisions");
     }
+    float ms = 0.f;
+    PHX_CUDA(cudaEventElapsedTime(&ms, evs[gi].e0, evs[gi].e1));
+    *ms_out = gi == 0 ? ms : std::max(*ms_out, ms);
   }
+  PHX_CUDA(cudaSetDevice(dev_prev));
 }
 
 void finish_eval(const PendingEval& pe, phx_run_record* rec);
@@ -1496,6 +1526,8 @@ int32_t phx_op_nparts(phx_op op) { return op ? op->nparts : 0; }
 
 phx_status phx_op_destroy(phx_op op) {
   if (!op) return PHX_OK;
+  int entry_dev = -1;  // the caller's device, restored on return
+  cudaGetDevice(&entry_dev);
   for (PartDev& d : op->parts) {
     cudaSetDevice(d.dev);
     if (d.stream) cudaStreamSynchronize(d.stream);
@@ -1532,8 +1564,9 @@ phx_status phx_op_destroy(phx_op op) {
     if (op->ev0) cudaEventDestroy(op->ev0);
     if (op->ev1) cudaEventDestroy(op->ev1);
     if (op->stream) cudaStreamDestroy(op->stream);
-    if (prev >= 0) cudaSetDevice(prev);
+    (void)prev;
   }
+  if (entry_dev >= 0) cudaSetDevice(entry_dev);
   delete op;
   return PHX_OK;
 }
@@ -1723,6 +1756,56 @@ phx_status phx_phimv_block_device(phx_op op, int32_t r, const double* t, const d
     in.tol = tol;
     in.params = *params;
     in.dW = d_W;
+    evaluate(op, in, rec);
+  });
+}
+
+phx_status phx_op_part_info(phx_op op, int32_t q, int64_t* row0, int64_t* nrows, int32_t* device,
+                            void** stream) {
+  return guarded([&] {
+    if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    if (q < 0 || q >= op->nparts) throw_phx(PHX_EINVAL, "phx_op_part_info: part index out of range");
+    if (op->nparts == 1) {
+      if (row0) *row0 = 0;
+      if (nrows) *nrows = op->n;
+      if (device) *device = op->device;
+      if (stream) *stream = op->stream;
+      return;
+    }
+    const PartDev& d = op->parts[size_t(q)];
+    if (row0) *row0 = d.row0;
+    if (nrows) *nrows = d.nrows;
+    if (device) *device = d.dev;
+    if (stream) *stream = d.stream;
+  });
+}
+
+phx_status phx_phimv_block_device_parts(phx_op op, int32_t r, const double* t, const double* alpha,
+                                        int32_t p, const double* const* d_V_parts, double tol,
+                                        const phx_scaling_shift* params, double* const* d_W_parts,
+                                        phx_run_record* rec) {
+  return guarded([&] {
+    if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
+    check_block_request(op, r, t, alpha, p, nullptr, op->n, false);
+    if (!params || !d_V_parts || !d_W_parts) throw_phx(PHX_EINVAL, "phimv_block: null argument");
+    for (int q = 0; q < op->nparts; ++q)
+      if (!d_V_parts[q] || !d_W_parts[q]) throw_phx(PHX_EINVAL, "phimv_block: null argument");
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard guard(op->device);
+    EvalIn in{};
+    in.r = r;
+    in.p = p;
+    in.t = t;
+    in.alpha = alpha;
+    in.tol = tol;
+    in.params = *params;
+    if (op->nparts == 1) {
+      in.dV = d_V_parts[0];
+      in.dW = d_W_parts[0];
+    } else {
+      in.dVp = d_V_parts;
+      in.dWp = d_W_parts;
+    }
     evaluate(op, in, rec);
   });
 }

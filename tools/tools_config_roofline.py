@@ -20,8 +20,9 @@ for arg in [x for x in sys.argv[1:] if not x.startswith("--")]:
     if "--once" not in sys.argv:
         res = P.phimv_block(op, req)
         ms, steps = P.last_eval_stats()
-    b = bench.algorithmic_bytes(wl, res.stats)
-    print(json.dumps({"cfg": cfg, "n": wl.n, "nnz": wl.nnz, "p": wl.p, "r": wl.r, "kernel_ms": ms,
+    bulk = P.last_eval_variant()["dynamic_tail"] == 2
+    b = bench.algorithmic_bytes(wl, res.stats, bulk)
+    print(json.dumps({"cfg": cfg, "n": wl.n, "nnz": wl.nnz, "p": wl.p, "r": wl.r, "kernel": "k_phimv_bulk" if bulk else "k_phimv_block", "kernel_ms": ms,
                       "grid_steps": steps, "s_eff": res.stats.s_effective,
                       "L_S": res.stats.series_len_S, "sweeps": len(res.stats.series_lens_F),
                       "alg_bytes": b, "alg_GBps": b / (ms * 1e-3) / 1e9,
