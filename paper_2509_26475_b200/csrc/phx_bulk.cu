@@ -56,6 +56,16 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "r"(parity)
       : "memory");
 }
+// the same wait with a suspend-time hint: a warp whose phase has not
+// completed sleeps (up to the hint) instead of re-issuing the probe
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(su32(b)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
@@ -115,6 +125,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cta = int(blockIdx.x), ncta = int(gridDim.x);
   const int NS = a.bulk_ns, SB = a.bulk_stage_bytes;
+  const bool sleepw = (a.bulk_flags & 2) != 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bar_full[s], 1);
@@ -190,9 +201,12 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
 
   // ================= the bulk phases: S term (kind 0) / recovery term (kind 1)
   // X: gather source (width `width`), A: stream A (Vw | E), B: stream B (S)
-  auto bulk_phase = [&](int kind, int width, const double* X, const double* A, const double* B,
-                        auto&& epi) -> unsigned long long {
-    const BulkStage L = bulk_stage(a.plan_rows, a.plan_emax, width, B != nullptr);
+  // G: lanes per row of the output layout, ow: output width, width: row
+  // width of the gather source X; gath(row_ptrs...) accumulates a row's
+  // entries, epi(...) finishes it
+  auto bulk_phase = [&](int G, int ow, int width, const double* X, const double* A, const double* B,
+                        auto&& gath, auto&& epi) -> unsigned long long {
+    const BulkStage L = bulk_stage(a.plan_rows, a.plan_emax, width, (A ? 1 : 0) + (B ? 1 : 0));
     unsigned long long* ctr = a.slots + 4 * (step % 3) + 2;
     unsigned long long mx = 0;
     if (warp == kProd) {
@@ -202,7 +216,10 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
       // is issued, so neither latency is on the producer's path.
       unsigned long long pfirst = 0, plast = 0;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pfirst));
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(plast));
+      if (a.bulk_flags & 1)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(plast));
+      else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(plast));
       auto fetch = [&](int pos, int buf) {
         const int q = pos + (lane >> 2);
         if (lane < 4 * kPB && q < nblk)
@@ -227,7 +244,10 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
           const int t = posA + j < nblk ? posA + j : -1;
           const int* d = pdesc[cur][j];
           const int s = kpipe % NS;
-          mbar_wait(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
+          if (sleepw)
+            mbar_wait_sleep(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
+          else
+            mbar_wait(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
           unsigned char* st = ring + size_t(s) * size_t(SB);
           unsigned long long* bf = &bar_full[s];
           const int nsgl = t >= 0 ? d[1] : 0;
@@ -243,7 +263,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
               const int c0 = e_lo & ~15, cn = (e_hi - c0 + 15) & ~15;  // slot bytes
               const int a0 = e_lo & ~1, an = (e_hi - a0 + 1) & ~1;    // values (16 B granules)
               const int rn = (rows + 1 + 3) & ~3;                     // row_ptr entries
-              unsigned nrow = unsigned(whi - wlo + nsgl + (B ? 2 : 1) * rows);
+              unsigned nrow = unsigned(whi - wlo + nsgl + ((A ? 1 : 0) + (B ? 1 : 0)) * rows);
               for (int g = 0; g < ng; ++g) nrow += unsigned(d[12 + g] & 0xffff);
               const unsigned rb = unsigned(width) * 8u;
               mbar_arrive_tx(bf, unsigned(rn * 4 + cn + an * 8) + nrow * rb);
@@ -256,7 +276,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
                 bulk_g2s(st + L.dr + dst * int(rb), X + size_t(d[8 + g]) * width, unsigned(cnt) * rb,
                          bf, plast);
               }
-              bulk_g2s(st + L.sa, A + size_t(base) * width, unsigned(rows) * rb, bf, pfirst);
+              if (A) bulk_g2s(st + L.sa, A + size_t(base) * width, unsigned(rows) * rb, bf, pfirst);
               if (B) bulk_g2s(st + L.sb, B + size_t(base) * width, unsigned(rows) * rb, bf, pfirst);
             }
           }
@@ -280,13 +300,15 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
       return mx;
     }
     // ---- consumers
-    const int G = kind == 0 ? GS : GF;
     const int gpw = 32 / G, g = lane / G, lg = lane % G;
     const int c = 2 * lg;
-    const bool cv = c < width;
+    const bool cv = c < ow;
     for (;;) {
       const int s = kpipe % NS;
-      mbar_wait(&bar_full[s], (kpipe / NS) & 1);
+      if (sleepw)
+        mbar_wait_sleep(&bar_full[s], (kpipe / NS) & 1);
+      else
+        mbar_wait(&bar_full[s], (kpipe / NS) & 1);
       const unsigned char* st = ring + size_t(s) * size_t(SB);
       const int t = *reinterpret_cast<const int*>(st + L.hdr);
       ++kpipe;
@@ -304,16 +326,8 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
           const int rr = r0 + g;
           const bool v = rr < rows && cv;
           double a0 = 0.0, a1 = 0.0;
-          if (v) {
-            const int e0 = rps[rr] - e_lo, e1 = rps[rr + 1] - e_lo;
-            for (int e = e0; e < e1; ++e) {
-              const double2 x = *reinterpret_cast<const double2*>(dr + int(sls[e]) * width + c);
-              const double av = avs[e];
-              a0 = a0 + av * x.x;
-              a1 = a1 + av * x.y;
-            }
-          }
-          const double* self = dr + (base + rr - wlo) * width + c;  // the row itself (window)
+          if (v) gath(dr, sls, avs, rps[rr] - e_lo, rps[rr + 1] - e_lo, c, a0, a1);
+          const double* self = dr + (base + rr - wlo) * width;  // the row itself (window)
           const unsigned long long m =
               epi(v, rr < rows, base + rr, c, a0, a1, self, sa + rr * width + c, sb + rr * width + c, lg, G);
           mx = umax64(mx, m);
@@ -326,37 +340,71 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     return mx;
   };
 
+  // gathers: columns (c, c+1) of every entry's staged row, in CSR order
+  auto gath_pair = [&](int width) {
+    return [width](const double* dr, const unsigned char* sls, const double* avs, int e0, int e1,
+                   int c, double& a0, double& a1) {
+      for (int e = e0; e < e1; ++e) {
+        const double2 x = *reinterpret_cast<const double2*>(dr + int(sls[e]) * width + c);
+        const double av = avs[e];
+        a0 = a0 + av * x.x;
+        a1 = a1 + av * x.y;
+      }
+    };
+  };
+
   // ================= init: row-major V into D0, ||Vw_1||, max|V| (phi_block.cpp:76-92)
+  // D0 holds V row-major with an even stride p1e (pad column 0): its rows
+  // are whole 16-byte granules, so the first S term stages them with bulk
+  // copies.  Lane lg of a row's group loads V columns lg and lg + G; the
+  // lanes' Vw_1 columns (V[src] * g) come by shuffle.  NB row groups per warp
+  // have their loads in flight together.
+  const int p1e = (p1 + 1) & ~1;
   unsigned long long m0 = 0, mv = 0;
   {
-    const int c = 2 * (lane % GS);
+    constexpr int NB = 4;
+    const int G = GS, gpw = 32 / G, g = lane / G, lg = lane % G, c = 2 * lg;
     int src[2];
     double gv[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int cc = c + e;
-      const int j = cc / r, i = cc - j * r;
+      const int j = cc < w ? cc / r : 0, i = cc < w ? cc - j * r : 0;
       src[e] = j == 0 ? 0 : p + 1 - j;
       gv[e] = cc < w ? __ldg(a.g + i) : 0.0;
     }
-    plain_rows(GS, [&](int row, bool rv, int lg) {
-      double ax[1][2];
+    const int nwarps = ncta * kBW, ngroups = (n + gpw - 1) / gpw;
+    for (int q0 = cta * kBW + warp; q0 < ngroups; q0 += NB * nwarps) {
+      double v0[NB], v1[NB];
+      int rowb[NB];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        double x = 0.0;
-        if (rv && c + e < w) {
-          const double vv = __ldg(a.V + size_t(src[e]) * size_t(n) + row);
-          mv = umax64(mv, abs_bits(vv));
-          x = vv * gv[e];
-        }
-        ax[0][e] = fabs(x);
+      for (int b = 0; b < NB; ++b) {
+        const int q = q0 + b * nwarps, row = q * gpw + g;
+        rowb[b] = (q < ngroups && row < n) ? row : -1;
+        v0[b] = (rowb[b] >= 0 && lg < p1) ? __ldg(a.V + size_t(lg) * size_t(n) + row) : 0.0;
+        v1[b] = (rowb[b] >= 0 && lg + G < p1) ? __ldg(a.V + size_t(lg + G) * size_t(n) + row) : 0.0;
       }
-      if (rv)
-        for (int col = lg; col < p1; col += GS)
-          a.D0[size_t(row) * size_t(p1) + col] = __ldg(a.V + size_t(col) * size_t(n) + row);
-      const double rsum = group_rowsum<1, 2>(ax, GS, 1);
-      if (rv) m0 = umax64(m0, abs_bits(rsum));
-    });
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int row = rowb[b];
+        if (row >= 0) {
+          if (lg < p1) mv = umax64(mv, abs_bits(v0[b]));
+          if (lg + G < p1) mv = umax64(mv, abs_bits(v1[b]));
+          if (lg < p1e) a.D0[size_t(row) * size_t(p1e) + lg] = v0[b];
+          if (lg + G < p1e) a.D0[size_t(row) * size_t(p1e) + lg + G] = v1[b];
+        }
+        double ax[1][2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double x0 = __shfl_sync(kFull, v0[b], g * G + (src[e] % G));
+          const double x1 = __shfl_sync(kFull, v1[b], g * G + (src[e] % G));
+          const double vv = src[e] < G ? x0 : x1;
+          ax[0][e] = (row >= 0 && c + e < w) ? fabs(vv * gv[e]) : 0.0;
+        }
+        const double rsum = group_rowsum<1, 2>(ax, G, 1);
+        if (row >= 0) m0 = umax64(m0, abs_bits(rsum));
+      }
+    }
   }
   double mD, mSn;
   sync_step(m0, mv, mD, mSn);
@@ -402,11 +450,10 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     ++k;
     c1 = c2;
     sigma *= k;
-    unsigned long long mdb = 0;
+    int src[2], srcl[2], jj[2];
+    double gg[2], kd[2], ka[2], tos[2];
     {
       const int c = 2 * (lane % GS);
-      int src[2], srcl[2], jj[2];
-      double gg[2], kd[2], ka[2], tos[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int cc = c + e;
@@ -420,58 +467,50 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
         ka[e] = ok ? __ldg(a.colKa + cc) : 0.0;
         tos[e] = ok ? __ldg(a.colTos + cc) : 0.0;
       }
-      plain_rows(GS, [&](int row, bool rv, int) {
-        const bool vv = rv && c < w;
-        double acc[2] = {0.0, 0.0};
-        if (vv) {
-          const int e1 = __ldg(a.rp + row + 1);
-          for (int e = __ldg(a.rp + row); e < e1; e += 8) {
-            double x0[8], x1[8], av[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              x0[u] = x1[u] = av[u] = 0.0;
-              if (e + u < e1) {
-                const double* vr = a.D0 + size_t(__ldg(a.ci + e + u)) * size_t(p1);
-                av[u] = __ldg(a.av + e + u);
-                x0[u] = vr[src[0]];
-                x1[u] = vr[src[1]];
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (e + u < e1) {
-                acc[0] = acc[0] + av[u] * (x0[u] * gg[0]);
-                acc[1] = acc[1] + av[u] * (x1[u] * gg[1]);
-              }
-          }
-        }
-        double ad[1][2], vn[2], dn[2], sn[2];
-        const double* vo = a.D0 + size_t(rv ? row : 0) * size_t(p1);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const double vw = vv ? vo[src[e]] * gg[e] : 0.0;  // Vw_1 = D_1 = S_1
-          const double vwl = (vv && jj[e] >= 2) ? vo[srcl[e]] * gg[e] : 0.0;
-          double g2 = 0.0;  // Vw = Vw * Kiter (:98)
-          if (jj[e] >= 2) g2 = g2 + vwl * ka[e];
-          g2 = g2 + vw * kd[e];
-          vn[e] = g2;
-          double y = acc[e];  // D = (A - xi I) D (:99), * t_i/s, + Vw
-          if (has_xi) y = y - a.xi * vw;
-          y = y * tos[e];
-          dn[e] = y + g2;
-          sn[e] = vw + dn[e] / sigma;  // S += D/sigma (:105)
-          ad[0][e] = vv ? fabs(dn[e]) : 0.0;
-        }
-        if (vv) {
-          const unsigned o = unsigned(row) * ldb + c;
-          __stcs(reinterpret_cast<double2*>(a.Vw + o), make_double2(vn[0], vn[1]));
-          __stcs(reinterpret_cast<double2*>(Dn + o), make_double2(dn[0], dn[1]));
-          __stcs(reinterpret_cast<double2*>(a.S + o), make_double2(sn[0], sn[1]));
-        }
-        const double rd = group_rowsum<1, 2>(ad, GS, 1);
-        if (rv) mdb = umax64(mdb, abs_bits(rd));
-      });
     }
+    double* const Dn1 = Dn;
+    const double sig1 = sigma;
+    const unsigned long long mdb = bulk_phase(
+        GS, w, p1e, a.D0, nullptr, nullptr,
+        // acc = sum_e av_e * Vw_1[col_e] = av_e * fl(V[col_e][src] * g)
+        [&](const double* dr, const unsigned char* sls, const double* avs, int e0, int e1, int,
+            double& a0, double& a1) {
+          for (int e = e0; e < e1; ++e) {
+            const double* vr = dr + int(sls[e]) * p1e;
+            const double av = avs[e];
+            a0 = a0 + av * (vr[src[0]] * gg[0]);
+            a1 = a1 + av * (vr[src[1]] * gg[1]);
+          }
+        },
+        [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
+            const double*, const double*, int, int G) -> unsigned long long {
+          double ad[1][2] = {{0.0, 0.0}};
+          if (v) {
+            const double acc[2] = {a0, a1};
+            double vn[2], dn[2], sn[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const double vw = self[src[e]] * gg[e];  // Vw_1 = D_1 = S_1
+              const double vwl = jj[e] >= 2 ? self[srcl[e]] * gg[e] : 0.0;
+              double g2 = 0.0;  // Vw = Vw * Kiter (:98)
+              if (jj[e] >= 2) g2 = g2 + vwl * ka[e];
+              g2 = g2 + vw * kd[e];
+              vn[e] = g2;
+              double y = acc[e];  // D = (A - xi I) D (:99), * t_i/s, + Vw
+              if (has_xi) y = y - a.xi * vw;
+              y = y * tos[e];
+              dn[e] = y + g2;
+              sn[e] = vw + dn[e] / sig1;  // S += D/sigma (:105)
+              ad[0][e] = fabs(dn[e]);
+            }
+            const unsigned o = unsigned(row) * ldb + c;
+            __stcs(reinterpret_cast<double2*>(a.Vw + o), make_double2(vn[0], vn[1]));
+            __stcs(reinterpret_cast<double2*>(Dn1 + o), make_double2(dn[0], dn[1]));
+            __stcs(reinterpret_cast<double2*>(a.S + o), make_double2(sn[0], sn[1]));
+          }
+          const double rd = group_rowsum<1, 2>(ad, G, 1);
+          return rvalid ? abs_bits(rd) : 0ull;
+        });
     double maxD, dmy;
     sync_step(mdb, mdb, maxD, dmy);
     c2 = maxD / sigma;  // :103
@@ -503,7 +542,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
         const int cc = c + e;
         const int j = cc / r, i = cc - j * r;
         const int sc = j == 0 ? 0 : p + 1 - j;
-        x[e] = a.D0[size_t(row) * size_t(p1) + sc] * __ldg(a.g + i);
+        x[e] = a.D0[size_t(row) * size_t(p1e) + sc] * __ldg(a.g + i);
       }
       *reinterpret_cast<double2*>(a.S + (unsigned(row) * ldb + c)) = make_double2(x[0], x[1]);
     });
@@ -553,7 +592,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     double* const Dnn = Dn;
     const double sig = sigma;
     const unsigned long long mdb = bulk_phase(
-        0, w, Dc, a.Vw, a.S,
+        GS, w, w, Dc, a.Vw, a.S, gath_pair(w),
         [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
             const double* pa, const double* pb, int, int G) -> unsigned long long {
           double ad[1][2] = {{0.0, 0.0}};
@@ -568,7 +607,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
               if (jjS[1] >= 2) vl.y = pa[1 - r];
             }
             double2 ds = make_double2(0.0, 0.0);
-            if (has_xi) ds = *reinterpret_cast<const double2*>(self);
+            if (has_xi) ds = *reinterpret_cast<const double2*>(self + c);
             const double vwv[2] = {vw.x, vw.y}, vlv[2] = {vl.x, vl.y}, sov[2] = {so.x, so.y},
                          dsv[2] = {ds.x, ds.y}, acc[2] = {a0, a1};
             double vn[2], dn[2], sn[2];
@@ -627,77 +666,61 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
   double* Fc = a.F0;
   double* Fn = a.F1;
   const bool sweeps = a.s_eff > 1;
-  unsigned long long mf = 0;
-  {
-    const int c = 2 * (lane % GF);
-    plain_rows(GF, [&](int row, bool rv, int) {
+  const unsigned long long mf = bulk_phase(
+      GF, fc, w, a.S, nullptr, nullptr,
       // gathers S block-0 columns (left F columns live at the same column
       // index in S); a pair straddling the left/right split gathers one extra
       // column, unused
-      const bool vl = rv && c < r;
-      double acc[2] = {0.0, 0.0};
-      if (vl) {
-        const int e1 = __ldg(a.rp + row + 1);
-        for (int e = __ldg(a.rp + row); e < e1; e += 8) {
-          double2 x[8];
-          double av[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            x[u] = make_double2(0.0, 0.0);
-            av[u] = 0.0;
-            if (e + u < e1) {
-              av[u] = __ldg(a.av + e + u);
-              x[u] = *reinterpret_cast<const double2*>(a.S + size_t(__ldg(a.ci + e + u)) * ldb + c);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (e + u < e1) {
-              acc[0] = acc[0] + av[u] * x[u].x;
-              acc[1] = acc[1] + av[u] * x[u].y;
-            }
+      [&](const double* dr, const unsigned char* sls, const double* avs, int e0, int e1, int c,
+          double& a0, double& a1) {
+        if (c >= r) return;
+        for (int e = e0; e < e1; ++e) {
+          const double2 x = *reinterpret_cast<const double2*>(dr + int(sls[e]) * w + c);
+          const double av = avs[e];
+          a0 = a0 + av * x.x;
+          a1 = a1 + av * x.y;
         }
-      }
-      double f[2], af[1][2];
+      },
+      [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
+          const double*, const double*, int, int G) -> unsigned long long {
+        double f[2] = {0.0, 0.0}, af[1][2] = {{0.0, 0.0}};
+        if (v) {
+          const double acc[2] = {a0, a1};
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        f[e] = 0.0;
-        const int cc = c + e;
-        if (rv && c < fc) {
-          const int i = cc < r ? cc : cc - r;
-          const size_t srow = size_t(row) * ldb + size_t(p) * size_t(r);
-          if (cc < r) {
-            const double sc = acc[e] * __ldg(a.t + i);
-            f[e] = sc + __ldg(a.V + row);
-          } else {
-            f[e] = a.S[srow + i];
-          }
-          if (!sweeps && cc < r) {
-            // assembly W = F_L + fl(F_R * alpha) (:148-154)
-            double wv = f[e];
-            double fr = 0.0;
-            if (p > 0) {
-              fr = a.S[srow + i];
-              wv = wv + fr * __ldg(a.alpha + i);
+          for (int e = 0; e < 2; ++e) {
+            const int cc = c + e;
+            const int i = cc < r ? cc : cc - r;
+            const double* srow = self + size_t(p) * size_t(r);  // S block p of the row
+            if (cc < r) {
+              const double sc = acc[e] * __ldg(a.t + i);
+              f[e] = sc + __ldg(a.V + row);
+            } else {
+              f[e] = srow[i];
             }
-            a.W[size_t(i) * size_t(n) + row] = wv;
-            if (a.FLo) a.FLo[size_t(i) * size_t(n) + row] = f[e];
-            if (a.FRo) a.FRo[size_t(i) * size_t(n) + row] = fr;
+            if (!sweeps && cc < r) {
+              // assembly W = F_L + fl(F_R * alpha) (:148-154)
+              double wv = f[e];
+              double fr = 0.0;
+              if (p > 0) {
+                fr = srow[i];
+                wv = wv + fr * __ldg(a.alpha + i);
+              }
+              a.W[size_t(i) * size_t(n) + row] = wv;
+              if (a.FLo) a.FLo[size_t(i) * size_t(n) + row] = f[e];
+              if (a.FRo) a.FRo[size_t(i) * size_t(n) + row] = fr;
+            }
+            af[0][e] = fabs(f[e]);
+          }
+          if (sweeps) {
+            const unsigned o = unsigned(row) * ldf + c;
+            *reinterpret_cast<double2*>(Fc + o) = make_double2(f[0], f[1]);
+            *reinterpret_cast<double2*>(a.E + o) = make_double2(f[0], f[1]);
           }
         }
-        af[0][e] = fabs(f[e]);
-      }
-      if (sweeps && rv && c < fc) {
-        const unsigned o = unsigned(row) * ldf + c;
-        *reinterpret_cast<double2*>(Fc + o) = make_double2(f[0], f[1]);
-        *reinterpret_cast<double2*>(a.E + o) = make_double2(f[0], f[1]);
-      }
-      if (sweeps) {
-        const double rf = group_rowsum<1, 2>(af, GF, 1);
-        if (rv) mf = umax64(mf, abs_bits(rf));
-      }
-    });
-  }
+        if (!sweeps) return 0ull;
+        const double rf = group_rowsum<1, 2>(af, G, 1);
+        return rvalid ? abs_bits(rf) : 0ull;
+      });
   if (!sweeps) {
     finish(kStOk, 0, L_S, 1);
     return;
@@ -769,14 +792,14 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
       const double dkk = double(kk);
       double* const Fnn = Fn;
       const unsigned long long mfb = bulk_phase(
-          1, fc, Fc, a.E, nullptr,
+          GF, fc, fc, Fc, a.E, nullptr, gath_pair(fc),
           [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
               const double* pa, const double*, int, int G) -> unsigned long long {
             double ay[1][2] = {{0.0, 0.0}};
             if (v) {
               const double2 eo = *reinterpret_cast<const double2*>(pa);
               double2 fs = make_double2(0.0, 0.0);
-              if (has_xi) fs = *reinterpret_cast<const double2*>(self);
+              if (has_xi) fs = *reinterpret_cast<const double2*>(self + c);
               const double eov[2] = {eo.x, eo.y}, fsv[2] = {fs.x, fs.y}, acc[2] = {a0, a1};
               double y[2], en[2];
 #pragma unroll

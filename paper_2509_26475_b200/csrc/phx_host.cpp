@@ -645,8 +645,12 @@ BulkChoice bulk_choice(phx_op op, int32_t V, int32_t QS, int32_t QF, int32_t w, 
   const int mode = env ? std::atoi(env) : -1;
   if (mode == 0 || !op->plan_ok || V != 2 || QS != 1 || QF != 1) return bc;
   if (mode != 1 && op->n < (int64_t(1) << 21)) return bc;
-  const phx::BulkStage ls = phx::bulk_stage(op->plan_rows, op->plan_emax, w, true);
-  const phx::BulkStage lf = phx::bulk_stage(op->plan_rows, op->plan_emax, fcols, false);
+  // the phases' stages: S terms (width w, Vw and S tiles), recovery terms
+  // (fcols, E tile), the first S term (row-major V, even stride p1e) and the
+  // promotion (S rows, no tiles) -- the ring is sized for the largest (the
+  // last two are never larger than the S terms': p1e <= w)
+  const phx::BulkStage ls = phx::bulk_stage(op->plan_rows, op->plan_emax, w, 2);
+  const phx::BulkStage lf = phx::bulk_stage(op->plan_rows, op->plan_emax, fcols, 1);
   const int32_t sb = std::max(ls.bytes, lf.bytes);
   int optin = 0;
   PHX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->device));
@@ -1217,6 +1221,10 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
     a.plan_emax = op->plan_emax;
     a.bulk_ns = bulk.ns;
     a.bulk_stage_bytes = bulk.stage_bytes;
+    {
+      const char* fe = std::getenv("PHX_BULK_FLAGS");  // tuning knob, read per call
+      a.bulk_flags = fe ? std::atoi(fe) : 2;
+    }
     a.dyn = 2;
     a.lat = 0;
     a.bsmall = 0;

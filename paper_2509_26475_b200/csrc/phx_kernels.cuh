@@ -117,6 +117,8 @@ struct BlockArgs {
   int32_t plan_emax;     // CSR entries per tile (max over the tiles, even)
   int32_t bulk_ns;       // stages in the ring
   int32_t bulk_stage_bytes;
+  int32_t bulk_flags;    // bit 0: gather copies evict_last (else evict_normal); bit 1: try_wait
+                         // with a suspend-time hint (waiting warps sleep instead of spinning)
   // diagnostics (PHX_STEP_TIMES): %globaltimer after each grid step barrier
   // at [step]; CTA arrivals (time mod 2^48 | smid << 48) at
   // [kCtaStampBase + step * ncta + cta]
@@ -168,15 +170,16 @@ bool build_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, 
 struct BulkStage {
   int32_t dr, sa, sb, av, sl, rp, hdr, bytes;
 };
-__host__ __device__ inline BulkStage bulk_stage(int32_t rows, int32_t emax, int32_t width, bool two) {
+__host__ __device__ inline BulkStage bulk_stage(int32_t rows, int32_t emax, int32_t width,
+                                                int32_t streams) {
   BulkStage L;
   int32_t o = 0;
   L.dr = o;  // gathered rows (width even: 16-byte multiples)
   o += rows * width * 8;
   L.sa = o;  // stream A tile (Vw | E)
-  o += kPlanT * width * 8;
+  o += streams >= 1 ? kPlanT * width * 8 : 0;
   L.sb = o;  // stream B tile (S)
-  o += two ? kPlanT * width * 8 : 0;
+  o += streams >= 2 ? kPlanT * width * 8 : 0;
   L.av = o;  // CSR values (copied from a 16-byte granule)
   o += (emax + 2) * 8;
   L.sl = o;  // slots
