@@ -286,9 +286,11 @@ phx_status phx_last_eval_variant(int32_t* out8);
  * every CSR entry a one-byte slot (its row in the stage: window rows first,
  * then singles, then groups).  info[0..5] = ok (0/1), tiles, stage rows,
  * single rows per stage, max entries per tile (even), total single rows.
- * When non-null, desc (tiles x 16 int32: groups, singles, first single,
- * e_lo, e_hi, -, -, -, group source rows[4], group rows | stage row << 16
- * [4]), slot (nnz + 16 bytes) and sgl (total single rows + 1) are filled. */
+ * When non-null, desc (tiles x 16 int32, in the kernel's processing order --
+ * natural, or y-blocked for a 3D lattice operator: groups, singles, first
+ * single, e_lo, e_hi, the tile, -, -, group source rows[4], group rows |
+ * stage row << 16 [4]), slot (nnz + 16 bytes) and sgl (total single rows + 1)
+ * are filled. */
 phx_status phx_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* info6,
                          int32_t* desc, uint8_t* slot, int32_t* sgl);
 

@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
         __syncwarp();
 #pragma unroll 1
         for (int j = 0; j < kPB; ++j) {
-          const int t = posA + j < nblk ? posA + j : -1;
           const int* d = pdesc[cur][j];
+          const int t = posA + j < nblk ? d[5] : -1;  // descriptors in processing order
           const int s = kpipe % NS;
           if (sleepw)
             mbar_wait_sleep(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);

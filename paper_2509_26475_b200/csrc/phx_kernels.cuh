@@ -146,7 +146,8 @@ enum : int32_t {
 // by many rows of the tile: rows [base+off, base+off+T) in one copy) and a few
 // single rows.  Descriptor (kPlanDesc int32 per tile):
 //   [0] groups  [1] singles  [2] first single in plan_sgl  [3] e_lo  [4] e_hi
-//   [8+g] group g's first source row   [12+g] rows | (stage row << 16)
+//   [5] the tile   [8+g] group g's first source row   [12+g] rows | (stage row << 16)
+// stored in the plan's processing order (phx_plan.cpp tile_order).
 constexpr int kPlanT = 32;
 constexpr int kPlanGroups = 4;
 constexpr int kPlanDesc = 16;
@@ -162,6 +163,7 @@ struct TilePlan {
   std::vector<int32_t> sgl;   // + 1
   int32_t rows = 0, sgl_cap = 0, emax = 0;
   bool ok = false;
+  bool blocked = false;  // y-blocked lattice order (else natural)
 };
 // false (plan.ok == false) when some tile needs more than the stage holds
 bool build_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, TilePlan* plan);

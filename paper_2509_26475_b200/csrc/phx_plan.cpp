@@ -17,6 +17,7 @@
 // where the gathered values are read from.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 #include <thread>
 #include <vector>
@@ -101,6 +102,61 @@ void parallel_tiles(int64_t ntiles, F&& f) {
   for (auto& x : th) x.join();
 }
 
+// Processing order of the tiles (the kernel hands out positions in this
+// order; the descriptors are stored in it, d[5] = the tile).  Lattice
+// operators -- offset groups +-B1 and +-B2 with T | B1 | B2 | n, e.g. a 3D
+// 7-point stencil (B1 = nx, B2 = nx*ny) -- are swept in y-blocks of kYBlock
+// lines: for each block, for z, for y in the block, for the x tiles.  A row
+// is then gathered again (as a z-1 neighbour) 2 * kYBlock lines after its
+// first use instead of two whole planes later, so the reuse fits in L2
+// (C3: 3.9 MB instead of 31 MB of D per reuse window).  Other operators keep
+// the natural order.
+constexpr int64_t kYBlock = 32;
+void tile_order(int64_t n, const std::vector<TileInfo>& info, TilePlan* plan) {
+  const int64_t T = kPlanT, ntiles = int64_t(info.size());
+  std::vector<int32_t> order(static_cast<size_t>(ntiles));
+  for (int64_t t = 0; t < ntiles; ++t) order[size_t(t)] = int32_t(t);
+  // the lattice strides: the two largest |group offsets| present in at least
+  // half of the tiles, as +- pairs
+  std::vector<std::pair<int64_t, int64_t>> cnt;  // (|off|, tiles)
+  for (const TileInfo& ti : info)
+    for (int g = 0; g < ti.ng; ++g) {
+      const int64_t a = std::abs(int64_t(ti.goff[g]));
+      bool f = false;
+      for (auto& c : cnt)
+        if (c.first == a) {
+          ++c.second;
+          f = true;
+        }
+      if (!f && cnt.size() < 64) cnt.push_back({a, 1});
+    }
+  std::vector<int64_t> strides;
+  for (const auto& c : cnt)
+    if (c.second >= ntiles) strides.push_back(c.first);  // +off and -off in >= half the tiles
+  std::sort(strides.begin(), strides.end());
+  const char* env = std::getenv("PHX_PLAN_BLOCKED");  // developer knob (read at creation)
+  if (strides.size() >= 2 && !(env && env[0] == '0')) {
+    const int64_t B2 = strides.back(), B1 = strides[strides.size() - 2];
+    if (B1 % T == 0 && B2 % B1 == 0 && n % B2 == 0 && B2 / B1 >= 2 * kYBlock) {
+      const int64_t ny = B2 / B1, nz = n / B2, xt = B1 / T;
+      size_t q = 0;
+      for (int64_t yb = 0; yb < ny; yb += kYBlock)
+        for (int64_t z = 0; z < nz; ++z)
+          for (int64_t y = yb; y < std::min(ny, yb + kYBlock); ++y)
+            for (int64_t x = 0; x < xt; ++x) order[q++] = int32_t((z * B2 + y * B1) / T + x);
+      plan->blocked = true;
+    }
+  }
+  std::vector<int32_t> desc(plan->desc.size());
+  for (int64_t q = 0; q < ntiles; ++q) {
+    const int32_t t = order[size_t(q)];
+    std::copy(plan->desc.begin() + size_t(t) * kPlanDesc,
+              plan->desc.begin() + size_t(t + 1) * kPlanDesc, desc.begin() + size_t(q) * kPlanDesc);
+    desc[size_t(q) * kPlanDesc + 5] = t;
+  }
+  plan->desc.swap(desc);
+}
+
 }  // namespace
 
 bool build_tile_plan(int64_t n, const int64_t* rp, const int32_t* ci, TilePlan* plan) {
@@ -172,6 +228,7 @@ bool build_tile_plan(int64_t n, const int64_t* rp, const int32_t* ci, TilePlan* 
         plan->slot[size_t(e)] = uint8_t(sl);
       }
   });
+  tile_order(n, info, plan);
   plan->ok = true;
   return true;
 }

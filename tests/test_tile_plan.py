@@ -18,8 +18,10 @@ def check_plan(n, rp, ci):
     gbase = T + 2 + scap
     assert info["rows"] <= 256 and (info["rows"] - gbase) % T == 0
     ngmax = (info["rows"] - gbase) // T
-    for t in range(info["tiles"]):
-        d = desc[t]
+    order = desc[:, 5]
+    assert sorted(order.tolist()) == list(range(info["tiles"]))  # a permutation of the tiles
+    for d in desc:
+        t = int(d[5])
         base = t * T
         rows = min(T, n - base)
         wlo, whi = max(base - 1, 0), min(base + rows + 1, n)
@@ -53,6 +55,19 @@ def test_stencil_3d_four_groups():
     wl = P.workload(3, 20, with_V=False)  # 20^3 7-point stencil
     info = check_plan(wl.n, wl.rp, wl.ci)
     assert info["rows"] == T + 2 + 4 * T and info["singles"] == 0
+
+
+def test_lattice_tile_order():
+    """A 3D lattice (strides 256, 256^2 -> here 64, 64^2 with 64 z-planes) is
+    swept in y-blocks of 32 lines: for each block, for z, for y, for x."""
+    wl = P.workload(3, 64, with_V=False)  # 64^3
+    info, desc, _, _ = P.tile_plan(wl.n, wl.rp, wl.ci)
+    order = desc[:, 5]
+    xt = 64 // T
+    want = [(z * 64 * 64 + y * 64) // T + x for yb in (0, 32) for z in range(64)
+            for y in range(yb, yb + 32) for x in range(xt)]
+    assert order.tolist() == want
+    check_plan(wl.n, wl.rp, wl.ci)
 
 
 def test_stencil_2d_two_groups():
