@@ -417,13 +417,21 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
 
   // exact ||S||_inf (canonical row sums) for an inconclusive stopping test
   // (see k_phimv_block: the bounds nSl <= ||S|| <= nSu decide every other term)
-  auto s_norm_exact = [&]() -> double {
+  // Paired S terms (see the S-series loop): after a skip term S holds
+  // S_{k-1}; S_k = fl(S + fl(D_k / sigma_k)) is then formed on the fly from
+  // D_k (Ds != nullptr) -- the same two roundings the fold applies.
+  auto s_norm_exact = [&](const double* Ds, double sig) -> double {
     unsigned long long m = 0;
     const int c = 2 * (lane % GS);
     plain_rows(GS, [&](int row, bool rv, int) {
       double as[1][2] = {{0.0, 0.0}};
       if (rv && c < w) {
-        const double2 x = *reinterpret_cast<const double2*>(a.S + (unsigned(row) * ldb + c));
+        double2 x = *reinterpret_cast<const double2*>(a.S + (unsigned(row) * ldb + c));
+        if (Ds) {
+          const double2 d = *reinterpret_cast<const double2*>(Ds + (unsigned(row) * ldb + c));
+          x.x = x.x + d.x / sig;
+          x.y = x.y + d.y / sig;
+        }
         as[0][0] = fabs(x.x);
         as[0][1] = fabs(x.y);
       }
@@ -522,7 +530,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
       nSl = (nSl - c2) * (1.0 - 1e-12);
       exact = false;
       if (exact_every_term) {
-        nS = s_norm_exact();
+        nS = s_norm_exact(nullptr, 0.0);
         nSl = nSu = nS;
         exact = true;
       }
@@ -564,6 +572,27 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
       tosS[e] = ok ? __ldg(a.colTos + cc) : 0.0;
     }
   }
+  // The lane's Vw column coefficients of block j - 1 (column c - r): the
+  // fold term recomputes Vw_{k-1}[c - r] from Vw_{k-2}.
+  double kaL[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int cc = 2 * (lane % GS) + e;
+    kaL[e] = (cc < w && cc >= r) ? __ldg(a.colKa + (cc - r)) : 0.0;
+  }
+  // Paired S terms (bitwise the reference's per-term data flow, 25% fewer
+  // bytes): S_k = S_{k-1} + D_k / sigma_k and Vw_k = Vw_{k-1} Kiter are
+  // STORED only every other term.  A skip term (odd k >= 3) reads Vw_{k-1},
+  // forms Vw_k in registers and writes D_k alone; the next, fold term (k + 1)
+  // reads Vw_{k-1} again, recomputes Vw_k with the same roundings, forms
+  // Vw_{k+1}, and folds both S updates in the reference order,
+  // S_{k+1} = fl(fl(S_{k-1} + fl(D_k / sigma_k)) + fl(D_{k+1} / sigma_{k+1}))
+  // with D_k the gather source's own row (already staged in the window).
+  // Per pair: D read, D' write and Vw read twice, Vw write and S read/write
+  // once -- 72 w n bytes instead of 96 w n.  After a final skip term one fold
+  // pass completes S for the promotion.
+  bool s_stale = false;  // S (and Vw) hold term k - 1's values
+  double sig_prev = sigma;
   const bool vwl_vec = (r % 2) == 0;
   for (; err == kStOk;) {
     const double lhs = c1 + c2;
@@ -575,7 +604,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     } else if (lhs <= a.tol * nSl) {
       cont = false;
     } else {
-      nS = s_norm_exact();
+      nS = s_norm_exact(s_stale ? Dc : nullptr, sigma);
       nSl = nSu = nS;
       exact = true;
       cont = lhs > a.tol * nS;
@@ -588,52 +617,103 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     }
     ++k;
     c1 = c2;
+    sig_prev = sigma;
     sigma *= k;
     double* const Dnn = Dn;
-    const double sig = sigma;
-    const unsigned long long mdb = bulk_phase(
-        GS, w, w, Dc, a.Vw, a.S, gath_pair(w),
-        [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
-            const double* pa, const double* pb, int, int G) -> unsigned long long {
-          double ad[1][2] = {{0.0, 0.0}};
-          if (v) {
-            const double2 vw = *reinterpret_cast<const double2*>(pa);
-            const double2 so = *reinterpret_cast<const double2*>(pb);
-            double2 vl = make_double2(0.0, 0.0);
-            if (vwl_vec) {
-              if (jjS[0] >= 2) vl = *reinterpret_cast<const double2*>(pa - r);
-            } else {
-              if (jjS[0] >= 2) vl.x = pa[-r];
-              if (jjS[1] >= 2) vl.y = pa[1 - r];
+    const double sig = sigma, sigp = sig_prev;
+    // Vw_k[c] = fl(fl(+0 + Vw_{k-1}[c - r] Ka) + Vw_{k-1}[c] Kd) (:98)
+    auto vw_next = [&](int e, double vw, double vl) {
+      double g2 = 0.0;
+      if (jjS[e] >= 2) g2 = g2 + vl * kaS[e];
+      g2 = g2 + vw * kdS[e];
+      return g2;
+    };
+    auto d_next = [&](int e, double acc, double ds, double g2) {
+      // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
+      double y = acc;
+      if (has_xi) y = y - a.xi * ds;
+      y = y * tosS[e];
+      return y + g2;
+    };
+    unsigned long long mdb;
+    if (!s_stale) {
+      // skip term: Vw_{k-1} in, D_k out
+      mdb = bulk_phase(
+          GS, w, w, Dc, a.Vw, nullptr, gath_pair(w),
+          [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
+              const double* pa, const double*, int, int G) -> unsigned long long {
+            double ad[1][2] = {{0.0, 0.0}};
+            if (v) {
+              const double2 vw = *reinterpret_cast<const double2*>(pa);
+              double2 vl = make_double2(0.0, 0.0);
+              if (vwl_vec) {
+                if (jjS[0] >= 2) vl = *reinterpret_cast<const double2*>(pa - r);
+              } else {
+                if (jjS[0] >= 2) vl.x = pa[-r];
+                if (jjS[1] >= 2) vl.y = pa[1 - r];
+              }
+              double2 ds = make_double2(0.0, 0.0);
+              if (has_xi) ds = *reinterpret_cast<const double2*>(self + c);
+              const double d0 = d_next(0, a0, ds.x, vw_next(0, vw.x, vl.x));
+              const double d1 = d_next(1, a1, ds.y, vw_next(1, vw.y, vl.y));
+              ad[0][0] = fabs(d0);
+              ad[0][1] = fabs(d1);
+              __stcs(reinterpret_cast<double2*>(Dnn + (unsigned(row) * ldb + c)), make_double2(d0, d1));
             }
-            double2 ds = make_double2(0.0, 0.0);
-            if (has_xi) ds = *reinterpret_cast<const double2*>(self + c);
-            const double vwv[2] = {vw.x, vw.y}, vlv[2] = {vl.x, vl.y}, sov[2] = {so.x, so.y},
-                         dsv[2] = {ds.x, ds.y}, acc[2] = {a0, a1};
-            double vn[2], dn[2], sn[2];
+            const double rd = group_rowsum<1, 2>(ad, G, 1);
+            return rvalid ? abs_bits(rd) : 0ull;
+          });
+    } else {
+      // fold term: Vw_{k-2} and S_{k-2} in; Vw_k, D_k, S_k out
+      mdb = bulk_phase(
+          GS, w, w, Dc, a.Vw, a.S, gath_pair(w),
+          [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
+              const double* pa, const double* pb, int, int G) -> unsigned long long {
+            double ad[1][2] = {{0.0, 0.0}};
+            if (v) {
+              // Vw_{k-2}[c], [c - r], [c - 2r] (zeros where the block has none)
+              const double2 v0 = *reinterpret_cast<const double2*>(pa);
+              double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
+              if (vwl_vec) {
+                if (jjS[0] >= 1) v1 = *reinterpret_cast<const double2*>(pa - r);
+                if (jjS[0] >= 2) v2 = *reinterpret_cast<const double2*>(pa - 2 * r);
+              } else {
+                if (jjS[0] >= 1) v1.x = pa[-r];
+                if (jjS[1] >= 1) v1.y = pa[1 - r];
+                if (jjS[0] >= 2) v2.x = pa[-2 * r];
+                if (jjS[1] >= 2) v2.y = pa[1 - 2 * r];
+              }
+              const double2 so = *reinterpret_cast<const double2*>(pb);
+              const double2 dp = *reinterpret_cast<const double2*>(self + c);  // D_{k-1}
+              const double v0v[2] = {v0.x, v0.y}, v1v[2] = {v1.x, v1.y}, v2v[2] = {v2.x, v2.y},
+                           sov[2] = {so.x, so.y}, dpv[2] = {dp.x, dp.y}, acc[2] = {a0, a1};
+              double vn[2], dn[2], sn[2];
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              // Vw = Vw * Kiter: ascending source column from +0 (:98)
-              double g2 = 0.0;
-              if (jjS[e] >= 2) g2 = g2 + vlv[e] * kaS[e];
-              g2 = g2 + vwv[e] * kdS[e];
-              vn[e] = g2;
-              // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
-              double y = acc[e];
-              if (has_xi) y = y - a.xi * dsv[e];
-              y = y * tosS[e];
-              dn[e] = y + g2;
-              sn[e] = sov[e] + dn[e] / sig;  // S += D/sigma (:105)
-              ad[0][e] = fabs(dn[e]);
+              for (int e = 0; e < 2; ++e) {
+                // Vw_{k-1}[c] and Vw_{k-1}[c - r], as the skip term formed them
+                const double wc = vw_next(e, v0v[e], v1v[e]);
+                double wl = 0.0;
+                if (jjS[e] >= 2) {  // column c - r, block j - 1 >= 1
+                  wl = 0.0;
+                  if (jjS[e] >= 3) wl = wl + v2v[e] * kaL[e];
+                  wl = wl + v1v[e] * kdS[e];
+                }
+                vn[e] = vw_next(e, wc, wl);            // Vw_k
+                dn[e] = d_next(e, acc[e], dpv[e], vn[e]);  // D_k (ds = D_{k-1} row)
+                const double s1 = sov[e] + dpv[e] / sigp;  // S_{k-1} (:105)
+                sn[e] = s1 + dn[e] / sig;                  // S_k
+                ad[0][e] = fabs(dn[e]);
+              }
+              const unsigned o = unsigned(row) * ldb + c;
+              __stcs(reinterpret_cast<double2*>(a.Vw + o), make_double2(vn[0], vn[1]));
+              __stcs(reinterpret_cast<double2*>(Dnn + o), make_double2(dn[0], dn[1]));
+              __stcs(reinterpret_cast<double2*>(a.S + o), make_double2(sn[0], sn[1]));
             }
-            const unsigned o = unsigned(row) * ldb + c;
-            __stcs(reinterpret_cast<double2*>(a.Vw + o), make_double2(vn[0], vn[1]));
-            __stcs(reinterpret_cast<double2*>(Dnn + o), make_double2(dn[0], dn[1]));
-            __stcs(reinterpret_cast<double2*>(a.S + o), make_double2(sn[0], sn[1]));
-          }
-          const double rd = group_rowsum<1, 2>(ad, G, 1);
-          return rvalid ? abs_bits(rd) : 0ull;
-        });
+            const double rd = group_rowsum<1, 2>(ad, G, 1);
+            return rvalid ? abs_bits(rd) : 0ull;
+          });
+    }
+    s_stale = !s_stale;
     double maxD, dmy;
     sync_step(mdb, mdb, maxD, dmy);
     c2 = maxD / sigma;  // :103
@@ -645,15 +725,31 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     nSu = (nSu + c2) * (1.0 + 1e-12);
     nSl = (nSl - c2) * (1.0 - 1e-12);
     exact = false;
+    double* tmp = Dc;
+    Dc = Dn;
+    Dn = tmp;
     if (exact_every_term) {
-      nS = s_norm_exact();
+      nS = s_norm_exact(s_stale ? Dc : nullptr, sigma);
       nSl = nSu = nS;
       exact = true;
     }
     trace(1.0, c2, nS);
-    double* tmp = Dc;
-    Dc = Dn;
-    Dn = tmp;
+  }
+  if (err == kStOk && s_stale) {
+    // the series ended on a skip term: S_L = fl(S_{L-1} + fl(D_L / sigma_L))
+    const int c = 2 * (lane % GS);
+    plain_rows(GS, [&](int row, bool rv, int) {
+      if (!rv || c >= w) return;
+      const unsigned o = unsigned(row) * ldb + c;
+      double2 x = *reinterpret_cast<const double2*>(a.S + o);
+      const double2 d = *reinterpret_cast<const double2*>(Dc + o);
+      x.x = x.x + d.x / sigma;
+      x.y = x.y + d.y / sigma;
+      *reinterpret_cast<double2*>(a.S + o) = x;
+    });
+    double dmy1, dmy2;
+    sync_step(0ull, 0ull, dmy1, dmy2);
+    s_stale = false;
   }
   const int L_S = k;
   if (err != kStOk) {
