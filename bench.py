@@ -156,26 +156,57 @@ def max_over_ranks(x: float, dist=None, device="cpu") -> float:
 
 def algorithmic_bytes(wl, rec, bulk=False):
     """Algorithmic HBM bytes of one evaluation launch,
-    counting only bytes the kernel moves.
+    counting only bytes the kernel moves.  CSR = 12 nnz + 4(n+1).
 
-    Both kernels: init 16n(p+1) (V read, V row-major write -- Vw_1 = D_1 =
-    S_1 is recomputed, not stored); the first S term CSR + 8n(p+1) + 24wn
-    (V rows gathered, Vw/D'/S written); promotion+assembly CSR + 8n(3r+1);
-    each sweep end 8n(2fc + 2pr).  Each further S term moves CSR_t + 48wn
-    and each recovery term CSR_t + 32 fc n, where CSR_t = CSR = 12 nnz +
-    4(n+1) for k_phimv_block and, for the bulk-copy kernel (which reads the
-    tile plan's one-byte slots instead of column indices), CSR_t = 9 nnz +
-    4(n+1) + 64 B per 32-row tile descriptor."""
+    k_phimv_block: init 16n(p+1) (V read, V row-major write -- Vw_1 = D_1 =
+    S_1 is recomputed, not stored); the first S term CSR + 8n(p+1) + 24wn;
+    each further S term CSR + 48wn; promotion+assembly CSR + 8n(3r+1); each
+    recovery term CSR + 32 fc n; each sweep end 8n(2fc + 2pr).
+
+    k_phimv_bulk (bulk_bytes): the CSR the bulk phases read is CSR_t = 9 nnz +
+    4(n+1) + 64 B per 32-row tile (values, one-byte slots, row_ptr, tile
+    descriptors); V row-major has an even stride p1e; S terms are paired."""
+    if bulk:
+        return bulk_bytes(wl, rec)
     n, p, r = wl.n, wl.p, wl.r
     w = (p + 1) * r
     fc = r if p == 0 else 2 * r
     csr = 12 * wl.nnz + 4 * (n + 1)
-    csr_t = (9 * wl.nnz + 4 * (n + 1) + 64 * ((n + 31) // 32)) if bulk else csr
     b = 16 * n * (p + 1)
     if rec.series_len_S >= 2:
         b += csr + 8 * n * (p + 1) + 24 * w * n
-    b += max(0, rec.series_len_S - 2) * (csr_t + 48 * w * n)
+    b += max(0, rec.series_len_S - 2) * (csr + 48 * w * n)
     b += csr + 8 * n * (3 * r + 1)
+    for lf in rec.series_lens_F:
+        b += lf * (csr + 32 * fc * n)
+    b += len(rec.series_lens_F) * 8 * n * (2 * fc + 2 * p * r)
+    return b
+
+
+def bulk_bytes(wl, rec):
+    """k_phimv_bulk's bytes (csrc/phx_bulk.cu): init 8n(p+1) + 8n p1e (V
+    read, even-stride row-major V written); first S term CSR_t + 8n p1e + 24wn
+    (V rows staged, Vw / D' / S written); paired S terms k >= 3: a skip term
+    (odd k) CSR_t + 24wn (D and Vw read, D' written), a fold term (even k)
+    CSR_t + 48wn (D, Vw read; S read and written; Vw, D' written), and a final
+    fold pass 24wn when the series ends on a skip term; promotion CSR_t + 8wn
+    (whole S rows staged) + 8n (v0) + 8nr (W) when s_eff = 1, else + 16 fc n
+    (F and E written); recovery terms CSR_t + 32 fc n; sweep ends 8n(2fc + 2pr)."""
+    n, p, r = wl.n, wl.p, wl.r
+    w = (p + 1) * r
+    fc = r if p == 0 else 2 * r
+    p1e = (p + 2) // 2 * 2
+    csr_t = 9 * wl.nnz + 4 * (n + 1) + 64 * ((n + 31) // 32)
+    L = rec.series_len_S
+    b = 8 * n * (p + 1) + 8 * n * p1e
+    if L >= 2:
+        b += csr_t + 8 * n * p1e + 24 * w * n
+    for k in range(3, L + 1):
+        b += csr_t + (24 if k % 2 else 48) * w * n
+    if L >= 3 and L % 2 == 1:
+        b += 24 * w * n
+    b += csr_t + 8 * w * n + 8 * n
+    b += 8 * n * r if not rec.series_lens_F else 16 * fc * n
     for lf in rec.series_lens_F:
         b += lf * (csr_t + 32 * fc * n)
     b += len(rec.series_lens_F) * 8 * n * (2 * fc + 2 * p * r)

@@ -280,12 +280,13 @@ phx_status phx_last_eval_variant(int32_t* out8);
 
 /* The tile plan of the bulk-copy evaluator for a host CSR matrix, built on
  * the host exactly as phx_op_create_csr builds it (no device needed; for
- * diagnostics and tests).  The plan covers every kPlanT = 32-row tile's
- * gathered rows with contiguous copies -- the window [base-1, base+33), up to
- * 4 offset groups (rows [base+off, base+off+32)) and single rows -- and gives
+ * diagnostics and tests).  The plan covers every kPlanT-row tile's
+ * gathered rows with contiguous copies -- the window [base-1, base+T+1), up to
+ * 4 offset groups (rows [base+off, base+off+T)) and single rows -- and gives
  * every CSR entry a one-byte slot (its row in the stage: window rows first,
- * then singles, then groups).  info[0..5] = ok (0/1), tiles, stage rows,
- * single rows per stage, max entries per tile (even), total single rows.
+ * then singles, then groups).  info[0..6] = ok (0/1), tiles, stage rows,
+ * single rows per stage, max entries per tile (even), total single rows,
+ * rows per tile.
  * When non-null, desc (tiles x 16 int32, in the kernel's processing order --
  * natural, or y-blocked for a 3D lattice operator: groups, singles, first
  * single, e_lo, e_hi, the tile, -, -, group source rows[4], group rows |

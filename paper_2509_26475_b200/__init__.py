@@ -513,11 +513,11 @@ def tile_plan(n, row_ptr, col_idx):
     (nnz + 16 bytes), sgl) -- arrays None when the plan does not fit."""
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
     ci = np.ascontiguousarray(col_idx, dtype=np.int32)
-    info = np.zeros(6, dtype=np.int32)
+    info = np.zeros(7, dtype=np.int32)
     i32 = C.POINTER(C.c_int32)
     _check(lib().phx_tile_plan(int(n), rp.ctypes.data_as(C.POINTER(C.c_int64)),
                                ci.ctypes.data_as(i32), info.ctypes.data_as(i32), None, None, None))
-    keys = ("ok", "tiles", "rows", "singles_cap", "emax", "singles")
+    keys = ("ok", "tiles", "rows", "singles_cap", "emax", "singles", "T")
     d = dict(zip(keys, (int(x) for x in info)))
     if not d["ok"]:
         return d, None, None, None

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     for (int blk = cta; blk < nblk; blk += ncta)
       for (int r0 = warp * gpw; r0 < kPlanT; r0 += kBW * gpw) {
         const int row = blk * kPlanT + r0 + g;
-        body(row, row < n, lg);
+        body(row, r0 + g < kPlanT && row < n, lg);
       }
   };
   const int GS = a.GS, GF = a.GF;

@@ -594,11 +594,11 @@ bool finite_all(const double* x, size_t n) {
 }
 
 // The operator's CSR on its device (int32 row_ptr / col_idx, f64 values).
-// row_ptr and the values are padded past their ends (+8 / +2): the bulk
+// row_ptr and the values are padded past their ends (+40 / +2): the bulk
 // evaluator copies their tile slices in whole 16-byte granules.
 void upload_csr(phx_op op, const int64_t* row_ptr, const int32_t* col_idx, const double* vals) {
   const int64_t n = op->n, nnz = op->nnz;
-  std::vector<int32_t> rp32(size_t(n) + 1 + 8, int32_t(nnz));
+  std::vector<int32_t> rp32(size_t(n) + 1 + 40, int32_t(nnz));
   for (int64_t i = 0; i <= n; ++i) rp32[size_t(i)] = int32_t(row_ptr[i]);
   PHX_CUDA(cudaMalloc(&op->d_rp, rp32.size() * 4));
   PHX_CUDA(cudaMalloc(&op->d_ci, std::max<size_t>(1, size_t(nnz)) * 4));
@@ -655,7 +655,7 @@ BulkChoice bulk_choice(phx_op op, int32_t V, int32_t QS, int32_t QF, int32_t w, 
   int optin = 0;
   PHX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->device));
   for (int want : {2, 1})
-    for (int ns = phx::kBulkMaxStages; ns >= 2; --ns) {
+    for (int ns = phx::kBulkMaxStages; ns >= 2; --ns) {  // the deepest ring that fits
       const size_t smem = size_t(ns) * size_t(sb);
       if (smem > size_t(optin)) continue;
       int per = 0;
@@ -2238,6 +2238,7 @@ phx_status phx_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_i
     info6[3] = ok ? plan.sgl_cap : 0;
     info6[4] = ok ? plan.emax : 0;
     info6[5] = ok ? int32_t(plan.sgl.size()) - 1 : 0;
+    info6[6] = phx::kPlanT;
     if (!ok) return;
     if (desc) std::copy(plan.desc.begin(), plan.desc.end(), desc);
     if (slot) std::copy(plan.slot.begin(), plan.slot.end(), slot);

@@ -148,14 +148,17 @@ enum : int32_t {
 //   [0] groups  [1] singles  [2] first single in plan_sgl  [3] e_lo  [4] e_hi
 //   [5] the tile   [8+g] group g's first source row   [12+g] rows | (stage row << 16)
 // stored in the plan's processing order (phx_plan.cpp tile_order).
-constexpr int kPlanT = 32;
+#ifndef PHX_PLAN_T
+#define PHX_PLAN_T 32
+#endif
+constexpr int kPlanT = PHX_PLAN_T;  // rows per tile
 constexpr int kPlanGroups = 4;
 constexpr int kPlanDesc = 16;
 constexpr int kPlanMaxSingles = 32;
 constexpr int kPlanMaxEntries = 1024;  // per tile (stage capacity)
 constexpr int kBulkConsumers = 8;      // consumer warps per CTA (+ 1 producer warp)
 constexpr int kBulkThreads = (kBulkConsumers + 1) * 32;
-constexpr int kBulkMaxStages = 4;
+constexpr int kBulkMaxStages = 8;
 
 struct TilePlan {
   std::vector<int32_t> desc;

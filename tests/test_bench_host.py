@@ -47,3 +47,18 @@ def test_algorithmic_bytes_single_term():
 def test_ncu_traffic_from_summary():
     t = bench.ncu_traffic(2)
     assert t is None or (isinstance(t, float) and 2.0e10 < t < 3.0e10)
+
+
+def test_bulk_bytes_c3_launch():
+    # C3: n = 2^24, nnz = 117,047,296, p = 4, r = 6 (w = 30, p1e = 6), L_S = 37:
+    # S terms 3..37 -> 18 skip (odd) + 17 fold (even) + a final fold pass
+    wl = _wl(16777216, 117047296, 4, 6)
+    rec = SimpleNamespace(series_len_S=37, series_lens_F=[])
+    n, w = wl.n, 30
+    csr_t = 9 * wl.nnz + 4 * (n + 1) + 64 * (n // 32)
+    want = 8 * n * 5 + 8 * n * 6                      # init
+    want += csr_t + 8 * n * 6 + 24 * w * n             # first S term
+    want += 18 * (csr_t + 24 * w * n) + 17 * (csr_t + 48 * w * n)
+    want += 24 * w * n                                 # final fold
+    want += csr_t + 8 * w * n + 8 * n + 8 * n * 6      # promotion + assembly
+    assert bench.algorithmic_bytes(wl, rec, bulk=True) == want

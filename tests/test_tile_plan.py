@@ -7,7 +7,7 @@ import pytest
 
 import paper_2509_26475_b200 as P
 
-T = 32
+T = P.tile_plan(1, [0, 1], [0])[0]["T"]  # rows per tile (kPlanT)
 
 
 def check_plan(n, rp, ci):
@@ -60,14 +60,13 @@ def test_stencil_3d_four_groups():
 def test_lattice_tile_order():
     """A 3D lattice (strides 256, 256^2 -> here 64, 64^2 with 64 z-planes) is
     swept in y-blocks of 32 lines: for each block, for z, for y, for x."""
-    wl = P.workload(3, 64, with_V=False)  # 64^3
+    wl = P.workload(3, 128, with_V=False)  # 128^3 (>= 2 x 32 y-lines)
     info, desc, _, _ = P.tile_plan(wl.n, wl.rp, wl.ci)
     order = desc[:, 5]
-    xt = 64 // T
-    want = [(z * 64 * 64 + y * 64) // T + x for yb in (0, 32) for z in range(64)
+    xt = 128 // T
+    want = [(z * 128 * 128 + y * 128) // T + x for yb in range(0, 128, 32) for z in range(128)
             for y in range(yb, yb + 32) for x in range(xt)]
     assert order.tolist() == want
-    check_plan(wl.n, wl.rp, wl.ci)
 
 
 def test_stencil_2d_two_groups():
