@@ -41,6 +41,7 @@ namespace {
 constexpr int kBW = kBulkConsumers + 1;  // warps per CTA
 constexpr int kProd = kBulkConsumers;    // the producer warp
 constexpr int kPB = 4;                   // tile positions per counter grab
+constexpr int kMaxMerge = 8;             // window-only plans: tiles merged per stage
 
 __device__ __forceinline__ unsigned su32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -204,9 +205,24 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
   // G: lanes per row of the output layout, ow: output width, width: row
   // width of the gather source X; gath(row_ptrs...) accumulates a row's
   // entries, epi(...) finishes it
+  // Window-only plans (every gathered row inside its tile's window: banded
+  // operators such as C5's bidiagonal rows) merge M consecutive tiles per
+  // stage -- one window copy, one stream copy each -- with M as large as the
+  // stage holds (narrow recovery terms: up to kMaxMerge): fewer, larger
+  // copies and barrier handshakes per byte.  A sub-tile's slots address its
+  // own window; the consumer shifts them into the merged window.
   auto bulk_phase = [&](int G, int ow, int width, const double* X, const double* A, const double* B,
                         auto&& gath, auto&& epi) -> unsigned long long {
-    const BulkStage L = bulk_stage(a.plan_rows, a.plan_emax, width, (A ? 1 : 0) + (B ? 1 : 0));
+    const int nst = (A ? 1 : 0) + (B ? 1 : 0);
+    int M = 1;
+    if (a.plan_merge)
+      while (M < kMaxMerge &&
+             bulk_stage(kPlanT * 2 * M + 2, a.plan_emax * 2 * M, width, nst, kPlanT * 2 * M).bytes <= SB)
+        M *= 2;
+    const int TM = kPlanT * M;  // rows per stage
+    const BulkStage L = M > 1 ? bulk_stage(TM + 2, a.plan_emax * M, width, nst, TM)
+                              : bulk_stage(a.plan_rows, a.plan_emax, width, nst);
+    const int npos = (nblk + M - 1) / M;
     unsigned long long* ctr = a.slots + 4 * (step % 3) + 2;
     unsigned long long mx = 0;
     if (warp == kProd) {
@@ -222,14 +238,21 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(plast));
       auto fetch = [&](int pos, int buf) {
         const int q = pos + (lane >> 2);
-        if (lane < 4 * kPB && q < nblk)
-          cp_async16(&pdesc[buf][lane >> 2][4 * (lane & 3)],
-                     a.plan_desc + size_t(q) * kPlanDesc + 4 * (lane & 3));
+        if (M == 1) {
+          if (lane < 4 * kPB && q < nblk)
+            cp_async16(&pdesc[buf][lane >> 2][4 * (lane & 3)],
+                       a.plan_desc + size_t(q) * kPlanDesc + 4 * (lane & 3));
+        } else if (lane < 4 * kPB && (lane & 3) < 2 && q < npos) {
+          // merged: e_lo from the first sub-tile's descriptor, e_hi from the last's
+          const int sub = (lane & 1) ? min(q * M + M - 1, nblk - 1) : q * M;
+          cp_async16(&pdesc[buf][lane >> 2][4 * (lane & 1)],
+                     a.plan_desc + size_t(sub) * kPlanDesc + 4 * (lane & 1));
+        }
         cp_commit();
       };
       unsigned long long pa_ = 0, pb_ = 0;
       if (lane == 0) pa_ = atomicAdd(ctr, (unsigned long long)kPB);
-      int posA = int(__shfl_sync(kFull, pa_, 0));
+      int posA = int(__shfl_sync(kFull, pa_, 0));  // positions: stages of M tiles
       fetch(posA, 0);
       if (lane == 0) pb_ = atomicAdd(ctr, (unsigned long long)kPB);
       int cur = 0;
@@ -242,7 +265,8 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
 #pragma unroll 1
         for (int j = 0; j < kPB; ++j) {
           const int* d = pdesc[cur][j];
-          const int t = posA + j < nblk ? d[5] : -1;  // descriptors in processing order
+          // descriptors in processing order (merged stages: natural order)
+          const int t = posA + j < npos ? (M == 1 ? d[5] : posA + j) : -1;
           const int s = kpipe % NS;
           if (sleepw)
             mbar_wait_sleep(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
@@ -250,14 +274,14 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
             mbar_wait(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
           unsigned char* st = ring + size_t(s) * size_t(SB);
           unsigned long long* bf = &bar_full[s];
-          const int nsgl = t >= 0 ? d[1] : 0;
+          const int nsgl = (t >= 0 && M == 1) ? d[1] : 0;
           if (lane == 0) {
             *reinterpret_cast<int*>(st + L.hdr) = t;
             if (t < 0) {
               mbar_arrive(bf);  // end of the phase: the consumers leave
             } else {
-              const int base = t * kPlanT, rows = min(kPlanT, n - base);
-              const int ng = d[0];
+              const int base = t * TM, rows = min(TM, n - base);
+              const int ng = M == 1 ? d[0] : 0;
               const int e_lo = d[3], e_hi = d[4];
               const int wlo = max(base - 1, 0), whi = min(base + rows + 1, n);
               const int c0 = e_lo & ~15, cn = (e_hi - c0 + 15) & ~15;  // slot bytes
@@ -320,13 +344,15 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
         const int e_lo = rps[0];
         const unsigned char* sls = st + L.sl + (e_lo & 15);
         const double* avs = reinterpret_cast<const double*>(st + L.av) + (e_lo & 1);
-        const int base = t * kPlanT, rows = min(kPlanT, n - base);
+        const int base = t * TM, rows = min(TM, n - base);
         const int wlo = max(base - 1, 0);
         for (int r0 = warp * gpw; r0 < rows; r0 += kBulkConsumers * gpw) {
           const int rr = r0 + g;
           const bool v = rr < rows && cv;
           double a0 = 0.0, a1 = 0.0;
-          if (v) gath(dr, sls, avs, rps[rr] - e_lo, rps[rr + 1] - e_lo, c, a0, a1);
+          // merged stages: the sub-tile's window starts dj rows into the stage's
+          const int dj = max(base + (rr / kPlanT) * kPlanT - 1, 0) - wlo;
+          if (v) gath(dr + dj * width, sls, avs, rps[rr] - e_lo, rps[rr + 1] - e_lo, c, a0, a1);
           const double* self = dr + (base + rr - wlo) * width;  // the row itself (window)
           const unsigned long long m =
               epi(v, rr < rows, base + rr, c, a0, a1, self, sa + rr * width + c, sb + rr * width + c, lg, G);

@@ -165,6 +165,7 @@ struct phx_op_s {
   // tile plan of the bulk-copy evaluator (phx_plan.cpp; device copies)
   bool plan_ok = false;
   int32_t plan_rows = 0, plan_sgl_cap = 0, plan_emax = 0;
+  bool plan_merge = false;  // window-only plan (tiles mergeable)
   int32_t* d_plan_desc = nullptr;
   uint8_t* d_plan_slot = nullptr;
   int32_t* d_plan_sgl = nullptr;
@@ -594,11 +595,11 @@ bool finite_all(const double* x, size_t n) {
 }
 
 // The operator's CSR on its device (int32 row_ptr / col_idx, f64 values).
-// row_ptr and the values are padded past their ends (+40 / +2): the bulk
+// row_ptr and the values are padded past their ends (+272 / +2): the bulk
 // evaluator copies their tile slices in whole 16-byte granules.
 void upload_csr(phx_op op, const int64_t* row_ptr, const int32_t* col_idx, const double* vals) {
   const int64_t n = op->n, nnz = op->nnz;
-  std::vector<int32_t> rp32(size_t(n) + 1 + 40, int32_t(nnz));
+  std::vector<int32_t> rp32(size_t(n) + 1 + 8 * 32 + 16, int32_t(nnz));
   for (int64_t i = 0; i <= n; ++i) rp32[size_t(i)] = int32_t(row_ptr[i]);
   PHX_CUDA(cudaMalloc(&op->d_rp, rp32.size() * 4));
   PHX_CUDA(cudaMalloc(&op->d_ci, std::max<size_t>(1, size_t(nnz)) * 4));
@@ -627,6 +628,7 @@ void upload_plan(phx_op op, const int64_t* row_ptr, const int32_t* col_idx) {
   op->plan_rows = plan.rows;
   op->plan_sgl_cap = plan.sgl_cap;
   op->plan_emax = plan.emax;
+  op->plan_merge = plan.rows == phx::kPlanT + 2;  // no singles, no groups
   op->plan_ok = true;
 }
 
@@ -651,7 +653,10 @@ BulkChoice bulk_choice(phx_op op, int32_t V, int32_t QS, int32_t QF, int32_t w, 
   // last two are never larger than the S terms': p1e <= w)
   const phx::BulkStage ls = phx::bulk_stage(op->plan_rows, op->plan_emax, w, 2);
   const phx::BulkStage lf = phx::bulk_stage(op->plan_rows, op->plan_emax, fcols, 1);
-  const int32_t sb = std::max(ls.bytes, lf.bytes);
+  int32_t sb = std::max(ls.bytes, lf.bytes);
+  // window-only plans merge tiles per stage (phx_bulk.cu): give their ring
+  // fewer, larger stages (~48 KB)
+  if (op->plan_merge) sb = std::max(sb, int32_t(48 * 1024));
   int optin = 0;
   PHX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->device));
   for (int want : {2, 1})
@@ -1219,6 +1224,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
     a.plan_rows = op->plan_rows;
     a.plan_sgl_cap = op->plan_sgl_cap;
     a.plan_emax = op->plan_emax;
+    a.plan_merge = op->plan_merge ? 1 : 0;
     a.bulk_ns = bulk.ns;
     a.bulk_stage_bytes = bulk.stage_bytes;
     {

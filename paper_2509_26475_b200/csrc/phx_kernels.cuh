@@ -115,6 +115,7 @@ struct BlockArgs {
   int32_t plan_rows;     // gathered rows per stage: window (T+2) + singles + groups
   int32_t plan_sgl_cap;  // single rows per stage (groups start after them)
   int32_t plan_emax;     // CSR entries per tile (max over the tiles, even)
+  int32_t plan_merge;    // 1: window-only plan (no groups, no singles): tiles may be merged
   int32_t bulk_ns;       // stages in the ring
   int32_t bulk_stage_bytes;
   int32_t bulk_flags;    // bit 0: gather copies evict_last (else evict_normal); bit 1: try_wait
@@ -176,21 +177,21 @@ struct BulkStage {
   int32_t dr, sa, sb, av, sl, rp, hdr, bytes;
 };
 __host__ __device__ inline BulkStage bulk_stage(int32_t rows, int32_t emax, int32_t width,
-                                                int32_t streams) {
+                                                int32_t streams, int32_t T = kPlanT) {
   BulkStage L;
   int32_t o = 0;
   L.dr = o;  // gathered rows (width even: 16-byte multiples)
   o += rows * width * 8;
   L.sa = o;  // stream A tile (Vw | E)
-  o += streams >= 1 ? kPlanT * width * 8 : 0;
+  o += streams >= 1 ? T * width * 8 : 0;
   L.sb = o;  // stream B tile (S)
-  o += streams >= 2 ? kPlanT * width * 8 : 0;
+  o += streams >= 2 ? T * width * 8 : 0;
   L.av = o;  // CSR values (copied from a 16-byte granule)
   o += (emax + 2) * 8;
   L.sl = o;  // slots
   o += (emax + 32 + 15) / 16 * 16;
   L.rp = o;  // row_ptr slice
-  o += (kPlanT + 4) * 4;
+  o += (T + 4 + 3) / 4 * 16;
   L.hdr = o;  // tile id
   o += 16;
   L.bytes = (o + 127) / 128 * 128;
