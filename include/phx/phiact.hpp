@@ -19,8 +19,15 @@
 //
 // Differences: the operator is a CSR matrix held on the device (the
 // reference's ApplyFn is an opaque host callback that cannot run on a GPU);
-// Matrix/Vector are minimal column-major containers instead of Eigen types
-// (Eigen is not required).  Header-only.
+// phiact::dense_operator (linop.cpp:26-38) stores every entry as CSR.
+// Matrix / Vector are Eigen::MatrixXd / Eigen::VectorXd -- the reference's own
+// types (linop.hpp:12) -- whenever <Eigen/Dense> is available (or
+// PHX_WITH_EIGEN is defined), so reference call sites compile unchanged;
+// without Eigen they are minimal column-major containers with the same
+// members (rows, cols, size, data, operator()).  Evaluations on one operator
+// may run concurrently from several threads (each takes its own device
+// workspace), as the reference's re-entrant operator allows (linop.hpp:16-18).
+// Header-only.
 #pragma once
 
 #include <algorithm>
@@ -34,10 +41,24 @@
 
 #include "../phx.h"
 
+#if !defined(PHX_WITH_EIGEN) && !defined(PHX_NO_EIGEN) && defined(__has_include)
+#if __has_include(<Eigen/Dense>)
+#define PHX_WITH_EIGEN 1
+#endif
+#endif
+#ifdef PHX_WITH_EIGEN
+#include <Eigen/Dense>
+#endif
+
 namespace phiact {
 
 using Index = std::int64_t;
 
+#ifdef PHX_WITH_EIGEN
+// the reference's types (linop.hpp:12): column-major, contiguous
+using Matrix = Eigen::MatrixXd;
+using Vector = Eigen::VectorXd;
+#else
 // Column-major dense block (the reference's Eigen::MatrixXd layout).
 class Matrix {
  public:
@@ -71,6 +92,7 @@ class Vector {
  private:
   std::vector<double> a_;
 };
+#endif
 
 inline constexpr int kDefaultDegree = 61;               // params.hpp:12
 inline constexpr double kDefaultGuardFraction = 0.8;    // params.hpp:13
@@ -118,7 +140,8 @@ class LinearOperator {
   std::string label_;
 };
 
-// CSR factory (the reference's dense_operator analogue, linop.cpp:26-38).
+// CSR factory (the entry point for sparse operators; the reference has only
+// dense_operator and user ApplyFns, linop.cpp:26-38).
 inline LinearOperator csr_operator(Index n, const std::vector<std::int64_t>& row_ptr,
                                    const std::vector<std::int32_t>& col_idx,
                                    const std::vector<double>& vals, std::string label = {},
@@ -130,6 +153,30 @@ inline LinearOperator csr_operator(Index n, const std::vector<std::int64_t>& row
   op.h_ = std::shared_ptr<phx_op_s>(h, [](phx_op p) { phx_op_destroy(p); });
   op.label_ = std::move(label);
   return op;
+}
+
+// dense_operator (linop.cpp:26-38): square, finite, every entry stored (as
+// CSR, rows in natural column order -- the reference's dense product sums a
+// row in the same order); the same checks and messages.
+inline LinearOperator dense_operator(const Matrix& A, std::string label = "dense",
+                                     int device = -1) {
+  if (A.rows() != A.cols()) throw std::invalid_argument("dense_operator: matrix must be square");
+  const Index n = A.rows();
+  if (n == 0) throw std::invalid_argument("dense_operator: matrix must be non-empty");
+  std::vector<std::int64_t> rp(size_t(n + 1));
+  std::vector<std::int32_t> ci(size_t(n * n));
+  std::vector<double> av(size_t(n * n));
+  for (Index i = 0; i < n; ++i) {
+    rp[size_t(i)] = i * n;
+    for (Index j = 0; j < n; ++j) {
+      const double x = A(i, j);
+      if (!(x - x == 0.0)) throw std::invalid_argument("dense_operator: matrix has non-finite entries");
+      ci[size_t(i * n + j)] = std::int32_t(j);
+      av[size_t(i * n + j)] = x;
+    }
+  }
+  rp[size_t(n)] = n * n;
+  return csr_operator(n, rp, ci, av, std::move(label), device);
 }
 
 // (A - xi I) X (linop.cpp:40-49)
@@ -156,6 +203,17 @@ struct RunRecord {  // phi_single.hpp:16-21
 };
 
 namespace detail {
+// recovery sweeps of an evaluation, s_eff - 1 with s_eff = max(1,
+// ceil(s * max|t|)) (phi_block.cpp:57-59): the size of the run record's
+// series_lens_F buffer
+inline std::size_t sweeps_of(double s, const double* t, Index r) {
+  double tmax = 0.0;
+  for (Index i = 0; i < r; ++i) tmax = std::max(tmax, t[i] < 0 ? -t[i] : t[i]);
+  const double prod = s * tmax;
+  if (!(prod < 2147483647.0)) return 1;  // the evaluator rejects it with the reference's error
+  const double c = prod <= 1.0 ? 1.0 : double(std::int64_t(prod) + (double(std::int64_t(prod)) < prod));
+  return std::size_t(std::max(1.0, c - 1.0));
+}
 inline phx_scaling_shift to_c(const ScalingShift& s) {
   return phx_scaling_shift{s.s, s.xi, s.s0, s.f_min, s.m, s.r};
 }
@@ -197,7 +255,7 @@ inline BlockPhiResult phimv_block(const LinearOperator& op, const BlockPhiReques
   BlockPhiResult out;
   out.W = Matrix(req.V.rows(), req.t.size());
   const phx_scaling_shift ss = detail::to_c(req.params);
-  std::vector<int32_t> lens(1 << 20);
+  std::vector<int32_t> lens(detail::sweeps_of(req.params.s, req.t.data(), req.t.size()));
   phx_run_record rec{0, 0, 0, lens.data(), int64_t(lens.size()), 0};
   detail::check(phx_phimv_block(op.handle(), int32_t(req.t.size()), req.t.data(), req.alpha.data(),
                                 int32_t(req.V.cols() - 1), req.V.data(), req.V.rows(), req.tol, &ss,
@@ -227,12 +285,14 @@ struct PhiResult {  // phi_single.hpp:34-39
 // phimv (phi_single.hpp:44)
 inline PhiResult phimv(const LinearOperator& op, const PhiRequest& req) {
   const Index n = op.dim();
+  if (req.V.cols() < 1) throw std::invalid_argument("phimv: V must have at least one column");
+  if (req.V.rows() != n) throw std::invalid_argument("phimv: V row count does not match operator");
   PhiResult out;
   out.w = Vector(n);
   out.exp_v0 = Vector(n);
   out.tail = Vector(n);
   const phx_scaling_shift ss = detail::to_c(req.params);
-  std::vector<int32_t> lens(1 << 20);
+  std::vector<int32_t> lens(detail::sweeps_of(req.params.s, &req.t, 1));
   phx_run_record rec{0, 0, 0, lens.data(), int64_t(lens.size()), 0};
   detail::check(phx_phimv(op.handle(), req.t, req.alpha, int32_t(req.V.cols() - 1), req.V.data(),
                           req.V.rows(), req.tol, &ss, out.w.data(), out.exp_v0.data(),
@@ -322,10 +382,12 @@ inline Vector exprk4s6_step(const ADRProblem& problem, const StepState& state, d
                             const ScalingShift& params, StepRecord* record = nullptr) {
   Vector out(state.u.size());
   const phx_scaling_shift ss = detail::to_c(params);
-  std::vector<std::vector<int32_t>> lens(4, std::vector<int32_t>(1 << 16));
+  // every stage's abscissae are <= h: at most sweeps_of(s, h) sweeps each
+  const std::size_t cap = detail::sweeps_of(params.s, &state.h, 1);
+  std::vector<std::vector<int32_t>> lens(4, std::vector<int32_t>(cap));
   phx_run_record recs[4];
   for (int k = 0; k < 4; ++k)
-    recs[k] = phx_run_record{0, 0, 0, lens[size_t(k)].data(), int64_t(1 << 16), 0};
+    recs[k] = phx_run_record{0, 0, 0, lens[size_t(k)].data(), int64_t(cap), 0};
   detail::check(phx_exprk4s6_step(problem.op.handle(), problem.gamma, state.u.data(), state.h,
                                   tol, &ss, out.data(), record ? recs : nullptr));
   if (record) {
@@ -352,7 +414,8 @@ inline IntegrateResult integrate(const ADRProblem& problem, double h, double t_e
     const double q = t_end / h;
     if (q >= 0.5 && q < 1.0e6 + 0.5) nrec = 4 * int64_t(std::llround(q));
   }
-  constexpr int64_t kLens = 1 << 10;
+  // per record: the sweeps of an evaluation with abscissae <= h
+  const int64_t kLens = int64_t(detail::sweeps_of(params.s, &h, 1));
   std::vector<int32_t> lens(size_t(std::max<int64_t>(1, nrec) * kLens));
   std::vector<phx_run_record> recs(size_t(std::max<int64_t>(1, nrec)));
   for (int64_t k = 0; k < nrec; ++k)

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <functional>
 #include <limits>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -146,11 +147,30 @@ struct PartDev {
   DevBuf Vw, D0, D1, S, F0, F1, E, W, V, coef, slots, arrive, mbox, status, lensF, trace, ptab;
 };
 
-}  // namespace
-
-// control-block slots per operator: evaluations that may be in flight at once
-// (the integrator enqueues a step's four before one synchronize)
+// control-block slots per workspace: evaluations that may be in flight at
+// once (the integrator enqueues a step's four before one synchronize)
 constexpr int kCtlSlots = 4;
+
+// One evaluation's device workspace and stream.  An operator owns ws0 (its
+// own stream: phx_op_stream) and grows a pool when evaluations run
+// concurrently on one handle -- the reference's operator is re-entrant and
+// its evaluations own their workspace (linop.hpp:16-18).
+struct Workspace {
+  DevBuf Vw, D0, D1, S, F0, F1, E, W, V, FLo, FRo, trace, tstamp, ctl[kCtlSlots];
+  HostBuf h_ctl[kCtlSlots];
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::mutex busy;
+  void release() {
+    for (DevBuf* b : {&Vw, &D0, &D1, &S, &F0, &F1, &E, &W, &V, &FLo, &FRo, &trace, &tstamp}) b->release();
+    for (int k = 0; k < kCtlSlots; ++k) {
+      ctl[k].release();
+      h_ctl[k].release();
+    }
+  }
+};
+
+}  // namespace
 
 struct phx_op_s {
   int nparts = 1;                // > 1: row-partitioned (parts[], no d_rp/d_ci/d_av)
@@ -171,12 +191,15 @@ struct phx_op_s {
   int32_t* d_plan_sgl = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  std::mutex mu;
-  // evaluation workspace
-  DevBuf Vw, D0, D1, S, F0, F1, E, W, V, FLo, FRo, trace, tstamp, ctl[kCtlSlots];
+  std::mutex mu;  // selection, apply, the integrator and partitioned evaluations
+  // evaluation workspaces: ws0 on the operator's stream, a pool for
+  // concurrent evaluations (Lease)
+  Workspace ws0;
+  std::mutex pool_mu;
+  std::vector<std::unique_ptr<Workspace>> pool;
   // selection workspace
   DevBuf w0, w1, y, chunkmax, inv, partial, gcoef, spx, spy;
-  HostBuf h_small, h_chunk, h_inv, h_part, h_lens, h_ctl[kCtlSlots], h_flag;
+  HostBuf h_small, h_chunk, h_inv, h_part, h_lens, h_flag;
   // fixed-seed start vectors (params.cpp:102-110), cached per operator
   std::vector<double> start1, start2;
   bool have_start2 = false;
@@ -947,16 +970,46 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
 
 void finish_eval(const PendingEval& pe, phx_run_record* rec);
 
+// A workspace for one evaluation: the operator's own (ws0) when free, else
+// a free pooled one, else a new one with its own stream.
+struct Lease {
+  Workspace* w = nullptr;
+  std::unique_lock<std::mutex> lk;
+  explicit Lease(phx_op op) {
+    if (op->ws0.busy.try_lock()) {
+      w = &op->ws0;
+    } else {
+      std::lock_guard<std::mutex> g(op->pool_mu);
+      for (auto& p : op->pool)
+        if (p->busy.try_lock()) {
+          w = p.get();
+          break;
+        }
+      if (!w) {
+        auto nw = std::make_unique<Workspace>();
+        PHX_CUDA(cudaStreamCreateWithFlags(&nw->stream, cudaStreamNonBlocking));
+        PHX_CUDA(cudaEventCreate(&nw->ev0));
+        PHX_CUDA(cudaEventCreate(&nw->ev1));
+        nw->busy.lock();
+        w = nw.get();
+        op->pool.push_back(std::move(nw));
+      }
+    }
+    lk = std::unique_lock<std::mutex>(w->busy, std::adopt_lock);
+  }
+};
+
 // defer != nullptr: enqueue only (single-device, no trace): the caller
 // synchronizes the stream and calls finish_eval(*defer, rec)
-void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* defer = nullptr) {
+void evaluate(phx_op op, Workspace& ws, const EvalIn& in, phx_run_record* rec,
+              PendingEval* defer = nullptr) {
   const char* who = in.single ? "phimv" : "phimv_block";
   const int64_t n = op->n;
   const int32_t r = in.r;
   const int32_t p = in.p;
   const double tol = in.tol > 0.0 ? in.tol : std::ldexp(1.0, -53);
   const double xi = in.params.xi;
-  cudaStream_t st = op->stream;
+  cudaStream_t st = ws.stream;
 
   double tmax = 0.0;
   for (int32_t i = 0; i < r; ++i) tmax = std::max(tmax, std::fabs(in.t[i]));
@@ -1131,10 +1184,10 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
   const size_t cb = ncoef * 8;
   const size_t ctl_up = cb + 128;  // coefficients + zeroed slots/status
   const size_t ctl_bytes = ctl_up + size_t(std::max<int64_t>(1, nsw)) * 4;
-  char* d_ctl = static_cast<char*>(op->ctl[in.slot].get(ctl_bytes));
+  char* d_ctl = static_cast<char*>(ws.ctl[in.slot].get(ctl_bytes));
   // pinned host side: the upload image, then the read-back area (kept apart:
   // a captured step graph re-uploads the image on every replay)
-  char* h_ctl = static_cast<char*>(op->h_ctl[in.slot].get(2 * ctl_bytes));
+  char* h_ctl = static_cast<char*>(ws.h_ctl[in.slot].get(2 * ctl_bytes));
   char* h_back = h_ctl + ctl_bytes;
   std::memcpy(h_ctl, coef.data(), cb);
   std::memset(h_ctl + cb, 0, 128);
@@ -1147,33 +1200,33 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
   a.mu = a.alpha + r;
   a.g = a.mu + r;
   a.jc = a.g + r;
-  a.Vw = op->Vw.as<double>(nb);
-  a.D0 = op->D0.as<double>(nb);
-  a.D1 = op->D1.as<double>(nb);
-  a.S = op->S.as<double>(nb);
+  a.Vw = ws.Vw.as<double>(nb);
+  a.D0 = ws.D0.as<double>(nb);
+  a.D1 = ws.D1.as<double>(nb);
+  a.S = ws.S.as<double>(nb);
   a.ldb = ldb;
-  a.F0 = op->F0.as<double>(nf);
-  a.F1 = op->F1.as<double>(nf);
-  a.E = op->E.as<double>(nf);
+  a.F0 = ws.F0.as<double>(nf);
+  a.F1 = ws.F1.as<double>(nf);
+  a.E = ws.E.as<double>(nf);
   a.ldf = ldf;
-  a.W = in.dW ? in.dW : op->W.as<double>(size_t(n) * size_t(r));
-  a.FLo = in.h_exp_v0 ? op->FLo.as<double>(size_t(n) * size_t(r)) : nullptr;
-  a.FRo = in.h_tail ? op->FRo.as<double>(size_t(n) * size_t(r)) : nullptr;
+  a.W = in.dW ? in.dW : ws.W.as<double>(size_t(n) * size_t(r));
+  a.FLo = in.h_exp_v0 ? ws.FLo.as<double>(size_t(n) * size_t(r)) : nullptr;
+  a.FRo = in.h_tail ? ws.FRo.as<double>(size_t(n) * size_t(r)) : nullptr;
   a.slots = reinterpret_cast<unsigned long long*>(d_ctl + cb);  // [3][maxA, maxB, tile counter, pad]
   a.status = reinterpret_cast<int32_t*>(d_ctl + cb + 96);
   a.lensF = reinterpret_cast<int32_t*>(d_ctl + ctl_up);
   a.nparts = 1;
   static const bool step_times = std::getenv("PHX_STEP_TIMES") != nullptr;
   a.tstamp_cap = step_times ? 1 << 20 : 0;
-  a.tstamp = step_times ? op->tstamp.as<unsigned long long>(size_t(a.tstamp_cap)) : nullptr;
+  a.tstamp = step_times ? ws.tstamp.as<unsigned long long>(size_t(a.tstamp_cap)) : nullptr;
   if (step_times) PHX_CUDA(cudaMemsetAsync(a.tstamp, 0, size_t(a.tstamp_cap) * 8, st));
-  a.trace = trace_cap > 0 ? op->trace.as<double>(size_t(trace_cap)) : nullptr;
+  a.trace = trace_cap > 0 ? ws.trace.as<double>(size_t(trace_cap)) : nullptr;
   a.trace_cap = int32_t(trace_cap);
 
   if (in.dV) {
     a.V = in.dV;
   } else {
-    double* dV = op->V.as<double>(size_t(n) * size_t(p + 1));
+    double* dV = ws.V.as<double>(size_t(n) * size_t(p + 1));
     if (in.ldv == n)
       PHX_CUDA(cudaMemcpyAsync(dV, in.hV, size_t(n) * size_t(p + 1) * 8, cudaMemcpyHostToDevice, st));
     else
@@ -1203,7 +1256,12 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
   // the dynamic-tail kernel when the CTAs get many tiles each: per-CTA speed
   // differs by up to ~20% on long steps; on short ones the tail grabs and the
   // larger kernel cost more than they balance
-  a.dyn = !a.lat && ntiles >= int64_t(kDynTilesPerCta) * max_blocks ? 1 : 0;
+  // PHX_FORCE_DYN=1 (read per call; tests): the dynamic-tail variant at any
+  // size above latency mode, so its production instantiations can be pinned
+  // to the oracle at sizes the oracle finishes quickly
+  const char* fdyn = std::getenv("PHX_FORCE_DYN");
+  const bool force_dyn = fdyn && fdyn[0] == '1';
+  a.dyn = !a.lat && (force_dyn || ntiles >= int64_t(kDynTilesPerCta) * max_blocks) ? 1 : 0;
   if (a.dyn)
     PHX_CUDA(phx::coop_grid_size(QT, V, R, false, true, a.bsmall != 0, block, &max_blocks));
   // developer knob for tuning studies: PHX_GRID_FRAC = fraction (0, 1] of the
@@ -1238,7 +1296,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
     PHX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, op->device));
     grid = bulk.per_sm * sms;
   }
-  PHX_CUDA(cudaEventRecord(op->ev0, st));
+  PHX_CUDA(cudaEventRecord(ws.ev0, st));
   if (bulk.use)
     PHX_CUDA(phx::launch_phimv_bulk(a, grid, st));
   else
@@ -1250,7 +1308,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
                             bulk.use ? phx::kBulkThreads : block};
     std::memcpy(g_last_variant, var, sizeof var);
   }
-  PHX_CUDA(cudaEventRecord(op->ev1, st));
+  PHX_CUDA(cudaEventRecord(ws.ev1, st));
   if (step_times) {
     std::vector<unsigned long long> ts(size_t(a.tstamp_cap));
     PHX_CUDA(cudaMemcpyAsync(ts.data(), a.tstamp, ts.size() * 8, cudaMemcpyDeviceToHost, st));
@@ -1300,7 +1358,7 @@ void evaluate(phx_op op, const EvalIn& in, phx_run_record* rec, PendingEval* def
     return;
   }
   PHX_CUDA(cudaStreamSynchronize(st));
-  PHX_CUDA(cudaEventElapsedTime(&ms, op->ev0, op->ev1));
+  PHX_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
   {
     std::lock_guard<std::mutex> lk(g_trace_mu);
     g_last_ms = ms;
@@ -1434,6 +1492,9 @@ phx_status phx_op_create_csr(int64_t n, const int64_t* row_ptr, const int32_t* c
       PHX_CUDA(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
       PHX_CUDA(cudaEventCreate(&op->ev0));
       PHX_CUDA(cudaEventCreate(&op->ev1));
+      op->ws0.stream = op->stream;  // the operator's own workspace runs on its stream
+      op->ws0.ev0 = op->ev0;
+      op->ws0.ev1 = op->ev1;
       upload_csr(op, row_ptr, col_idx, vals);
       upload_plan(op, row_ptr, col_idx);
     } catch (...) {
@@ -1526,6 +1587,9 @@ phx_status phx_op_create_csr_partitioned(int64_t n, const int64_t* row_ptr,
       PHX_CUDA(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
       PHX_CUDA(cudaEventCreate(&op->ev0));
       PHX_CUDA(cudaEventCreate(&op->ev1));
+      op->ws0.stream = op->stream;  // the operator's own workspace runs on its stream
+      op->ws0.ev0 = op->ev0;
+      op->ws0.ev1 = op->ev1;
       // the selection replica: the whole CSR on part 0's device
       upload_csr(op, row_ptr, col_idx, vals);
     } catch (...) {
@@ -1558,17 +1622,20 @@ phx_status phx_op_destroy(phx_op op) {
     cudaGetDevice(&prev);
     cudaSetDevice(op->device);
     if (op->stream) cudaStreamSynchronize(op->stream);
-    for (DevBuf* b : {&op->Vw, &op->D0, &op->D1, &op->S, &op->F0, &op->F1, &op->E, &op->W, &op->V,
-                      &op->FLo, &op->FRo,
-                      &op->trace, &op->w0, &op->w1, &op->y, &op->chunkmax, &op->inv,
-                      &op->partial, &op->gcoef, &op->spx, &op->spy, &op->tstamp})
+    op->ws0.release();
+    for (auto& w : op->pool) {
+      if (w->stream) cudaStreamSynchronize(w->stream);
+      w->release();
+      if (w->ev0) cudaEventDestroy(w->ev0);
+      if (w->ev1) cudaEventDestroy(w->ev1);
+      if (w->stream) cudaStreamDestroy(w->stream);
+    }
+    op->pool.clear();
+    for (DevBuf* b : {&op->w0, &op->w1, &op->y, &op->chunkmax, &op->inv, &op->partial, &op->gcoef,
+                      &op->spx, &op->spy})
       b->release();
     for (HostBuf* b : {&op->h_small, &op->h_chunk, &op->h_inv, &op->h_part, &op->h_lens, &op->h_flag})
       b->release();
-    for (int k = 0; k < kCtlSlots; ++k) {
-      op->ctl[k].release();
-      op->h_ctl[k].release();
-    }
     if (op->d_rp) cudaFree(op->d_rp);
     if (op->d_ci) cudaFree(op->d_ci);
     if (op->d_av) cudaFree(op->d_av);
@@ -1734,8 +1801,12 @@ phx_status phx_phimv_block(phx_op op, int32_t r, const double* t, const double* 
     check_block_request(op, r, t, alpha, p, V, ldv, true);
     if (!params) throw_phx(PHX_EINVAL, "phimv_block: params is null");
     if (ldw < op->n) throw_phx(PHX_EINVAL, "phimv_block: W leading dimension below n");
-    std::lock_guard<std::mutex> lk(op->mu);
     DeviceGuard guard(op->device);
+    // concurrent evaluations on one handle each lease a workspace; a
+    // partitioned operator's evaluations serialize on the handle
+    std::unique_lock<std::mutex> plk(op->mu, std::defer_lock);
+    if (op->nparts > 1) plk.lock();
+    Lease lease(op);
     EvalIn in{};
     in.r = r;
     in.p = p;
@@ -1747,7 +1818,7 @@ phx_status phx_phimv_block(phx_op op, int32_t r, const double* t, const double* 
     in.params = *params;
     in.hW = W;
     in.ldw = ldw;
-    evaluate(op, in, rec);
+    evaluate(op, *lease.w, in, rec);
   });
 }
 
@@ -1759,8 +1830,10 @@ phx_status phx_phimv_block_device(phx_op op, int32_t r, const double* t, const d
     if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
     check_block_request(op, r, t, alpha, p, nullptr, op->n, false);
     if (!params || !d_V || !d_W) throw_phx(PHX_EINVAL, "phimv_block: null argument");
-    std::lock_guard<std::mutex> lk(op->mu);
     DeviceGuard guard(op->device);
+    std::unique_lock<std::mutex> plk(op->mu, std::defer_lock);
+    if (op->nparts > 1) plk.lock();
+    Lease lease(op);
     EvalIn in{};
     in.r = r;
     in.p = p;
@@ -1770,7 +1843,7 @@ phx_status phx_phimv_block_device(phx_op op, int32_t r, const double* t, const d
     in.tol = tol;
     in.params = *params;
     in.dW = d_W;
-    evaluate(op, in, rec);
+    evaluate(op, *lease.w, in, rec);
   });
 }
 
@@ -1804,8 +1877,10 @@ phx_status phx_phimv_block_device_parts(phx_op op, int32_t r, const double* t, c
     if (!params || !d_V_parts || !d_W_parts) throw_phx(PHX_EINVAL, "phimv_block: null argument");
     for (int q = 0; q < op->nparts; ++q)
       if (!d_V_parts[q] || !d_W_parts[q]) throw_phx(PHX_EINVAL, "phimv_block: null argument");
-    std::lock_guard<std::mutex> lk(op->mu);
     DeviceGuard guard(op->device);
+    std::unique_lock<std::mutex> plk(op->mu, std::defer_lock);
+    if (op->nparts > 1) plk.lock();
+    Lease lease(op);
     EvalIn in{};
     in.r = r;
     in.p = p;
@@ -1820,7 +1895,7 @@ phx_status phx_phimv_block_device_parts(phx_op op, int32_t r, const double* t, c
       in.dVp = d_V_parts;
       in.dWp = d_W_parts;
     }
-    evaluate(op, in, rec);
+    evaluate(op, *lease.w, in, rec);
   });
 }
 
@@ -1838,8 +1913,10 @@ phx_status phx_phimv(phx_op op, double t, double alpha, int32_t p, const double*
     if (!std::isfinite(t) || !std::isfinite(alpha))
       throw_phx(PHX_EINVAL, "phimv: t and alpha must be finite");
     if (!params) throw_phx(PHX_EINVAL, "phimv: params is null");
-    std::lock_guard<std::mutex> lk(op->mu);
     DeviceGuard guard(op->device);
+    std::unique_lock<std::mutex> plk(op->mu, std::defer_lock);
+    if (op->nparts > 1) plk.lock();
+    Lease lease(op);
     EvalIn in{};
     in.r = 1;
     in.p = p;
@@ -1854,7 +1931,7 @@ phx_status phx_phimv(phx_op op, double t, double alpha, int32_t p, const double*
     in.single = true;
     in.h_exp_v0 = exp_v0;
     in.h_tail = tail;
-    evaluate(op, in, rec);
+    evaluate(op, *lease.w, in, rec);
   });
 }
 
@@ -1927,7 +2004,7 @@ int* rk_step_enqueue(phx_op op, RkWork& w, double gamma, const double* d_u, doub
     in.params = ss;
     in.dW = dW;
     in.slot = k;
-    evaluate(op, in, nullptr, &pend[k]);
+    evaluate(op, op->ws0, in, nullptr, &pend[k]);
   };
   // g_n, f_n = A u + g_n, hf = h f_n; stage 2 alone (:38-57)
   a.mode = 0;
@@ -2052,6 +2129,7 @@ phx_status phx_exprk4s6_step(phx_op op, double gamma, const double* u, double h,
     rk_check_op(op, "exprk4s6_step");
     if (!u || !u_next || !params) throw_phx(PHX_EINVAL, "exprk4s6_step: null argument");
     std::lock_guard<std::mutex> lk(op->mu);
+    std::lock_guard<std::mutex> wlk(op->ws0.busy);  // the integrator's evaluations use ws0
     DeviceGuard guard(op->device);
     RkWork w;
     const size_t n = size_t(op->n);
@@ -2081,6 +2159,7 @@ phx_status phx_integrate(phx_op op, double gamma, const double* u0, double h, do
       throw_phx(PHX_EINVAL, "integrate: t_end is not a multiple of h");
     if (n_steps_out) *n_steps_out = n_steps;
     std::lock_guard<std::mutex> lk(op->mu);
+    std::lock_guard<std::mutex> wlk(op->ws0.busy);  // the integrator's evaluations use ws0
     DeviceGuard guard(op->device);
     RkWork w;
     const size_t n = size_t(op->n);

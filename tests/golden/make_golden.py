@@ -7,7 +7,11 @@ from the image), so the fixtures pin the oracle restatement: every fixture is
 long-double augmented-matrix reference (reference_w, oracle.cpp:53-91
 restated) that the oracle's W must match within the user tolerance.
 
-Usage:  python tests/golden/make_golden.py [small] [highprec] [full2] [full4] [full3]
+Usage:  python tests/golden/make_golden.py [small] [highprec] [full2] [full4] [full3] [c5big]
+
+c5big: C5 at n = 2^21 (419 recovery sweeps) -- the size from which the
+production kernel variants run C5 -- with the oracle's row-parallel loops on
+all host cores (bitwise those of one thread).
 """
 from __future__ import annotations
 
@@ -110,3 +114,9 @@ if __name__ == "__main__":
             highprec()
         elif w.startswith("full"):
             full(int(w[4:]))
+        elif w == "c5big":
+            O.set_threads(os.cpu_count() or 1)
+            wl, ss, W, rec, tr, dt = run_oracle(5, 1 << 21)
+            save_record("full_cfg5_s2097152", 5, 1 << 21, ss, W, rec, tr, store_W=False)
+            print(f"c5big: sel {dt[0]:.1f}s eval {dt[1]:.1f}s L_S={rec.series_len_S} "
+                  f"s_eff={rec.s_effective} sweeps={len(rec.series_lens_F)}", flush=True)

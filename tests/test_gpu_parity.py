@@ -418,3 +418,55 @@ def test_single_variant_grid_kernel_bitwise():
     assert res.stats.series_lens_F == rec.series_lens_F
     assert np.array_equal(res.w, w)
     assert np.array_equal(res.exp_v0, e0) and np.array_equal(res.tail, tail)
+
+
+def test_c5_dynamic_tail_variant_bitwise(monkeypatch):
+    """C5's production variant of k_phimv_block at full size -- the
+    dynamic-tail (1, 2, 2) short-batch-2 kernel, chosen from ~1.8 M rows --
+    forced (PHX_FORCE_DYN) at n = 2^14, where the oracle is quick: run record
+    and W bitwise the oracle's through 420 recovery sweeps."""
+    monkeypatch.setenv("PHX_BULK", "0")
+    monkeypatch.setenv("PHX_FORCE_DYN", "1")
+    p = P()
+    wl = p.workload(5, 1 << 14)
+    op = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    oop = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    ss = O.select_parameters(oop, 61, wl.tol)
+    Wo, ro = O.phimv_block(oop, wl.t, wl.alpha, wl.V, wl.tol, ss)
+    res = p.phimv_block(op, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol,
+                                              p.ScalingShift(*ss.astuple())))
+    var = p.last_eval_variant()
+    assert (var["Q"], var["V"], var["R"]) == (1, 2, 2)
+    assert (var["dynamic_tail"], var["short_batch"], var["latency_mode"]) == (1, 1, 0)
+    assert ro.s_effective > 400
+    assert (res.stats.series_len_S, res.stats.series_lens_F) == (ro.series_len_S, ro.series_lens_F)
+    assert np.array_equal(res.W, Wo)
+
+
+@pytest.mark.parametrize("bulk", ["1", "0"])
+def test_c5_production_size_bitwise(golden_dir, monkeypatch, bulk):
+    """C5 at n = 2^21 (419 recovery sweeps, ~16,000 grid steps), the size from
+    which both production kernels run it -- the bulk-copy kernel (merged
+    window-only stages) and k_phimv_block's dynamic-tail (1, 2, 2) batch-2
+    variant -- against the oracle's committed SHA-256 of W, sampled rows and
+    run record (tests/golden/full_cfg5_s2097152, make_golden.py c5big)."""
+    name = "full_cfg5_s2097152"
+    if not os.path.exists(os.path.join(golden_dir, name + ".json")):
+        pytest.skip("C5 2^21 fixture not generated")
+    monkeypatch.setenv("PHX_BULK", bulk)
+    meta, arr = load(golden_dir, name)
+    wl = P().workload(5, 1 << 21)
+    p = P()
+    op = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    ss = p.ScalingShift(*meta["params"])
+    res = p.phimv_block(op, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    var = p.last_eval_variant()
+    if bulk == "1":
+        assert var["dynamic_tail"] == 2
+    else:
+        assert (var["dynamic_tail"], var["short_batch"], var["R"]) == (1, 1, 2)
+    st = res.stats
+    assert (st.s_effective, st.series_len_S, st.series_lens_F, st.matvecs) == (
+        meta["s_effective"], meta["series_len_S"], meta["series_lens_F"], meta["matvecs"])
+    assert np.array_equal(res.W[arr["sample_rows"]], arr["sample_W"])
+    assert sha(res.W) == meta["W_sha256"]
