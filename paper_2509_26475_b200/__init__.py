@@ -84,6 +84,11 @@ ABI_SYMBOLS = (
 
 
 def lib_path() -> str:
+    """libphx.so, or the self-checking build libphx_checked.so (device-side
+    bounds checks; `make -C paper_2509_26475_b200/csrc checked`) when the
+    environment sets PHX_LIB=checked."""
+    if os.environ.get("PHX_LIB") == "checked":
+        return os.path.join(_LIBDIR, "libphx_checked.so")
     return os.path.join(_LIBDIR, "libphx.so")
 
 

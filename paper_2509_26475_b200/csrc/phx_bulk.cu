@@ -38,6 +38,17 @@ namespace cg = cooperative_groups;
 namespace phx {
 namespace {
 
+// PHX_CHECKS=1 (libphx_checked.so, `make checked`): device-side bounds checks
+// on every staged copy and slot -- the self-check used in place of
+// compute-sanitizer, which this pool does not allow
+#ifndef PHX_CHECKS
+#define PHX_CHECKS 0
+#endif
+#define PHX_CHECK(cond)              \
+  do {                               \
+    if (PHX_CHECKS && !(cond)) __trap(); \
+  } while (0)
+
 constexpr int kBW = kBulkConsumers + 1;  // warps per CTA
 constexpr int kProd = kBulkConsumers;    // the producer warp
 constexpr int kPB = 4;                   // tile positions per counter grab
@@ -290,6 +301,14 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
               unsigned nrow = unsigned(whi - wlo + nsgl + ((A ? 1 : 0) + (B ? 1 : 0)) * rows);
               for (int g = 0; g < ng; ++g) nrow += unsigned(d[12 + g] & 0xffff);
               const unsigned rb = unsigned(width) * 8u;
+              // the copies fit their stage regions
+              PHX_CHECK(whi - wlo <= (M > 1 ? TM + 2 : kPlanT + 2));
+              PHX_CHECK(e_hi - e_lo <= a.plan_emax * M && e_lo >= 0);
+              PHX_CHECK(L.sl + cn <= L.rp && L.av + an * 8 <= L.sl && L.rp + rn * 4 <= L.hdr);
+              PHX_CHECK(L.bytes <= SB && nsgl <= a.plan_sgl_cap);
+              for (int g = 0; g < ng; ++g)
+                PHX_CHECK((d[12 + g] >> 16) + (d[12 + g] & 0xffff) <= a.plan_rows &&
+                          d[8 + g] >= 0 && d[8 + g] + (d[12 + g] & 0xffff) <= n);
               mbar_arrive_tx(bf, unsigned(rn * 4 + cn + an * 8) + nrow * rb);
               bulk_g2s(st + L.rp, a.rp + base, unsigned(rn) * 4u, bf, pfirst);
               if (cn) bulk_g2s(st + L.sl, a.plan_slot + c0, unsigned(cn), bf, pfirst);
@@ -352,6 +371,9 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
           double a0 = 0.0, a1 = 0.0;
           // merged stages: the sub-tile's window starts dj rows into the stage's
           const int dj = max(base + (rr / kPlanT) * kPlanT - 1, 0) - wlo;
+          if (PHX_CHECKS && v)
+            for (int e = rps[rr] - e_lo; e < rps[rr + 1] - e_lo; ++e)
+              PHX_CHECK(e >= 0 && e < a.plan_emax * M && int(sls[e]) + dj < (M > 1 ? TM + 2 : a.plan_rows));
           if (v) gath(dr + dj * width, sls, avs, rps[rr] - e_lo, rps[rr + 1] - e_lo, c, a0, a1);
           const double* self = dr + (base + rr - wlo) * width;  // the row itself (window)
           const unsigned long long m =
