@@ -431,7 +431,7 @@ def main():
     launches = P.kernel_launches() - launches0
     elapsed = max(e0.elapsed_time(e1) for e0, e1 in evs) / 1e3  # max over devices
     value = args.steps / elapsed
-    var = P.last_eval_variant() if N == 1 else None
+    var = P.last_eval_variant()
     bulk = bool(var and var["dynamic_tail"] == 2)
     W_dev = np.concatenate([x.cpu().numpy() for x in dW], axis=1).T  # (n, r)
 

@@ -294,6 +294,13 @@ phx_status phx_last_eval_variant(int32_t* out8);
  * are filled. */
 phx_status phx_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* info6,
                          int32_t* desc, uint8_t* slot, int32_t* sgl);
+/* The tile plan of one row part [row0, row0 + nrows) of an n-row operator
+ * (row-partitioned operators, phx_op_create_csr_partitioned): tiles and entry
+ * slots part-local, window / group / single source rows global.
+ * phx_tile_plan(n, ...) is phx_tile_plan_part(n, ..., 0, n, ...). */
+phx_status phx_tile_plan_part(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                              int64_t row0, int64_t nrows, int32_t* info7, int32_t* desc,
+                              uint8_t* slot, int32_t* sgl);
 
 /* Device-event time (ms) of the last phimv_block evaluation kernel, and the
  * number of grid-wide steps it executed (S terms + promotion + recovery

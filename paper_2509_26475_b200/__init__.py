@@ -79,7 +79,7 @@ ABI_SYMBOLS = (
     "phx_mm_read_csr", "phx_mm_write_csr", "phx_op_create_mm", "phx_block_series_direct",
     "phx_last_eval_mode",
     "phx_last_eval_variant",
-    "phx_tile_plan", "phx_op_part_info", "phx_phimv_block_device_parts",
+    "phx_tile_plan", "phx_tile_plan_part", "phx_op_part_info", "phx_phimv_block_device_parts",
 )
 
 
@@ -87,8 +87,9 @@ def lib_path() -> str:
     """libphx.so, or the self-checking build libphx_checked.so (device-side
     bounds checks; `make -C paper_2509_26475_b200/csrc checked`) when the
     environment sets PHX_LIB=checked."""
-    if os.environ.get("PHX_LIB") == "checked":
-        return os.path.join(_LIBDIR, "libphx_checked.so")
+    v = os.environ.get("PHX_LIB")
+    if v:  # "checked", or a developer A/B build (csrc/Makefile `variant`)
+        return os.path.join(_LIBDIR, f"libphx_{v}.so")
     return os.path.join(_LIBDIR, "libphx.so")
 
 
@@ -150,6 +151,11 @@ def lib():
     L.phx_tile_plan.argtypes = [C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                 C.POINTER(C.c_uint8), C.POINTER(C.c_int32)]
+    if hasattr(L, "phx_tile_plan_part"):  # (older developer A/B builds lack it)
+        L.phx_tile_plan_part.argtypes = [C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                         C.c_int64, C.c_int64, C.POINTER(C.c_int32),
+                                         C.POINTER(C.c_int32), C.POINTER(C.c_uint8),
+                                         C.POINTER(C.c_int32)]
     L.phx_op_part_info.argtypes = [C.c_void_p, C.c_int32, i64p, i64p, i32p,
                                    C.POINTER(C.c_void_p)]
     L.phx_phimv_block_device_parts.argtypes = [C.c_void_p, C.c_int32, dp, dp, C.c_int32,
@@ -512,27 +518,31 @@ def last_eval_variant() -> dict:
     return dict(zip(keys, (int(x) for x in out)))
 
 
-def tile_plan(n, row_ptr, col_idx):
+def tile_plan(n, row_ptr, col_idx, row0=0, nrows=None):
     """The bulk-copy evaluator's tile plan of a host CSR (built on the host,
-    as phx_op_create_csr builds it): (info dict, desc (tiles x 16), slot
-    (nnz + 16 bytes), sgl) -- arrays None when the plan does not fit."""
+    as phx_op_create_csr builds it) -- or, with row0 / nrows, of the row part
+    [row0, row0 + nrows) as phx_op_create_csr_partitioned builds it (tiles and
+    slots part-local, source rows global): (info dict, desc (tiles x 16),
+    slot (part nnz + 16 bytes), sgl) -- arrays None when the plan does not
+    fit."""
+    nrows = int(n) - int(row0) if nrows is None else int(nrows)
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
     ci = np.ascontiguousarray(col_idx, dtype=np.int32)
     info = np.zeros(7, dtype=np.int32)
     i32 = C.POINTER(C.c_int32)
-    _check(lib().phx_tile_plan(int(n), rp.ctypes.data_as(C.POINTER(C.c_int64)),
-                               ci.ctypes.data_as(i32), info.ctypes.data_as(i32), None, None, None))
+    i64p = C.POINTER(C.c_int64)
+    L = lib()
+    args = (int(n), rp.ctypes.data_as(i64p), ci.ctypes.data_as(i32), int(row0), nrows)
+    _check(L.phx_tile_plan_part(*args, info.ctypes.data_as(i32), None, None, None))
     keys = ("ok", "tiles", "rows", "singles_cap", "emax", "singles", "T")
     d = dict(zip(keys, (int(x) for x in info)))
     if not d["ok"]:
         return d, None, None, None
     desc = np.zeros((d["tiles"], 16), dtype=np.int32)
-    slot = np.zeros(int(rp[-1]) + 16, dtype=np.uint8)
+    slot = np.zeros(int(rp[row0 + nrows] - rp[row0]) + 16, dtype=np.uint8)
     sgl = np.zeros(d["singles"] + 1, dtype=np.int32)
-    _check(lib().phx_tile_plan(int(n), rp.ctypes.data_as(C.POINTER(C.c_int64)),
-                               ci.ctypes.data_as(i32), info.ctypes.data_as(i32),
-                               desc.ctypes.data_as(i32),
-                               slot.ctypes.data_as(C.POINTER(C.c_uint8)), sgl.ctypes.data_as(i32)))
+    _check(L.phx_tile_plan_part(*args, info.ctypes.data_as(i32), desc.ctypes.data_as(i32),
+                                slot.ctypes.data_as(C.POINTER(C.c_uint8)), sgl.ctypes.data_as(i32)))
     return d, desc, slot, sgl
 
 

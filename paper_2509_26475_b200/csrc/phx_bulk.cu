@@ -126,16 +126,77 @@ __device__ __forceinline__ void publish_b(unsigned long long a, unsigned long lo
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
-  const BlockArgs& a = ga;
+// PART: a row-partitioned operator.  The launch runs parts
+// plo .. plo+pcount-1 with the CTAs split evenly; a CTA binds its part's
+// row-local buffers, CSR and tile plan (rows are part-local from there on).
+// The plan's window / group / single source rows are GLOBAL rows: the
+// producer cuts every staged range at the part boundaries and copies each
+// piece from its owner's buffer (peer-GPU memory over NVLink in a multi-GPU
+// run), so the consumers -- and every row's arithmetic -- are unchanged.  The
+// per-step maxima are combined through the parts' mailboxes (system scope),
+// which is also the step barrier across devices.
+#ifdef PHX_BULK_MAXNREG
+#define PHX_BULK_BOUNDS __maxnreg__(PHX_BULK_MAXNREG)
+#else
+#define PHX_BULK_BOUNDS __launch_bounds__(kBulkThreads, kBulkConsumers > 8 ? 1 : 2)
+#endif
+template <bool PART>
+__global__ void PHX_BULK_BOUNDS k_phimv_bulk(BlockArgs ga) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ unsigned long long bar_full[kBulkMaxStages], bar_empty[kBulkMaxStages];
   __shared__ unsigned long long red[2][kBW];
   __shared__ __align__(16) int pdesc[2][kPB][kPlanDesc];  // producer: descriptor batches
+  __shared__ __align__(16) unsigned char s_pa_raw[PART ? sizeof(BlockArgs) : 16];
+  __shared__ const double* gtab[5][PART ? kMaxParts : 1];  // [D0, D1, S, F0, F1][part]
+  __shared__ int sbnd[PART ? kMaxParts + 1 : 1];           // part row boundaries (global)
+  __shared__ double gmax[2];
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int cta = int(blockIdx.x), ncta = int(gridDim.x);
+  int my = 0, cta = int(blockIdx.x), ncta = int(gridDim.x);
+  const PartTab* T = nullptr;
+  const int Ng = ga.n;  // global rows
+  if (PART) {
+    const int per = int(gridDim.x) / ga.pcount;
+    my = ga.plo + int(blockIdx.x) / per;
+    cta = int(blockIdx.x) % per;
+    ncta = per;
+    T = ga.ptab + my;
+    if (threadIdx.x == 0) {
+      BlockArgs pa = ga;
+      pa.n = T->nrows;
+      pa.rp = T->rp;
+      pa.ci = T->ci;
+      pa.av = T->av;
+      pa.V = T->V;
+      pa.Vw = T->Vw;
+      pa.D0 = T->D0;
+      pa.D1 = T->D1;
+      pa.S = T->S;
+      pa.F0 = T->F0;
+      pa.F1 = T->F1;
+      pa.E = T->E;
+      pa.W = T->W;
+      pa.slots = T->slots;
+      pa.plan_desc = T->plan_desc;
+      pa.plan_slot = T->plan_slot;
+      pa.plan_sgl = T->plan_sgl;
+      *reinterpret_cast<BlockArgs*>(s_pa_raw) = pa;
+    }
+    for (int q = threadIdx.x; q < ga.nparts; q += blockDim.x) {
+      const PartTab& U = ga.ptab[q];
+      gtab[0][q] = U.D0;
+      gtab[1][q] = U.D1;
+      gtab[2][q] = U.S;
+      gtab[3][q] = U.F0;
+      gtab[4][q] = U.F1;
+      sbnd[q] = U.row0;
+    }
+    if (threadIdx.x == 0) sbnd[ga.nparts] = Ng;
+    __syncthreads();
+  }
+  const BlockArgs& a = PART ? *reinterpret_cast<const BlockArgs*>(s_pa_raw) : ga;
+  const int row0 = PART ? T->row0 : 0;
   const int NS = a.bulk_ns, SB = a.bulk_stage_bytes;
   const bool sleepw = (a.bulk_flags & 2) != 0;
   if (threadIdx.x == 0) {
@@ -151,7 +212,8 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
   const int w = a.w, fc = a.fcols;
   const unsigned ldb = unsigned(a.ldb), ldf = unsigned(a.ldf);
   const bool has_xi = a.xi != 0.0;
-  const bool master = blockIdx.x == 0 && threadIdx.x == 0;
+  const bool master = blockIdx.x == 0 && threadIdx.x == 0 && (!PART || ga.plo == 0);
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;  // writes this launch's status
   const int nblk = (n + kPlanT - 1) / kPlanT;  // row blocks = plan tiles
   int kpipe = 0;                               // ring stages used so far (producer == consumers)
   int step = 0, tr_len = 0;
@@ -172,24 +234,71 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
   auto sync_step = [&](unsigned long long ma, unsigned long long mb, double& ra, double& rb) {
     unsigned long long* slot = a.slots + 4 * (step % 3);
     publish_b(ma, mb, slot, red);
-    if (master) {
-      unsigned long long* nxt = a.slots + 4 * ((step + 1) % 3);
-      nxt[0] = 0ull;
-      nxt[1] = 0ull;
-      nxt[2] = 0ull;  // the next step's tile counter
+    if (!PART) {
+      if (master) {
+        unsigned long long* nxt = a.slots + 4 * ((step + 1) % 3);
+        nxt[0] = 0ull;
+        nxt[1] = 0ull;
+        nxt[2] = 0ull;  // the next step's tile counter
+      }
+      grid.sync();
+      if (master && a.tstamp != nullptr && step < a.tstamp_cap) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        a.tstamp[step] = ns;
+      }
+      ra = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot)));
+      rb = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot + 1)));
+    } else {
+      // part-local arrival; the part's last CTA publishes the part's maxima
+      // into every part's mailbox (peer memory, double-buffered by step
+      // parity) and everyone waits until all parts have published this step
+      // (the same protocol as k_phimv_block's partitioned variants)
+      if (threadIdx.x == 0) {
+        const unsigned gen = unsigned(step) + 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(T->arrive + (step % 3), 1u);
+        if (old == unsigned(ncta) - 1u) {
+          __threadfence();
+          const unsigned long long A = __ldcg(slot), Bv = __ldcg(slot + 1);
+          unsigned long long* nxt = a.slots + 4 * ((step + 1) % 3);
+          nxt[0] = 0ull;
+          nxt[1] = 0ull;
+          nxt[2] = 0ull;  // the part's next tile counter
+          T->arrive[(step + 1) % 3] = 0u;
+          const int buf = (step & 1) * ga.nparts;
+          for (int q = 0; q < ga.nparts; ++q) {
+            MailBox* mbx = ga.ptab[q].mbox + buf + my;
+            mbx->a = A;
+            mbx->b = Bv;
+          }
+          // release at system scope: the mailboxes may be peer-GPU memory
+          __threadfence_system();
+          for (int q = 0; q < ga.nparts; ++q) atomicExch_system(&(ga.ptab[q].mbox + buf + my)->gen, gen);
+        }
+        unsigned long long A = 0, Bv = 0;
+        for (int q = 0; q < ga.nparts; ++q) {
+          const MailBox* mbx = T->mbox + (step & 1) * ga.nparts + q;
+          while (ld_acquire_sys(&mbx->gen) < gen) {
+          }
+          A = umax64(A, ld_relaxed_sys(&mbx->a));
+          Bv = umax64(Bv, ld_relaxed_sys(&mbx->b));
+        }
+        gmax[0] = from_bits(A);
+        gmax[1] = from_bits(Bv);
+        // the next step's bulk copies read other parts' rows written before
+        // their arrival: make them visible to this CTA's async proxy
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+      }
+      __syncthreads();
+      ra = gmax[0];
+      rb = gmax[1];
     }
-    grid.sync();
-    if (master && a.tstamp != nullptr && step < a.tstamp_cap) {
-      unsigned long long ns;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-      a.tstamp[step] = ns;
-    }
-    ra = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot)));
-    rb = from_bits(__ldcg(reinterpret_cast<const unsigned long long*>(slot + 1)));
     ++step;
   };
   auto finish = [&](int err, int idx, int L_S, int extra_steps) {
-    if (master) {
+    if (lead) {
       a.status[0] = err;
       a.status[1] = idx;
       a.status[2] = L_S;
@@ -222,8 +331,28 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
   // stage holds (narrow recovery terms: up to kMaxMerge): fewer, larger
   // copies and barrier handshakes per byte.  A sub-tile's slots address its
   // own window; the consumer shifts them into the merged window.
-  auto bulk_phase = [&](int G, int ow, int width, const double* X, const double* A, const double* B,
-                        auto&& gath, auto&& epi) -> unsigned long long {
+  // stage `cnt` GLOBAL rows from g0 of gather source X (row width `width`;
+  // PART: buffer xsel of each owning part) into dst
+  auto copy_rows = [&](unsigned char* dst, const double* X, int xsel, int width, int g0, int cnt,
+                       unsigned long long* bf, unsigned long long pol) {
+    const unsigned rb = unsigned(width) * 8u;
+    if (!PART) {
+      bulk_g2s(dst, X + size_t(g0) * width, unsigned(cnt) * rb, bf, pol);
+      return;
+    }
+    while (cnt > 0) {
+      int q = 0;
+      while (sbnd[q + 1] <= g0) ++q;
+      const int c = min(cnt, sbnd[q + 1] - g0);
+      const double* src = (q == my ? X : gtab[xsel][q]) + size_t(g0 - sbnd[q]) * width;
+      bulk_g2s(dst, src, unsigned(c) * rb, bf, pol);
+      dst += size_t(c) * rb;
+      g0 += c;
+      cnt -= c;
+    }
+  };
+  auto bulk_phase = [&](int G, int ow, int width, const double* X, int xsel, const double* A,
+                        const double* B, auto&& gath, auto&& epi) -> unsigned long long {
     const int nst = (A ? 1 : 0) + (B ? 1 : 0);
     int M = 1;
     if (a.plan_merge)
@@ -294,7 +423,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
               const int base = t * TM, rows = min(TM, n - base);
               const int ng = M == 1 ? d[0] : 0;
               const int e_lo = d[3], e_hi = d[4];
-              const int wlo = max(base - 1, 0), whi = min(base + rows + 1, n);
+              const int wlo = max(row0 + base - 1, 0), whi = min(row0 + base + rows + 1, Ng);
               const int c0 = e_lo & ~15, cn = (e_hi - c0 + 15) & ~15;  // slot bytes
               const int a0 = e_lo & ~1, an = (e_hi - a0 + 1) & ~1;    // values (16 B granules)
               const int rn = (rows + 1 + 3) & ~3;                     // row_ptr entries
@@ -308,16 +437,15 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
               PHX_CHECK(L.bytes <= SB && nsgl <= a.plan_sgl_cap);
               for (int g = 0; g < ng; ++g)
                 PHX_CHECK((d[12 + g] >> 16) + (d[12 + g] & 0xffff) <= a.plan_rows &&
-                          d[8 + g] >= 0 && d[8 + g] + (d[12 + g] & 0xffff) <= n);
+                          d[8 + g] >= 0 && d[8 + g] + (d[12 + g] & 0xffff) <= Ng);
               mbar_arrive_tx(bf, unsigned(rn * 4 + cn + an * 8) + nrow * rb);
               bulk_g2s(st + L.rp, a.rp + base, unsigned(rn) * 4u, bf, pfirst);
               if (cn) bulk_g2s(st + L.sl, a.plan_slot + c0, unsigned(cn), bf, pfirst);
               if (an) bulk_g2s(st + L.av, a.av + a0, unsigned(an) * 8u, bf, pfirst);
-              bulk_g2s(st + L.dr, X + size_t(wlo) * width, unsigned(whi - wlo) * rb, bf, plast);
+              copy_rows(st + L.dr, X, xsel, width, wlo, whi - wlo, bf, plast);
               for (int g = 0; g < ng; ++g) {
                 const int cnt = d[12 + g] & 0xffff, dst = d[12 + g] >> 16;
-                bulk_g2s(st + L.dr + dst * int(rb), X + size_t(d[8 + g]) * width, unsigned(cnt) * rb,
-                         bf, plast);
+                copy_rows(st + L.dr + dst * int(rb), X, xsel, width, d[8 + g], cnt, bf, plast);
               }
               if (A) bulk_g2s(st + L.sa, A + size_t(base) * width, unsigned(rows) * rb, bf, pfirst);
               if (B) bulk_g2s(st + L.sb, B + size_t(base) * width, unsigned(rows) * rb, bf, pfirst);
@@ -325,8 +453,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
           }
           if (t >= 0 && lane < nsgl) {  // single rows, one lane each
             const int col = __ldg(a.plan_sgl + d[2] + lane);
-            bulk_g2s(st + L.dr + (kPlanT + 2 + lane) * width * 8, X + size_t(col) * width,
-                     unsigned(width) * 8u, bf, plast);
+            copy_rows(st + L.dr + (kPlanT + 2 + lane) * width * 8, X, xsel, width, col, 1, bf, plast);
           }
           __syncwarp();
           ++kpipe;
@@ -364,18 +491,18 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
         const unsigned char* sls = st + L.sl + (e_lo & 15);
         const double* avs = reinterpret_cast<const double*>(st + L.av) + (e_lo & 1);
         const int base = t * TM, rows = min(TM, n - base);
-        const int wlo = max(base - 1, 0);
+        const int wlo = max(row0 + base - 1, 0);  // global
         for (int r0 = warp * gpw; r0 < rows; r0 += kBulkConsumers * gpw) {
           const int rr = r0 + g;
           const bool v = rr < rows && cv;
           double a0 = 0.0, a1 = 0.0;
           // merged stages: the sub-tile's window starts dj rows into the stage's
-          const int dj = max(base + (rr / kPlanT) * kPlanT - 1, 0) - wlo;
+          const int dj = max(row0 + base + (rr / kPlanT) * kPlanT - 1, 0) - wlo;
           if (PHX_CHECKS && v)
             for (int e = rps[rr] - e_lo; e < rps[rr + 1] - e_lo; ++e)
               PHX_CHECK(e >= 0 && e < a.plan_emax * M && int(sls[e]) + dj < (M > 1 ? TM + 2 : a.plan_rows));
           if (v) gath(dr + dj * width, sls, avs, rps[rr] - e_lo, rps[rr + 1] - e_lo, c, a0, a1);
-          const double* self = dr + (base + rr - wlo) * width;  // the row itself (window)
+          const double* self = dr + (row0 + base + rr - wlo) * width;  // the row itself (window)
           const unsigned long long m =
               epi(v, rr < rows, base + rr, c, a0, a1, self, sa + rr * width + c, sb + rr * width + c, lg, G);
           mx = umax64(mx, m);
@@ -525,9 +652,9 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
       }
     }
     double* const Dn1 = Dn;
-    const double sig1 = sigma;
+    const double sig1 = sigma, rsig1 = 1.0 / sigma;
     const unsigned long long mdb = bulk_phase(
-        GS, w, p1e, a.D0, nullptr, nullptr,
+        GS, w, p1e, a.D0, 0, nullptr, nullptr,
         // acc = sum_e av_e * Vw_1[col_e] = av_e * fl(V[col_e][src] * g)
         [&](const double* dr, const unsigned char* sls, const double* avs, int e0, int e1, int,
             double& a0, double& a1) {
@@ -556,7 +683,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
               if (has_xi) y = y - a.xi * vw;
               y = y * tos[e];
               dn[e] = y + g2;
-              sn[e] = vw + dn[e] / sig1;  // S += D/sigma (:105)
+              sn[e] = vw + div_rcp(dn[e], sig1, rsig1);  // S += D/sigma (:105)
               ad[0][e] = fabs(dn[e]);
             }
             const unsigned o = unsigned(row) * ldb + c;
@@ -668,7 +795,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     sig_prev = sigma;
     sigma *= k;
     double* const Dnn = Dn;
-    const double sig = sigma, sigp = sig_prev;
+    const double sig = sigma, sigp = sig_prev, rsig = 1.0 / sigma, rsigp = 1.0 / sig_prev;
     // Vw_k[c] = fl(fl(+0 + Vw_{k-1}[c - r] Ka) + Vw_{k-1}[c] Kd) (:98)
     auto vw_next = [&](int e, double vw, double vl) {
       double g2 = 0.0;
@@ -687,7 +814,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     if (!s_stale) {
       // skip term: Vw_{k-1} in, D_k out
       mdb = bulk_phase(
-          GS, w, w, Dc, a.Vw, nullptr, gath_pair(w),
+          GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, nullptr, gath_pair(w),
           [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
               const double* pa, const double*, int, int G) -> unsigned long long {
             double ad[1][2] = {{0.0, 0.0}};
@@ -714,7 +841,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
     } else {
       // fold term: Vw_{k-2} and S_{k-2} in; Vw_k, D_k, S_k out
       mdb = bulk_phase(
-          GS, w, w, Dc, a.Vw, a.S, gath_pair(w),
+          GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, a.S, gath_pair(w),
           [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
               const double* pa, const double* pb, int, int G) -> unsigned long long {
             double ad[1][2] = {{0.0, 0.0}};
@@ -748,8 +875,8 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
                 }
                 vn[e] = vw_next(e, wc, wl);            // Vw_k
                 dn[e] = d_next(e, acc[e], dpv[e], vn[e]);  // D_k (ds = D_{k-1} row)
-                const double s1 = sov[e] + dpv[e] / sigp;  // S_{k-1} (:105)
-                sn[e] = s1 + dn[e] / sig;                  // S_k
+                const double s1 = sov[e] + div_rcp(dpv[e], sigp, rsigp);  // S_{k-1} (:105)
+                sn[e] = s1 + div_rcp(dn[e], sig, rsig);                   // S_k
                 ad[0][e] = fabs(dn[e]);
               }
               const unsigned o = unsigned(row) * ldb + c;
@@ -811,7 +938,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
   double* Fn = a.F1;
   const bool sweeps = a.s_eff > 1;
   const unsigned long long mf = bulk_phase(
-      GF, fc, w, a.S, nullptr, nullptr,
+      GF, fc, w, a.S, 2, nullptr, nullptr,
       // gathers S block-0 columns (left F columns live at the same column
       // index in S); a pair straddling the left/right split gathers one extra
       // column, unused
@@ -933,10 +1060,10 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
       ++kk;
       d1 = d2;
       const double fac = a.single_variant ? a.t_single / (double(a.s_eff) * kk) : 0.0;
-      const double dkk = double(kk);
+      const double dkk = double(kk), rkk = 1.0 / dkk;
       double* const Fnn = Fn;
       const unsigned long long mfb = bulk_phase(
-          GF, fc, fc, Fc, a.E, nullptr, gath_pair(fc),
+          GF, fc, fc, Fc, Fc == a.F0 ? 3 : 4, a.E, nullptr, gath_pair(fc),
           [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
               const double* pa, const double*, int, int G) -> unsigned long long {
             double ay[1][2] = {{0.0, 0.0}};
@@ -953,7 +1080,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
                 if (a.single_variant) {
                   yv = fac * yv;  // phi_single.cpp:106
                 } else {
-                  yv = yv / dkk;        // phi_block.cpp:132
+                  yv = div_rcp(yv, dkk, rkk);  // phi_block.cpp:132
                   yv = yv * tosF[e];  // :134-135
                 }
                 y[e] = yv;
@@ -989,7 +1116,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
       Fn = tmp;
     }
     if (err != kStOk) break;
-    if (master) a.lensF[sweep - 1] = kk;
+    if (lead) a.lensF[sweep - 1] = kk;
 
     // ---- sweep end (:141-145): E *= mu; Sadv = Sadv*Jexp; F refresh
     // phase A (S layout): Sadv blocks 1..p in place, ascending source column
@@ -1074,23 +1201,24 @@ __global__ void __launch_bounds__(kBulkThreads, 2) k_phimv_bulk(BlockArgs ga) {
 
 }  // namespace
 
-cudaError_t bulk_occupancy(size_t smem, int* per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_phimv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(smem));
+cudaError_t bulk_occupancy(size_t smem, int* per_sm, bool part) {
+  const void* f = part ? reinterpret_cast<const void*>(k_phimv_bulk<true>)
+                       : reinterpret_cast<const void*>(k_phimv_bulk<false>);
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_phimv_bulk, kBulkThreads, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, f, kBulkThreads, smem);
 }
 
-cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st, bool part) {
   BlockArgs copy = a;
   void* args[] = {&copy};
   const size_t smem = size_t(a.bulk_ns) * size_t(a.bulk_stage_bytes);
-  cudaError_t e = cudaFuncSetAttribute(k_phimv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(smem));
+  const void* f = part ? reinterpret_cast<const void*>(k_phimv_bulk<true>)
+                       : reinterpret_cast<const void*>(k_phimv_bulk<false>);
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   count_launch();
-  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_phimv_bulk), grid,
-                                     kBulkThreads, args, smem, st);
+  return cudaLaunchCooperativeKernel(f, grid, kBulkThreads, args, smem, st);
 }
 
 }  // namespace phx

@@ -145,6 +145,12 @@ struct PartDev {
   double* av = nullptr;
   cudaStream_t stream = nullptr;
   DevBuf Vw, D0, D1, S, F0, F1, E, W, V, coef, slots, arrive, mbox, status, lensF, trace, ptab;
+  // the part's tile plan for the bulk kernel (global source rows)
+  int32_t* plan_desc = nullptr;
+  uint8_t* plan_slot = nullptr;
+  int32_t* plan_sgl = nullptr;
+  int32_t plan_rows = 0, plan_sgl_cap = 0, plan_emax = 0;
+  bool plan_ok = false, plan_merge = false;
 };
 
 // control-block slots per workspace: evaluations that may be in flight at
@@ -699,6 +705,52 @@ BulkChoice bulk_choice(phx_op op, int32_t V, int32_t QS, int32_t QF, int32_t w, 
   return bc;
 }
 
+// The same choice for a row-partitioned operator: every part has a tile
+// plan; the ring is sized for the largest part plan (parts on one device
+// share a launch, so they share the stage layout).
+struct BulkPartChoice : BulkChoice {
+  int32_t rows = 0, sgl_cap = 0, emax = 0;
+  bool merge = true;
+};
+BulkPartChoice bulk_choice_parts(phx_op op, int32_t V, int32_t QS, int32_t QF, int32_t w,
+                                 int32_t fcols) {
+  BulkPartChoice bc;
+  const char* env = std::getenv("PHX_BULK");
+  const int mode = env ? std::atoi(env) : -1;
+  if (mode == 0 || V != 2 || QS != 1 || QF != 1) return bc;
+  if (mode != 1 && op->n < (int64_t(1) << 21)) return bc;
+  for (const PartDev& d : op->parts) {
+    if (!d.plan_ok) return bc;
+    bc.rows = std::max(bc.rows, d.plan_rows);
+    bc.sgl_cap = std::max(bc.sgl_cap, d.plan_sgl_cap);
+    bc.emax = std::max(bc.emax, d.plan_emax);
+    bc.merge = bc.merge && d.plan_merge;
+  }
+  const phx::BulkStage ls = phx::bulk_stage(bc.rows, bc.emax, w, 2);
+  const phx::BulkStage lf = phx::bulk_stage(bc.rows, bc.emax, fcols, 1);
+  int32_t sb = std::max(ls.bytes, lf.bytes);
+  if (bc.merge) sb = std::max(sb, int32_t(48 * 1024));
+  const int dev = op->parts[0].dev;
+  DeviceGuard guard(dev);
+  int optin = 0;
+  PHX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  for (int want : {2, 1})
+    for (int ns = phx::kBulkMaxStages; ns >= 2; --ns) {
+      const size_t smem = size_t(ns) * size_t(sb);
+      if (smem > size_t(optin)) continue;
+      int per = 0;
+      PHX_CUDA(phx::bulk_occupancy(smem, &per, true));
+      if (per >= want) {
+        bc.use = true;
+        bc.ns = ns;
+        bc.stage_bytes = sb;
+        bc.per_sm = want;
+        return bc;
+      }
+    }
+  return bc;
+}
+
 // ---------------------------------------------------------------------------
 // Block evaluator (phi_block.cpp:48-157) / single evaluator
 // (phi_single.cpp:38-127, r = 1) — host preparation + one persistent launch.
@@ -784,6 +836,9 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     T.mbox = d.mbox.as<phx::MailBox>(2 * size_t(P));  // [step parity][part]
     T.row0 = int32_t(d.row0);
     T.nrows = int32_t(d.nrows);
+    T.plan_desc = d.plan_desc;
+    T.plan_slot = d.plan_slot;
+    T.plan_sgl = d.plan_sgl;
     if (host_io)
       PHX_CUDA(cudaMemcpy2DAsync(dV, nr * 8, in.hV + d.row0, size_t(in.ldv) * 8, nr * 8,
                                  size_t(p + 1), cudaMemcpyHostToDevice, d.stream));
@@ -855,6 +910,12 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
               phx::eval_cluster_smem(int32_t(max_rows), int32_t(max_nnz), cl_tile, ldb, ldf) <=
                   size_t(optin);
   }
+  // the bulk-copy kernel (phx_bulk.cu, PART instantiation) when every part
+  // has a tile plan: the parts' CTAs stage their gathers -- peer rows
+  // included -- with cp.async.bulk
+  const BulkPartChoice bulk = cluster ? BulkPartChoice{}
+                                      : bulk_choice_parts(op, base.vec, base.QS, base.QF, base.w,
+                                                          base.fcols);
   // per launch group: start / end events on its device (the evaluation's
   // time is the slowest group's)
   struct EvPair {
@@ -916,6 +977,32 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
       }
       continue;
     }
+    if (bulk.use) {
+      a.plan_rows = bulk.rows;
+      a.plan_sgl_cap = bulk.sgl_cap;
+      a.plan_emax = bulk.emax;
+      a.plan_merge = bulk.merge ? 1 : 0;
+      a.bulk_ns = bulk.ns;
+      a.bulk_stage_bytes = bulk.stage_bytes;
+      const char* fe = std::getenv("PHX_BULK_FLAGS");
+      a.bulk_flags = fe ? std::atoi(fe) : 2;
+      a.dyn = 2;
+      a.lat = 0;
+      a.bsmall = 0;
+      int sms = 0;
+      PHX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.dev));
+      const int per = std::max(1, bulk.per_sm * sms / g.pcount);
+      PHX_CUDA(cudaEventRecord(ev.e0, d.stream));
+      PHX_CUDA(phx::launch_phimv_bulk(a, per * g.pcount, d.stream, true));
+      PHX_CUDA(cudaEventRecord(ev.e1, d.stream));
+      {
+        std::lock_guard<std::mutex> lk(g_trace_mu);
+        g_last_mode = 1;
+        const int32_t var[8] = {a.QT, a.vec, a.R, 2, 0, 0, per * g.pcount, phx::kBulkThreads};
+        std::memcpy(g_last_variant, var, sizeof var);
+      }
+      continue;
+    }
     int max_blocks = 0;
     PHX_CUDA(phx::coop_grid_size(a.QT, a.vec, a.R, true, true, a.bsmall != 0, block, &max_blocks));
     int64_t most = 1;
@@ -928,6 +1015,8 @@ void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::v
     {
       std::lock_guard<std::mutex> lk(g_trace_mu);
       g_last_mode = 1;
+      const int32_t var[8] = {a.QT, a.vec, a.R, a.dyn, 0, a.bsmall, per * g.pcount, block};
+      std::memcpy(g_last_variant, var, sizeof var);
     }
   }
   // collect: status / sweep lengths / trace from part 0's launch, W slices
@@ -1120,6 +1209,7 @@ void evaluate(phx_op op, Workspace& ws, const EvalIn& in, phx_run_record* rec,
   }
   if (op->nparts > 1) {
     phx::BlockArgs b{};
+    b.n = int32_t(n);  // global rows (the bulk kernel's part boundaries end at n)
     b.p = p;
     b.r = r;
     b.w = w;
@@ -1549,7 +1639,10 @@ phx_status phx_op_create_csr_partitioned(int64_t n, const int64_t* row_ptr,
         d.nrows = bnd[size_t(q + 1)] - bnd[size_t(q)];
         const int64_t e0 = row_ptr[d.row0], e1 = row_ptr[d.row0 + d.nrows];
         d.nnz = e1 - e0;
-        std::vector<int32_t> rp(size_t(d.nrows) + 1), ci(std::max<size_t>(1, size_t(d.nnz)));
+        // row_ptr / values padded past their ends like upload_csr's (the bulk
+        // kernel copies tile slices in whole 16-byte granules)
+        std::vector<int32_t> rp(size_t(d.nrows) + 1 + 8 * 32 + 16, int32_t(d.nnz));
+        std::vector<int32_t> ci(std::max<size_t>(1, size_t(d.nnz)));
         for (int64_t i = 0; i <= d.nrows; ++i) rp[size_t(i)] = int32_t(row_ptr[d.row0 + i] - e0);
         for (int64_t e = e0; e < e1; ++e) {
           const int64_t col = col_idx[e];
@@ -1563,11 +1656,28 @@ phx_status phx_op_create_csr_partitioned(int64_t n, const int64_t* row_ptr,
         PHX_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
         PHX_CUDA(cudaMalloc(&d.rp, rp.size() * 4));
         PHX_CUDA(cudaMalloc(&d.ci, ci.size() * 4));
-        PHX_CUDA(cudaMalloc(&d.av, std::max<size_t>(1, size_t(d.nnz)) * 8));
+        PHX_CUDA(cudaMalloc(&d.av, (size_t(d.nnz) + 2) * 8));
         PHX_CUDA(cudaMemcpy(d.rp, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
+        PHX_CUDA(cudaMemset(d.av, 0, (size_t(d.nnz) + 2) * 8));
         if (d.nnz > 0) {
           PHX_CUDA(cudaMemcpy(d.ci, ci.data(), size_t(d.nnz) * 4, cudaMemcpyHostToDevice));
           PHX_CUDA(cudaMemcpy(d.av, vals + e0, size_t(d.nnz) * 8, cudaMemcpyHostToDevice));
+          // the part's tile plan: part-local tiles and slots, global sources
+          phx::TilePlan plan;
+          if (phx::build_tile_plan(d.nrows, row_ptr + d.row0, col_idx, &plan, d.row0, n)) {
+            PHX_CUDA(cudaMalloc(&d.plan_desc, plan.desc.size() * 4));
+            PHX_CUDA(cudaMalloc(&d.plan_slot, plan.slot.size()));
+            PHX_CUDA(cudaMalloc(&d.plan_sgl, plan.sgl.size() * 4));
+            PHX_CUDA(cudaMemcpy(d.plan_desc, plan.desc.data(), plan.desc.size() * 4,
+                                cudaMemcpyHostToDevice));
+            PHX_CUDA(cudaMemcpy(d.plan_slot, plan.slot.data(), plan.slot.size(), cudaMemcpyHostToDevice));
+            PHX_CUDA(cudaMemcpy(d.plan_sgl, plan.sgl.data(), plan.sgl.size() * 4, cudaMemcpyHostToDevice));
+            d.plan_rows = plan.rows;
+            d.plan_sgl_cap = plan.sgl_cap;
+            d.plan_emax = plan.emax;
+            d.plan_merge = plan.rows == phx::kPlanT + 2;
+            d.plan_ok = true;
+          }
         }
       }
       // peer access between the parts' devices (NVLink P2P)
@@ -1615,6 +1725,9 @@ phx_status phx_op_destroy(phx_op op) {
     if (d.rp) cudaFree(d.rp);
     if (d.ci) cudaFree(d.ci);
     if (d.av) cudaFree(d.av);
+    if (d.plan_desc) cudaFree(d.plan_desc);
+    if (d.plan_slot) cudaFree(d.plan_slot);
+    if (d.plan_sgl) cudaFree(d.plan_sgl);
     if (d.stream) cudaStreamDestroy(d.stream);
   }
   {
@@ -2313,12 +2426,19 @@ phx_status phx_block_series_direct(phx_op op, int32_t r, const double* t, const 
 
 phx_status phx_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* info6,
                          int32_t* desc, uint8_t* slot, int32_t* sgl) {
+  return phx_tile_plan_part(n, row_ptr, col_idx, 0, n, info6, desc, slot, sgl);
+}
+
+phx_status phx_tile_plan_part(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t row0,
+                              int64_t nrows, int32_t* info6, int32_t* desc, uint8_t* slot,
+                              int32_t* sgl) {
   return guarded([&] {
-    if (!info6 || !row_ptr || n < 1) throw_phx(PHX_EINVAL, "phx_tile_plan: bad arguments");
+    if (!info6 || !row_ptr || n < 1 || row0 < 0 || nrows < 1 || row0 + nrows > n)
+      throw_phx(PHX_EINVAL, "phx_tile_plan: bad arguments");
     phx::TilePlan plan;
-    const bool ok = phx::build_tile_plan(n, row_ptr, col_idx, &plan);
+    const bool ok = phx::build_tile_plan(nrows, row_ptr + row0, col_idx, &plan, row0, n);
     info6[0] = ok ? 1 : 0;
-    info6[1] = int32_t((n + phx::kPlanT - 1) / phx::kPlanT);
+    info6[1] = int32_t((nrows + phx::kPlanT - 1) / phx::kPlanT);
     info6[2] = ok ? plan.rows : 0;
     info6[3] = ok ? plan.sgl_cap : 0;
     info6[4] = ok ? plan.emax : 0;

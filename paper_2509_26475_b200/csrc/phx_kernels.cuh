@@ -43,6 +43,10 @@ struct PartTab {
   unsigned* arrive;           // [3]
   MailBox* mbox;              // [2 step parities][nparts]
   int32_t row0, nrows;
+  // the part's tile plan (bulk kernel; phx_plan.cpp with row0 / ntot)
+  const int32_t* plan_desc;
+  const uint8_t* plan_slot;
+  const int32_t* plan_sgl;
 };
 
 // Per-call parameters of the persistent phimv_block kernel.
@@ -157,7 +161,10 @@ constexpr int kPlanGroups = 4;
 constexpr int kPlanDesc = 16;
 constexpr int kPlanMaxSingles = 32;
 constexpr int kPlanMaxEntries = 1024;  // per tile (stage capacity)
-constexpr int kBulkConsumers = 8;      // consumer warps per CTA (+ 1 producer warp)
+#ifndef PHX_BULK_CONS
+#define PHX_BULK_CONS 8
+#endif
+constexpr int kBulkConsumers = PHX_BULK_CONS;  // consumer warps per CTA (+ 1 producer warp)
 constexpr int kBulkThreads = (kBulkConsumers + 1) * 32;
 constexpr int kBulkMaxStages = 8;
 
@@ -170,7 +177,13 @@ struct TilePlan {
   bool blocked = false;  // y-blocked lattice order (else natural)
 };
 // false (plan.ok == false) when some tile needs more than the stage holds
-bool build_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, TilePlan* plan);
+// A part's plan (row-partitioned operators): its n rows start at global row
+// row0 of an operator of ntot rows; row_ptr points at the part's first entry
+// of the whole row_ptr, col_idx is the whole column array (global columns).
+// Tiles and entry slots are part-local; window, group and single source rows
+// are global (the kernel resolves them to the owning part's buffer).
+bool build_tile_plan(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, TilePlan* plan,
+                     int64_t row0 = 0, int64_t ntot = -1);
 
 // byte layout of one stage of the bulk ring (host and device agree)
 struct BulkStage {
@@ -198,9 +211,9 @@ __host__ __device__ inline BulkStage bulk_stage(int32_t rows, int32_t emax, int3
   return L;
 }
 
-cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st, bool part = false);
 // co-resident CTAs per SM of k_phimv_bulk at the given dynamic shared memory
-cudaError_t bulk_occupancy(size_t smem, int* per_sm);
+cudaError_t bulk_occupancy(size_t smem, int* per_sm, bool part = false);
 
 // launch wrappers (phx_kernels.cu)
 cudaError_t launch_phimv_block(const BlockArgs& a, int grid, int block, cudaStream_t st);

@@ -38,16 +38,21 @@ struct TileInfo {
 
 // groups and singles of one tile (deterministic: groups by count desc, then
 // offset asc; singles sorted by column)
-void analyse_tile(int64_t n, const int64_t* rp, const int32_t* ci, int64_t t, TileInfo* info,
-                  std::vector<int32_t>* singles, std::vector<int64_t>& scratch) {
+// Rows are the part's (n of them, the first one global row row0; rp points at
+// the part's first row_ptr entry, ci is the whole column array); columns and
+// the window are global rows of an operator of ntot rows.
+void analyse_tile(int64_t n, const int64_t* rp, const int32_t* ci, int64_t row0, int64_t ntot,
+                  int64_t t, TileInfo* info, std::vector<int32_t>* singles,
+                  std::vector<int64_t>& scratch) {
   const int64_t base = t * kPlanT, rows = std::min<int64_t>(kPlanT, n - base);
-  const int64_t wlo = std::max<int64_t>(base - 1, 0), whi = std::min<int64_t>(base + rows + 1, n);
+  const int64_t gb = row0 + base;
+  const int64_t wlo = std::max<int64_t>(gb - 1, 0), whi = std::min<int64_t>(gb + rows + 1, ntot);
   scratch.clear();
   for (int64_t rr = 0; rr < rows; ++rr)
     for (int64_t e = rp[base + rr]; e < rp[base + rr + 1]; ++e) {
       const int64_t col = ci[e];
       if (col >= wlo && col < whi) continue;
-      scratch.push_back(col - (base + rr));
+      scratch.push_back(col - (gb + rr));
     }
   info->ne = int32_t(rp[base + rows] - rp[base]);
   std::sort(scratch.begin(), scratch.end());
@@ -71,7 +76,7 @@ void analyse_tile(int64_t n, const int64_t* rp, const int32_t* ci, int64_t t, Ti
     for (int64_t e = rp[base + rr]; e < rp[base + rr + 1]; ++e) {
       const int64_t col = ci[e];
       if (col >= wlo && col < whi) continue;
-      const int64_t off = col - (base + rr);
+      const int64_t off = col - (gb + rr);
       bool grouped = false;
       for (int g = 0; g < info->ng; ++g) grouped = grouped || info->goff[g] == off;
       if (!grouped) sg.push_back(int32_t(col));
@@ -112,7 +117,7 @@ void parallel_tiles(int64_t ntiles, F&& f) {
 // (C3: 3.9 MB instead of 31 MB of D per reuse window).  Other operators keep
 // the natural order.
 constexpr int64_t kYBlock = 32;
-void tile_order(int64_t n, const std::vector<TileInfo>& info, TilePlan* plan) {
+void tile_order(int64_t n, int64_t row0, const std::vector<TileInfo>& info, TilePlan* plan) {
   const int64_t T = kPlanT, ntiles = int64_t(info.size());
   std::vector<int32_t> order(static_cast<size_t>(ntiles));
   for (int64_t t = 0; t < ntiles; ++t) order[size_t(t)] = int32_t(t);
@@ -137,7 +142,7 @@ void tile_order(int64_t n, const std::vector<TileInfo>& info, TilePlan* plan) {
   const char* env = std::getenv("PHX_PLAN_BLOCKED");  // developer knob (read at creation)
   if (strides.size() >= 2 && !(env && env[0] == '0')) {
     const int64_t B2 = strides.back(), B1 = strides[strides.size() - 2];
-    if (B1 % T == 0 && B2 % B1 == 0 && n % B2 == 0 && B2 / B1 >= 2 * kYBlock) {
+    if (B1 % T == 0 && B2 % B1 == 0 && n % B2 == 0 && row0 % B2 == 0 && B2 / B1 >= 2 * kYBlock) {
       const int64_t ny = B2 / B1, nz = n / B2, xt = B1 / T;
       size_t q = 0;
       for (int64_t yb = 0; yb < ny; yb += kYBlock)
@@ -159,14 +164,16 @@ void tile_order(int64_t n, const std::vector<TileInfo>& info, TilePlan* plan) {
 
 }  // namespace
 
-bool build_tile_plan(int64_t n, const int64_t* rp, const int32_t* ci, TilePlan* plan) {
+bool build_tile_plan(int64_t n, const int64_t* rp, const int32_t* ci, TilePlan* plan, int64_t row0,
+                     int64_t ntot) {
   plan->ok = false;
+  if (ntot < 0) ntot = n;
   const int64_t ntiles = (n + kPlanT - 1) / kPlanT;
   std::vector<TileInfo> info(static_cast<size_t>(ntiles));
   std::atomic<bool> ok{true};
   parallel_tiles(ntiles, [&](int64_t t, std::vector<int64_t>& scratch) {
     if (!ok.load(std::memory_order_relaxed)) return;
-    analyse_tile(n, rp, ci, t, &info[size_t(t)], nullptr, scratch);
+    analyse_tile(n, rp, ci, row0, ntot, t, &info[size_t(t)], nullptr, scratch);
     if (!info[size_t(t)].ok) ok = false;
   });
   if (!ok) return false;
@@ -185,25 +192,26 @@ bool build_tile_plan(int64_t n, const int64_t* rp, const int32_t* ci, TilePlan* 
   plan->sgl_cap = smax;
   plan->emax = (emax + 1) / 2 * 2;
   if (plan->rows > 256) return false;  // one-byte slots
-  const int64_t nnz = rp[n];
+  const int64_t e0 = rp[0], nnz = rp[n] - e0;  // the part's entries (slots are part-local)
   plan->desc.assign(size_t(ntiles) * kPlanDesc, 0);
   plan->slot.assign(size_t(nnz) + 16, 0);
   plan->sgl.assign(size_t(sgl_lo[size_t(ntiles)]) + 1, 0);
   parallel_tiles(ntiles, [&](int64_t t, std::vector<int64_t>& scratch) {
     TileInfo ti;
     std::vector<int32_t> sg;
-    analyse_tile(n, rp, ci, t, &ti, &sg, scratch);
+    analyse_tile(n, rp, ci, row0, ntot, t, &ti, &sg, scratch);
     const int64_t base = t * T, rows = std::min<int64_t>(T, n - base);
-    const int64_t wlo = std::max<int64_t>(base - 1, 0), whi = std::min<int64_t>(base + rows + 1, n);
+    const int64_t gb = row0 + base;
+    const int64_t wlo = std::max<int64_t>(gb - 1, 0), whi = std::min<int64_t>(gb + rows + 1, ntot);
     int32_t* d = plan->desc.data() + size_t(t) * kPlanDesc;
     d[0] = ti.ng;
     d[1] = ti.nsgl;
     d[2] = int32_t(sgl_lo[size_t(t)]);
-    d[3] = int32_t(rp[base]);
-    d[4] = int32_t(rp[base + rows]);
+    d[3] = int32_t(rp[base] - e0);
+    d[4] = int32_t(rp[base + rows] - e0);
     for (int g = 0; g < ti.ng; ++g) {
-      const int64_t o0 = base + ti.goff[g];
-      const int64_t s0 = std::max<int64_t>(0, o0), s1 = std::min<int64_t>(n, o0 + rows);
+      const int64_t o0 = gb + ti.goff[g];
+      const int64_t s0 = std::max<int64_t>(0, o0), s1 = std::min<int64_t>(ntot, o0 + rows);
       const int64_t dst = gbase + int64_t(g) * T + (s0 - o0);
       d[8 + g] = int32_t(s0);
       d[12 + g] = int32_t((s1 - s0) | (dst << 16));
@@ -216,7 +224,7 @@ bool build_tile_plan(int64_t n, const int64_t* rp, const int32_t* ci, TilePlan* 
         if (col >= wlo && col < whi) {
           sl = col - wlo;
         } else {
-          const int64_t off = col - (base + rr);
+          const int64_t off = col - (gb + rr);
           int g = -1;
           for (int q = 0; q < ti.ng; ++q)
             if (ti.goff[q] == off) g = q;
@@ -225,10 +233,10 @@ bool build_tile_plan(int64_t n, const int64_t* rp, const int32_t* ci, TilePlan* 
           else
             sl = (T + 2) + (std::lower_bound(sg.begin(), sg.end(), int32_t(col)) - sg.begin());
         }
-        plan->slot[size_t(e)] = uint8_t(sl);
+        plan->slot[size_t(e - e0)] = uint8_t(sl);
       }
   });
-  tile_order(n, info, plan);
+  tile_order(n, row0, info, plan);
   plan->ok = true;
   return true;
 }

@@ -55,8 +55,8 @@ if __name__ == "__main__":
     rep = sys.argv[1]
     r = raw(rep)
     d = {k: r[k][0] + " " + r[k][1] for k in KEYS if k in r}
-    rb = float(r["dram__bytes_read.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1}[r["dram__bytes_read.sum"][1]]
-    wb = float(r["dram__bytes_write.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1}[r["dram__bytes_write.sum"][1]]
+    rb = float(r["dram__bytes_read.sum"][0]) * {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[r["dram__bytes_read.sum"][1]]
+    wb = float(r["dram__bytes_write.sum"][0]) * {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[r["dram__bytes_write.sum"][1]]
     d["dram_bytes_per_launch"] = rb + wb
     d["sass_mix_pct_instr_pct_stall"] = sass_mix(rep)
     print(json.dumps(d, indent=1))

@@ -98,3 +98,56 @@ def test_partitioned_selection_is_the_whole_operators(cfg, size, parts):
     assert np.array_equal(part.apply(X), whole.apply(X))
     req = p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss_p)
     assert np.array_equal(p.phimv_block(part, req).W, p.phimv_block(whole, req).W)
+
+
+@pytest.mark.parametrize("cfg,size,parts", [(1, 0, 2), (2, 64, 3), (3, 12, 3), (3, 20, 8),
+                                            (5, 2000, 2), (5, 3000, 7), (2, 160, 16)])
+def test_partitioned_bulk_bitwise(cfg, size, parts, monkeypatch):
+    """The bulk-copy kernel's partitioned instantiation (forced with
+    PHX_BULK=1): each part stages its tiles' gathers -- rows of other parts
+    included, cut at the part boundaries and copied from the owner's buffers
+    -- and the parts combine their maxima through the mailboxes.  Bitwise the
+    unpartitioned evaluation, term by term against the oracle's trace."""
+    monkeypatch.setenv("PHX_BULK", "1")
+    p = P()
+    wl = p.workload(cfg, size)
+    whole = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    ss = p.select_parameters(whole, 61, wl.tol)
+    ref = p.phimv_block(whole, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    part = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=parts)
+    res = p.phimv_block(part, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    assert p.last_eval_mode() == 1 and p.last_eval_variant()["dynamic_tail"] == 2
+    assert res.stats.series_len_S == ref.stats.series_len_S
+    assert res.stats.series_lens_F == ref.stats.series_lens_F
+    assert res.stats.matvecs == ref.stats.matvecs
+    assert np.array_equal(res.W, ref.W)
+    p.set_trace(3 * 100000)
+    p.phimv_block(part, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    tr = p.get_trace(3 * 100000)
+    p.set_trace(0)
+    oop = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    _, _, otr = O.phimv_block(oop, wl.t, wl.alpha, wl.V, wl.tol, O.ScalingShift(*ss.astuple()),
+                              trace=True)
+    assert np.array_equal(tr, otr)
+
+
+@pytest.mark.parametrize("parts", [2, 8])
+def test_partitioned_full_c3_bulk_bitwise(golden_dir, parts):
+    """Full-size C3 (n = 2^24) row-partitioned into 2 / 8 parts -- the
+    multi-GPU configuration of SURVEY.md §8e in its single-GPU emulation --
+    runs the partitioned bulk kernel and reproduces the oracle's committed
+    SHA-256 of W (tests/golden/full_cfg3.json)."""
+    import hashlib
+    import json
+    import os
+    p = P()
+    with open(os.path.join(golden_dir, "full_cfg3.json")) as f:
+        meta = json.load(f)
+    wl = p.workload(3, 0)
+    part = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=parts)
+    ss = p.ScalingShift(*meta["params"])
+    res = p.phimv_block(part, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    assert p.last_eval_variant()["dynamic_tail"] == 2
+    assert res.stats.series_len_S == meta["series_len_S"]
+    h = hashlib.sha256(np.asfortranarray(res.W).tobytes(order="F")).hexdigest()
+    assert h == meta["W_sha256"]

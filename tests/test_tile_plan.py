@@ -10,10 +10,15 @@ import paper_2509_26475_b200 as P
 T = P.tile_plan(1, [0, 1], [0])[0]["T"]  # rows per tile (kPlanT)
 
 
-def check_plan(n, rp, ci):
-    info, desc, slot, sgl = P.tile_plan(n, rp, ci)
+def check_plan(n, rp, ci, row0=0, nrows=None):
+    """Checks the plan of the whole operator, or of the row part [row0,
+    row0 + nrows) as a partitioned operator builds it (tiles and slots
+    part-local, window / group / single source rows global)."""
+    nrows = n - row0 if nrows is None else nrows
+    info, desc, slot, sgl = P.tile_plan(n, rp, ci, row0, nrows)
     assert info["ok"] == 1
-    assert info["tiles"] == (n + T - 1) // T
+    assert info["tiles"] == (nrows + T - 1) // T
+    e0 = int(rp[row0])
     scap = info["singles_cap"]
     gbase = T + 2 + scap
     assert info["rows"] <= 256 and (info["rows"] - gbase) % T == 0
@@ -23,10 +28,11 @@ def check_plan(n, rp, ci):
     for d in desc:
         t = int(d[5])
         base = t * T
-        rows = min(T, n - base)
-        wlo, whi = max(base - 1, 0), min(base + rows + 1, n)
+        rows = min(T, nrows - base)
+        gb = row0 + base
+        wlo, whi = max(gb - 1, 0), min(gb + rows + 1, n)
         ng, nsgl, s0, e_lo, e_hi = (int(x) for x in d[:5])
-        assert (e_lo, e_hi) == (rp[base], rp[base + rows])
+        assert (e_lo, e_hi) == (rp[gb] - e0, rp[gb + rows] - e0)
         assert ng <= ngmax and nsgl <= scap
         groups = []
         for g in range(ng):
@@ -47,7 +53,7 @@ def check_plan(n, rp, ci):
                 hit = [src0 + (s - dst) for (src0, cnt, dst) in groups if dst <= s < dst + cnt]
                 assert len(hit) == 1
                 src = hit[0]
-            assert src == ci[e], (t, e, s)
+            assert src == ci[e0 + e], (t, e, s)
     return info
 
 
@@ -130,3 +136,52 @@ def test_plan_rejects_what_the_stage_cannot_hold():
     ci2 = np.tile(np.arange(1300, dtype=np.int32), n2)
     info2, *_ = P.tile_plan(n2, rp2, ci2)
     assert info2["ok"] == 0
+
+
+def part_bounds(n, parts):
+    """phx_op_create_csr_partitioned's contiguous row parts."""
+    return [q * n // parts for q in range(parts + 1)]
+
+
+@pytest.mark.parametrize("cfg,size,parts", [(3, 20, 2), (3, 20, 3), (3, 24, 8), (2, 96, 5),
+                                            (5, 5000, 7), (1, 300, 4)])
+def test_partition_plans(cfg, size, parts):
+    """Every part's plan of a row-partitioned operator resolves each of the
+    part's entries to its global column -- including the halo rows other
+    parts own (window edges, the +-plane groups across a part boundary)."""
+    wl = P.workload(cfg, size, with_V=False)
+    b = part_bounds(wl.n, parts)
+    halo = 0
+    for q in range(parts):
+        info = check_plan(wl.n, wl.rp, wl.ci, b[q], b[q + 1] - b[q])
+        ents = wl.ci[wl.rp[b[q]]:wl.rp[b[q + 1]]]
+        halo += int(((ents < b[q]) | (ents >= b[q + 1])).sum())
+        assert info["rows"] <= 256
+    if parts > 1 and cfg != 1:
+        assert halo > 0  # some entries gather another part's rows
+
+
+def test_partition_plans_random_with_singles():
+    rng = np.random.default_rng(5)
+    n = 2500
+    rp, ci = [0], []
+    for i in range(n):
+        cols = {i, max(0, i - 1), min(n - 1, i + 1)}
+        if rng.random() < 0.2:
+            cols.add(int(rng.integers(0, n)))
+        ci += sorted(cols)
+        rp.append(len(ci))
+    rp, ci = np.array(rp), np.array(ci, dtype=np.int32)
+    b = part_bounds(n, 3)
+    for q in range(3):
+        info = check_plan(n, rp, ci, b[q], b[q + 1] - b[q])
+        assert info["singles"] > 0
+
+
+def test_whole_plan_is_the_one_part_plan():
+    wl = P.workload(3, 20, with_V=False)
+    a = P.tile_plan(wl.n, wl.rp, wl.ci)
+    b = P.tile_plan(wl.n, wl.rp, wl.ci, 0, wl.n)
+    assert a[0] == b[0]
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y)
