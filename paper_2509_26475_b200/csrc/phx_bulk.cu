@@ -127,7 +127,7 @@ __device__ __forceinline__ void publish_b(unsigned long long a, unsigned long lo
 }
 
 // PART: a row-partitioned operator.  The launch runs parts
-// plo .. plo+pcount-1 with the CTAs split evenly; a CTA binds its part's
+// plo .. plo+pcount-1 with the CTAs split evenly (interleaved); a CTA binds its part's
 // row-local buffers, CSR and tile plan (rows are part-local from there on).
 // The plan's window / group / single source rows are GLOBAL rows: the
 // producer cuts every staged range at the part boundaries and copies each
@@ -140,49 +140,46 @@ __device__ __forceinline__ void publish_b(unsigned long long a, unsigned long lo
 #else
 #define PHX_BULK_BOUNDS __launch_bounds__(kBulkThreads, kBulkConsumers > 8 ? 1 : 2)
 #endif
+// the kernel's parameter: one BlockArgs, or (PART) every part's BlockArgs
+// (n = the part's rows, its buffers, CSR and plan) in the parameter space --
+// indexed by the CTA's part, so the per-part arguments stay in the constant
+// bank like the unpartitioned kernel's instead of a shared-memory copy
 template <bool PART>
-__global__ void PHX_BULK_BOUNDS k_phimv_bulk(BlockArgs ga) {
+struct BulkParam {
+  using type = BlockArgs;
+};
+template <>
+struct BulkParam<true> {
+  using type = BulkPartArgs;
+};
+__device__ __forceinline__ const BlockArgs& part_args(const BlockArgs& g, int) { return g; }
+__device__ __forceinline__ const BlockArgs& part_args(const BulkPartArgs& g, int q) { return g.pa[q]; }
+
+template <bool PART>
+__global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename BulkParam<PART>::type gp) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ unsigned long long bar_full[kBulkMaxStages], bar_empty[kBulkMaxStages];
   __shared__ unsigned long long red[2][kBW];
   __shared__ __align__(16) int pdesc[2][kPB][kPlanDesc];  // producer: descriptor batches
-  __shared__ __align__(16) unsigned char s_pa_raw[PART ? sizeof(BlockArgs) : 16];
   __shared__ const double* gtab[5][PART ? kMaxParts : 1];  // [D0, D1, S, F0, F1][part]
   __shared__ int sbnd[PART ? kMaxParts + 1 : 1];           // part row boundaries (global)
   __shared__ double gmax[2];
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const BlockArgs& ga = part_args(gp, 0);  // the fields common to all parts
   int my = 0, cta = int(blockIdx.x), ncta = int(gridDim.x);
   const PartTab* T = nullptr;
-  const int Ng = ga.n;  // global rows
+  int Ng = ga.n;  // global rows
   if (PART) {
+    // parts interleaved over the CTAs (CTA b works for part plo + b mod
+    // pcount): on one device every part's CTAs spread over all SMs alike
     const int per = int(gridDim.x) / ga.pcount;
-    my = ga.plo + int(blockIdx.x) / per;
-    cta = int(blockIdx.x) % per;
+    my = ga.plo + int(blockIdx.x) % ga.pcount;
+    cta = int(blockIdx.x) / ga.pcount;
     ncta = per;
     T = ga.ptab + my;
-    if (threadIdx.x == 0) {
-      BlockArgs pa = ga;
-      pa.n = T->nrows;
-      pa.rp = T->rp;
-      pa.ci = T->ci;
-      pa.av = T->av;
-      pa.V = T->V;
-      pa.Vw = T->Vw;
-      pa.D0 = T->D0;
-      pa.D1 = T->D1;
-      pa.S = T->S;
-      pa.F0 = T->F0;
-      pa.F1 = T->F1;
-      pa.E = T->E;
-      pa.W = T->W;
-      pa.slots = T->slots;
-      pa.plan_desc = T->plan_desc;
-      pa.plan_slot = T->plan_slot;
-      pa.plan_sgl = T->plan_sgl;
-      *reinterpret_cast<BlockArgs*>(s_pa_raw) = pa;
-    }
+    Ng = ga.ptab[ga.nparts - 1].row0 + ga.ptab[ga.nparts - 1].nrows;
     for (int q = threadIdx.x; q < ga.nparts; q += blockDim.x) {
       const PartTab& U = ga.ptab[q];
       gtab[0][q] = U.D0;
@@ -195,7 +192,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(BlockArgs ga) {
     if (threadIdx.x == 0) sbnd[ga.nparts] = Ng;
     __syncthreads();
   }
-  const BlockArgs& a = PART ? *reinterpret_cast<const BlockArgs*>(s_pa_raw) : ga;
+  const BlockArgs& a = part_args(gp, my);
   const int row0 = PART ? T->row0 : 0;
   const int NS = a.bulk_ns, SB = a.bulk_stage_bytes;
   const bool sleepw = (a.bulk_flags & 2) != 0;
@@ -286,6 +283,11 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(BlockArgs ga) {
         }
         gmax[0] = from_bits(A);
         gmax[1] = from_bits(Bv);
+        if (master && a.tstamp != nullptr && step < a.tstamp_cap) {
+          unsigned long long ns;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+          a.tstamp[step] = ns;
+        }
         // the next step's bulk copies read other parts' rows written before
         // their arrival: make them visible to this CTA's async proxy
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -336,8 +338,8 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(BlockArgs ga) {
   auto copy_rows = [&](unsigned char* dst, const double* X, int xsel, int width, int g0, int cnt,
                        unsigned long long* bf, unsigned long long pol) {
     const unsigned rb = unsigned(width) * 8u;
-    if (!PART) {
-      bulk_g2s(dst, X + size_t(g0) * width, unsigned(cnt) * rb, bf, pol);
+    if (!PART || (g0 >= row0 && g0 + cnt <= row0 + n)) {  // the part's own rows
+      bulk_g2s(dst, X + size_t(g0 - row0) * width, unsigned(cnt) * rb, bf, pol);
       return;
     }
     while (cnt > 0) {
@@ -366,6 +368,13 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(BlockArgs ga) {
     unsigned long long* ctr = a.slots + 4 * (step % 3) + 2;
     unsigned long long mx = 0;
     if (warp == kProd) {
+      // the part's CSR / plan pointers in registers (PART: `a` lives in shared
+      // memory, and the producer's per-tile chain should not wait on it)
+      const int* const c_rp = a.rp;
+      const uint8_t* const c_slot = a.plan_slot;
+      const double* const c_av = a.av;
+      const int* const c_desc = a.plan_desc;
+      const int* const c_sgl = a.plan_sgl;
       // Batches of kPB tile positions from the step's counter.  The atomic
       // for a batch is issued one batch ahead; its descriptors are copied
       // (cp.async, 16 lanes x 16 B) into pdesc[nxt] while the current batch
@@ -381,12 +390,12 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(BlockArgs ga) {
         if (M == 1) {
           if (lane < 4 * kPB && q < nblk)
             cp_async16(&pdesc[buf][lane >> 2][4 * (lane & 3)],
-                       a.plan_desc + size_t(q) * kPlanDesc + 4 * (lane & 3));
+                       c_desc + size_t(q) * kPlanDesc + 4 * (lane & 3));
         } else if (lane < 4 * kPB && (lane & 3) < 2 && q < npos) {
           // merged: e_lo from the first sub-tile's descriptor, e_hi from the last's
           const int sub = (lane & 1) ? min(q * M + M - 1, nblk - 1) : q * M;
           cp_async16(&pdesc[buf][lane >> 2][4 * (lane & 1)],
-                     a.plan_desc + size_t(sub) * kPlanDesc + 4 * (lane & 1));
+                     c_desc + size_t(sub) * kPlanDesc + 4 * (lane & 1));
         }
         cp_commit();
       };
@@ -439,9 +448,9 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(BlockArgs ga) {
                 PHX_CHECK((d[12 + g] >> 16) + (d[12 + g] & 0xffff) <= a.plan_rows &&
                           d[8 + g] >= 0 && d[8 + g] + (d[12 + g] & 0xffff) <= Ng);
               mbar_arrive_tx(bf, unsigned(rn * 4 + cn + an * 8) + nrow * rb);
-              bulk_g2s(st + L.rp, a.rp + base, unsigned(rn) * 4u, bf, pfirst);
-              if (cn) bulk_g2s(st + L.sl, a.plan_slot + c0, unsigned(cn), bf, pfirst);
-              if (an) bulk_g2s(st + L.av, a.av + a0, unsigned(an) * 8u, bf, pfirst);
+              bulk_g2s(st + L.rp, c_rp + base, unsigned(rn) * 4u, bf, pfirst);
+              if (cn) bulk_g2s(st + L.sl, c_slot + c0, unsigned(cn), bf, pfirst);
+              if (an) bulk_g2s(st + L.av, c_av + a0, unsigned(an) * 8u, bf, pfirst);
               copy_rows(st + L.dr, X, xsel, width, wlo, whi - wlo, bf, plast);
               for (int g = 0; g < ng; ++g) {
                 const int cnt = d[12 + g] & 0xffff, dst = d[12 + g] >> 16;
@@ -452,7 +461,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(BlockArgs ga) {
             }
           }
           if (t >= 0 && lane < nsgl) {  // single rows, one lane each
-            const int col = __ldg(a.plan_sgl + d[2] + lane);
+            const int col = __ldg(c_sgl + d[2] + lane);
             copy_rows(st + L.dr + (kPlanT + 2 + lane) * width * 8, X, xsel, width, col, 1, bf, plast);
           }
           __syncwarp();
@@ -1209,12 +1218,22 @@ cudaError_t bulk_occupancy(size_t smem, int* per_sm, bool part) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, f, kBulkThreads, smem);
 }
 
-cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st, bool part) {
+cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st) {
   BlockArgs copy = a;
   void* args[] = {&copy};
   const size_t smem = size_t(a.bulk_ns) * size_t(a.bulk_stage_bytes);
-  const void* f = part ? reinterpret_cast<const void*>(k_phimv_bulk<true>)
-                       : reinterpret_cast<const void*>(k_phimv_bulk<false>);
+  const void* f = reinterpret_cast<const void*>(k_phimv_bulk<false>);
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  count_launch();
+  return cudaLaunchCooperativeKernel(f, grid, kBulkThreads, args, smem, st);
+}
+
+cudaError_t launch_phimv_bulk_parts(const BulkPartArgs& pa, int grid, cudaStream_t st) {
+  void* args[] = {const_cast<BulkPartArgs*>(&pa)};
+  const BlockArgs& a = pa.pa[pa.pa[0].plo];
+  const size_t smem = size_t(a.bulk_ns) * size_t(a.bulk_stage_bytes);
+  const void* f = reinterpret_cast<const void*>(k_phimv_bulk<true>);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   count_launch();

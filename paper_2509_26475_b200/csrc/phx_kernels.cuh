@@ -211,7 +211,14 @@ __host__ __device__ inline BulkStage bulk_stage(int32_t rows, int32_t emax, int3
   return L;
 }
 
-cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st, bool part = false);
+cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st);
+// every part's arguments (pa[q] for the launch's parts plo .. plo+pcount-1;
+// pa[0] also carries the fields common to all parts: nparts, plo, pcount,
+// ptab) -- the kernel parameter of the partitioned bulk kernel
+struct BulkPartArgs {
+  BlockArgs pa[kMaxParts];
+};
+cudaError_t launch_phimv_bulk_parts(const BulkPartArgs& pa, int grid, cudaStream_t st);
 // co-resident CTAs per SM of k_phimv_bulk at the given dynamic shared memory
 cudaError_t bulk_occupancy(size_t smem, int* per_sm, bool part = false);
 
