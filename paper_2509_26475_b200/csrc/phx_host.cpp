@@ -196,13 +196,6 @@ struct phx_op_s {
   int32_t* d_plan_desc = nullptr;
   uint8_t* d_plan_slot = nullptr;
   int32_t* d_plan_sgl = nullptr;
-  // column-blocked CSR (scattered-gather operators): the entries of column
-  // block b = [b cb_rows, (b+1) cb_rows) of every row, rows in order; per-block
-  // row_ptr arrays (cb_ld apart, absolute offsets into cb_ci / cb_av)
-  int32_t cb_nb = 0, cb_rows = 0, cb_ld = 0;
-  int32_t* d_cb_rp = nullptr;
-  int32_t* d_cb_ci = nullptr;
-  double* d_cb_av = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::mutex mu;  // selection, apply, the integrator and partitioned evaluations
@@ -667,62 +660,6 @@ void upload_plan(phx_op op, const int64_t* row_ptr, const int32_t* col_idx) {
   op->plan_emax = plan.emax;
   op->plan_merge = plan.rows == phx::kPlanT + 2;  // no singles, no groups
   op->plan_ok = true;
-}
-
-// Column blocks for operators whose gathers scatter over the whole block
-// (no tile plan: a tile's sources are not a few contiguous ranges) and whose
-// rows are long enough to matter: each S term's gather then runs as one pass
-// per column block of cb_rows rows, so the gathered source rows of a pass
-// (cb_rows x w doubles) stay in L2 instead of being re-fetched from HBM per
-// entry (C4: 16 random columns per row).  Every row's entries are
-// accumulated in storage order across the passes (the partial sums carry
-// over in a row-major buffer), which requires each row's entries to be in
-// non-decreasing column-block order -- true for column-sorted rows; an
-// operator that violates it keeps the single pass.  PHX_CB_ROWS sets the
-// block size (default 2^20 rows), PHX_CB=0 disables.
-void upload_colblocks(phx_op op, const int64_t* row_ptr, const int32_t* col_idx, const double* vals) {
-  const char* env = std::getenv("PHX_CB");
-  if (env && env[0] == '0') return;
-  const int64_t n = op->n, nnz = op->nnz;
-  const char* er = std::getenv("PHX_CB_ROWS");
-  const int64_t B = er ? std::max<int64_t>(1024, std::atoll(er)) : (int64_t(1) << 20);
-  if (op->plan_ok || n < 2 * B || nnz < 4 * n) return;
-  const int64_t nb = (n + B - 1) / B;
-  if (nb > 64) return;
-  for (int64_t i = 0; i < n; ++i) {  // block order along every row
-    int64_t last = 0;
-    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
-      const int64_t b = col_idx[e] / B;
-      if (b < last) return;
-      last = b;
-    }
-  }
-  const int64_t ld = (n + 1 + 8 * 32 + 16 + 3) / 4 * 4;  // padded like upload_csr's row_ptr
-  std::vector<int32_t> rp(size_t(ld * nb), 0), ci(size_t(std::max<int64_t>(1, nnz)));
-  std::vector<double> av(size_t(nnz) + 2, 0.0);
-  int64_t o = 0;
-  for (int64_t b = 0; b < nb; ++b) {
-    int32_t* r = rp.data() + b * ld;
-    for (int64_t i = 0; i < n; ++i) {
-      r[i] = int32_t(o);
-      for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
-        if (col_idx[e] / B == b) {
-          ci[size_t(o)] = col_idx[e];
-          av[size_t(o)] = vals[e];
-          ++o;
-        }
-    }
-    for (int64_t i = n; i < ld; ++i) r[i] = int32_t(o);
-  }
-  PHX_CUDA(cudaMalloc(&op->d_cb_rp, rp.size() * 4));
-  PHX_CUDA(cudaMalloc(&op->d_cb_ci, ci.size() * 4));
-  PHX_CUDA(cudaMalloc(&op->d_cb_av, av.size() * 8));
-  PHX_CUDA(cudaMemcpy(op->d_cb_rp, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
-  PHX_CUDA(cudaMemcpy(op->d_cb_ci, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice));
-  PHX_CUDA(cudaMemcpy(op->d_cb_av, av.data(), av.size() * 8, cudaMemcpyHostToDevice));
-  op->cb_nb = int32_t(nb);
-  op->cb_rows = int32_t(B);
-  op->cb_ld = int32_t(ld);
 }
 
 // Whether an evaluation runs the bulk-copy kernel, and its ring: PHX_BULK=0
@@ -1690,7 +1627,6 @@ phx_status phx_op_create_csr(int64_t n, const int64_t* row_ptr, const int32_t* c
       op->ws0.ev1 = op->ev1;
       upload_csr(op, row_ptr, col_idx, vals);
       upload_plan(op, row_ptr, col_idx);
-      upload_colblocks(op, row_ptr, col_idx, vals);
     } catch (...) {
       phx_op_destroy(op);
       throw;
@@ -1859,9 +1795,6 @@ phx_status phx_op_destroy(phx_op op) {
     if (op->d_plan_desc) cudaFree(op->d_plan_desc);
     if (op->d_plan_slot) cudaFree(op->d_plan_slot);
     if (op->d_plan_sgl) cudaFree(op->d_plan_sgl);
-    if (op->d_cb_rp) cudaFree(op->d_cb_rp);
-    if (op->d_cb_ci) cudaFree(op->d_cb_ci);
-    if (op->d_cb_av) cudaFree(op->d_cb_av);
     if (op->ev0) cudaEventDestroy(op->ev0);
     if (op->ev1) cudaEventDestroy(op->ev1);
     if (op->stream) cudaStreamDestroy(op->stream);
