@@ -294,14 +294,16 @@ def run_reference(args):
         # steps: S terms 2, 3, ... of sampled evaluations (setup once per
         # sample, not a step), each timed alone; block time = fixed costs +
         # (L_S - 2) x the step's term time
-        per_run = max(1, L_S - 2)
+        # (terms 2 and 3 of a sample are skipped: they touch the sample's
+        # fresh buffers first, which a full evaluation amortises over L_S terms)
+        per_run = max(1, L_S - 3)
         while len(steps) < args.warmup + args.steps:
-            want = min(per_run, args.warmup + args.steps - len(steps)) + 1
+            want = min(per_run, args.warmup + args.steps - len(steps)) + 2
             _, _, tt = O.phimv_block_timed(op, wl.t, wl.alpha, wl.V, wl.tol, ss, want, 0,
                                            term_times=True)
-            steps += [(x, fixed + (L_S - 2) * x) for x in tt[1:want]]
+            steps += [(x, fixed + (L_S - 2) * x) for x in tt[2:want]]
         steps = steps[args.warmup:]
-        how = (f"Each step: one steady S term (terms 2.. of sampled evaluations), timed alone; "
+        how = (f"Each step: one steady S term (terms 4.. of sampled evaluations), timed alone; "
                f"block time = fixed phases of the calibration (setup, first S term, promotion, "
                f"assembly: {fixed:.2f} s) + {L_S - 2} x the step's term time")
     else:
