@@ -206,6 +206,7 @@ struct phx_op_s {
   std::vector<std::unique_ptr<Workspace>> pool;
   // selection workspace
   DevBuf w0, w1, y, chunkmax, inv, partial, gcoef, spx, spy;
+  DevBuf bmax, bpart;  // the power basis's per-step chunk maxima and partial sums
   HostBuf h_small, h_chunk, h_inv, h_part, h_lens, h_flag;
   // fixed-seed start vectors (params.cpp:102-110), cached per operator
   std::vector<double> start1, start2;
@@ -286,31 +287,16 @@ void require_whole(phx_op op, const char* who) {
 // chunk maxima on the device, Eigen's sequential block-scale logic here, the
 // scaled chunk sums of squares on the device, the fold here.
 // ---------------------------------------------------------------------------
-double stable_norm_dev(phx_op op, const double* d_x, int64_t n, bool have_chunkmax) {
-  cudaStream_t st = op->stream;
-  if (n == 1) {
-    double* h = op->h_small.as<double>(1);
-    PHX_CUDA(cudaMemcpyAsync(h, d_x, sizeof(double), cudaMemcpyDeviceToHost, st));
-    PHX_CUDA(cudaStreamSynchronize(st));
-    return std::fabs(h[0]);
-  }
-  const int64_t nch = (n + phx::kChunk - 1) / phx::kChunk;
-  auto* d_max = op->chunkmax.as<unsigned long long>(size_t(nch));
-  if (!have_chunkmax) PHX_CUDA(phx::launch_chunkmax(int32_t(n), d_x, d_max, st));
-  auto* h_max = op->h_chunk.as<unsigned long long>(size_t(nch));
-  PHX_CUDA(cudaMemcpyAsync(h_max, d_max, size_t(nch) * 8, cudaMemcpyDeviceToHost, st));
-  PHX_CUDA(cudaStreamSynchronize(st));
-  double* h_inv = op->h_inv.as<double>(size_t(nch));
-  std::vector<double> ratio(static_cast<size_t>(nch));
-  std::vector<char> rescale(static_cast<size_t>(nch)), add(static_cast<size_t>(nch));
-  double scale = 0.0, inv_scale = 1.0;
+// Eigen's sequential block-scale scan and fold over a vector's chunk maxima
+// and scaled chunk sums of squares (host; the order and branches of
+// Eigen::stableNorm's blocked algorithm)
+double stable_fold(const unsigned long long* h_max, const double* h_part, int64_t nch) {
+  double scale = 0.0, inv_scale = 1.0, ssq = 0.0;
   for (int64_t b = 0; b < nch; ++b) {
     double maxc;
     std::memcpy(&maxc, &h_max[b], 8);
-    rescale[size_t(b)] = 0;
     if (maxc > scale) {
-      rescale[size_t(b)] = 1;
-      ratio[size_t(b)] = scale / maxc;
+      const double ratio = scale / maxc;
       const double tmp = 1.0 / maxc;
       if (tmp > DBL_MAX) {
         inv_scale = DBL_MAX;
@@ -322,40 +308,53 @@ double stable_norm_dev(phx_op op, const double* d_x, int64_t n, bool have_chunkm
         scale = maxc;
         inv_scale = tmp;
       }
+      ssq = ssq * (ratio * ratio);
     } else if (maxc != maxc) {
       scale = maxc;
     }
-    add[size_t(b)] = scale > 0.0;
-    h_inv[b] = inv_scale;
+    if (scale > 0.0) ssq = ssq + h_part[b];
   }
-  auto* d_inv = op->inv.as<double>(size_t(nch));
-  auto* d_part = op->partial.as<double>(size_t(nch));
-  PHX_CUDA(cudaMemcpyAsync(d_inv, h_inv, size_t(nch) * 8, cudaMemcpyHostToDevice, st));
-  PHX_CUDA(phx::launch_chunk_ssq(int32_t(n), d_x, d_inv, d_part, st));
-  double* h_part = op->h_part.as<double>(size_t(nch));
-  PHX_CUDA(cudaMemcpyAsync(h_part, d_part, size_t(nch) * 8, cudaMemcpyDeviceToHost, st));
-  PHX_CUDA(cudaStreamSynchronize(st));
-  double ssq = 0.0;
-  for (int64_t b = 0; b < nch; ++b) {
-    if (rescale[size_t(b)]) {
-      const double rt = ratio[size_t(b)];
-      ssq = ssq * (rt * rt);
-    }
-    if (add[size_t(b)]) ssq = ssq + h_part[b];
-  }
+  (void)inv_scale;
   return scale * std::sqrt(ssq);
 }
 
-bool all_finite_from_chunkmax(phx_op op, int64_t n) {
+// the device half of a stableNorm: per-chunk invScale from the chunk maxima
+// (k_stable_inv: a parallel restatement of the sequential scan) and the
+// scaled chunk sums of squares, written to d_part
+void stable_norm_enqueue(phx_op op, const double* d_x, int64_t n, const unsigned long long* d_max,
+                         double* d_part) {
+  const int64_t nch = (n + phx::kChunk - 1) / phx::kChunk;
+  double* d_inv = op->inv.as<double>(size_t(nch));
+  PHX_CUDA(phx::launch_stable_inv(int32_t(nch), d_max, d_inv, op->stream));
+  PHX_CUDA(phx::launch_chunk_ssq(int32_t(n), d_x, d_inv, d_part, op->stream));
+}
+
+// ---------------------------------------------------------------------------
+// stableNorm (params.cpp call sites :108,117,124,168,201) on a device vector:
+// chunk maxima, invScale and scaled chunk sums on the device, ONE read-back
+// (maxima + partials), the sequential scan and fold here.
+// ---------------------------------------------------------------------------
+double stable_norm_dev(phx_op op, const double* d_x, int64_t n, bool have_chunkmax) {
+  cudaStream_t st = op->stream;
+  if (n == 1) {
+    double* h = op->h_small.as<double>(1);
+    PHX_CUDA(cudaMemcpyAsync(h, d_x, sizeof(double), cudaMemcpyDeviceToHost, st));
+    PHX_CUDA(cudaStreamSynchronize(st));
+    return std::fabs(h[0]);
+  }
   const int64_t nch = (n + phx::kChunk - 1) / phx::kChunk;
   auto* d_max = op->chunkmax.as<unsigned long long>(size_t(nch));
+  if (!have_chunkmax) PHX_CUDA(phx::launch_chunkmax(int32_t(n), d_x, d_max, st));
+  double* d_part = op->partial.as<double>(size_t(nch));
+  stable_norm_enqueue(op, d_x, n, d_max, d_part);
   auto* h_max = op->h_chunk.as<unsigned long long>(size_t(nch));
-  PHX_CUDA(cudaMemcpyAsync(h_max, d_max, size_t(nch) * 8, cudaMemcpyDeviceToHost, op->stream));
-  PHX_CUDA(cudaStreamSynchronize(op->stream));
-  for (int64_t b = 0; b < nch; ++b)
-    if (h_max[b] >= 0x7FF0000000000000ull) return false;
-  return true;
+  double* h_part = op->h_part.as<double>(size_t(nch));
+  PHX_CUDA(cudaMemcpyAsync(h_max, d_max, size_t(nch) * 8, cudaMemcpyDeviceToHost, st));
+  PHX_CUDA(cudaMemcpyAsync(h_part, d_part, size_t(nch) * 8, cudaMemcpyDeviceToHost, st));
+  PHX_CUDA(cudaStreamSynchronize(st));
+  return stable_fold(h_max, h_part, nch);
 }
+
 
 void spmv(phx_op op, const double* x, double* y, int mode, double xi, double div, bool chunkmax) {
   auto* d_max = chunkmax ? op->chunkmax.as<unsigned long long>(size_t((op->n + phx::kChunk - 1) /
@@ -406,27 +405,53 @@ phx_basis_s* build_basis(phx_op op, int m, double delta) {
     auto col = [&](int k) { return b->d_cols + size_t(k) * size_t(n); };
     const std::vector<double>& v1 = start_vector(op, 1);
     PHX_CUDA(cudaMemcpyAsync(col0, v1.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
-    spmv(op, col0, col(1), 0, 0.0, 1.0, true);
-    if (!all_finite_from_chunkmax(op, n))
-      throw_phx(PHX_ENUMERIC, "build_power_basis: A*v is not finite; operator rejected");
-    double first_norm = stable_norm_dev(op, col(1), n, true);
+    // the m raw powers A^k v and their stableNorms' device halves enqueued
+    // back to back (per-step chunk maxima and partial sums), ONE read-back, the
+    // folds here; the host then takes the reference's decisions on the same
+    // norms (params.cpp:99-134).  Powers past the cut r are recomputed below
+    // from the scaled basis (mode 2), as before.
+    const int64_t nch = (n + phx::kChunk - 1) / phx::kChunk;
+    auto* d_maxs = op->bmax.as<unsigned long long>(size_t(nch) * size_t(m));
+    double* d_parts = op->bpart.as<double>(size_t(nch) * size_t(m));
+    std::vector<unsigned long long> h_maxs(size_t(nch) * size_t(m));
+    std::vector<double> h_parts(size_t(nch) * size_t(m));
+    std::vector<double> norms(size_t(m) + 1, 0.0);
+    auto raw_powers = [&](const std::vector<double>& v) {
+      PHX_CUDA(cudaMemcpyAsync(col0, v.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+      for (int k = 1; k <= m; ++k) {
+        unsigned long long* mk = d_maxs + size_t(k - 1) * size_t(nch);
+        PHX_CUDA(phx::launch_spmv(int32_t(n), op->d_rp, op->d_ci, op->d_av, col(k - 1), col(k), 0, 0.0,
+                                  1.0, mk, st));
+        if (n > 1) stable_norm_enqueue(op, col(k), n, mk, d_parts + size_t(k - 1) * size_t(nch));
+      }
+      PHX_CUDA(cudaMemcpyAsync(h_maxs.data(), d_maxs, h_maxs.size() * 8, cudaMemcpyDeviceToHost, st));
+      if (n > 1)
+        PHX_CUDA(cudaMemcpyAsync(h_parts.data(), d_parts, h_parts.size() * 8, cudaMemcpyDeviceToHost, st));
+      PHX_CUDA(cudaStreamSynchronize(st));
+      // A v must be finite (params.cpp:105-107)
+      for (int64_t c = 0; c < nch; ++c)
+        if (h_maxs[size_t(c)] >= 0x7FF0000000000000ull)
+          throw_phx(PHX_ENUMERIC, "build_power_basis: A*v is not finite; operator rejected");
+      for (int k = 1; k <= m; ++k) {
+        const size_t o = size_t(k - 1) * size_t(nch);
+        if (n == 1) {
+          double x;
+          std::memcpy(&x, &h_maxs[o], 8);  // |A^k v| (the chunk maximum of one entry)
+          norms[size_t(k)] = x;
+        } else {
+          norms[size_t(k)] = stable_fold(h_maxs.data() + o, h_parts.data() + o, nch);
+        }
+      }
+    };
+    raw_powers(start_vector(op, 1));
+    double first_norm = norms[1];
     if (first_norm == 0.0) {
-      const std::vector<double>& v2 = start_vector(op, 2);
-      PHX_CUDA(cudaMemcpyAsync(col0, v2.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
-      spmv(op, col0, col(1), 0, 0.0, 1.0, true);
-      if (!all_finite_from_chunkmax(op, n))
-        throw_phx(PHX_ENUMERIC, "build_power_basis: A*v is not finite; operator rejected");
-      first_norm = stable_norm_dev(op, col(1), n, true);
+      raw_powers(start_vector(op, 2));
+      first_norm = norms[1];
     }
     int r = 0;
     for (int k = 1; k <= m; ++k) {
-      double norm_w;
-      if (k > 1) {
-        spmv(op, col(k - 1), col(k), 0, 0.0, 1.0, true);
-        norm_w = stable_norm_dev(op, col(k), n, true);
-      } else {
-        norm_w = first_norm;
-      }
+      const double norm_w = norms[size_t(k)];
       const double L = norm_w > 0.0 ? std::log(norm_w) : -std::numeric_limits<double>::infinity();
       if (!(L + 0.5 * std::log(k + 1.0) + ell_max <= g_max) || L < g_min) break;
       b->logs.push_back(L);
@@ -1785,7 +1810,7 @@ phx_status phx_op_destroy(phx_op op) {
     }
     op->pool.clear();
     for (DevBuf* b : {&op->w0, &op->w1, &op->y, &op->chunkmax, &op->inv, &op->partial, &op->gcoef,
-                      &op->spx, &op->spy})
+                      &op->spx, &op->spy, &op->bmax, &op->bpart})
       b->release();
     for (HostBuf* b : {&op->h_small, &op->h_chunk, &op->h_inv, &op->h_part, &op->h_lens, &op->h_flag})
       b->release();

@@ -336,6 +336,84 @@ cudaError_t launch_scale(int32_t n, double* x, double s, int mode, cudaStream_t 
   return cudaGetLastError();
 }
 
+// stableNorm's per-chunk invScale on the device, in parallel.  Eigen's
+// sequential block-scale update (scale / invScale, with its NaN, overflow and
+// tiny-maximum branches; restated on the host in stable_norm_dev) leaves
+// after chunk b: scale_b = the running maximum of F(x_j) = max(x_j, 1/DBL_MAX)
+// over the chunks j <= b with a positive maximum x_j before the first NaN
+// chunk (0 if none), and invScale_b = G(scale_b): 1 for 0 or inf, else
+// fl(1/scale_b) capped at DBL_MAX; after the first NaN chunk invScale no
+// longer changes.  (Checked against the sequential update on 2e5 random
+// sequences of zeros, subnormals, 1/DBL_MAX, normals, DBL_MAX, inf and NaN.)
+// One CTA: the first NaN chunk by a min-reduction, then an inclusive max-scan
+// of the masked keys (non-negative doubles order as their bit patterns).
+constexpr int kInvBlock = 1024;
+__global__ void __launch_bounds__(kInvBlock)
+    k_stable_inv(int32_t nch, const unsigned long long* __restrict__ chunkmax, double* __restrict__ inv) {
+  __shared__ int s_first;
+  __shared__ unsigned long long s_w[kInvBlock / 32];
+  __shared__ unsigned long long s_carry;
+  const double dmax = 1.7976931348623157e308;
+  const unsigned long long tiny = static_cast<unsigned long long>(__double_as_longlong(1.0 / dmax));
+  const unsigned long long infb = 0x7FF0000000000000ull;
+  if (threadIdx.x == 0) {
+    s_first = nch;
+    s_carry = 0ull;
+  }
+  __syncthreads();
+  int first = nch;
+  for (int b = threadIdx.x; b < nch; b += blockDim.x)
+    if (chunkmax[b] > infb) first = min(first, b);
+  atomicMin(&s_first, first);
+  __syncthreads();
+  first = s_first;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int p0 = 0; p0 < nch; p0 += kInvBlock) {
+    const int b = p0 + int(threadIdx.x);
+    unsigned long long key = 0ull;
+    if (b < nch && b < first) {
+      const unsigned long long x = chunkmax[b];
+      if (x != 0ull) key = x > tiny ? x : tiny;  // F(x) = max(x, 1/DBL_MAX)
+    }
+    for (int o = 1; o < 32; o <<= 1) {  // warp inclusive max-scan
+      const unsigned long long y = __shfl_up_sync(kFull, key, o);
+      if (lane >= o) key = key > y ? key : y;
+    }
+    if (lane == 31) s_w[wid] = key;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long v = s_w[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v = v > y ? v : y;
+      }
+      s_w[lane] = v;
+    }
+    __syncthreads();
+    unsigned long long sc = key;
+    if (wid > 0) sc = sc > s_w[wid - 1] ? sc : s_w[wid - 1];
+    sc = sc > s_carry ? sc : s_carry;
+    if (b < nch) {
+      double g = 1.0;
+      if (sc != 0ull && sc != infb) {
+        const double t = 1.0 / __longlong_as_double(static_cast<long long>(sc));
+        g = t > dmax ? dmax : t;
+      }
+      inv[b] = g;
+    }
+    __syncthreads();
+    if (threadIdx.x == kInvBlock - 1) s_carry = sc;  // the piece's last (inclusive) value
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_stable_inv(int32_t nch, const unsigned long long* chunkmax, double* inv,
+                              cudaStream_t st) {
+  ++g_launches;
+  k_stable_inv<<<1, kInvBlock, 0, st>>>(nch, chunkmax, inv);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spmm_cols(int32_t n, int32_t k, const int32_t* rp, const int32_t* ci,
                              const double* av, const double* X, double* Y, int mode, double xi,
                              cudaStream_t st) {

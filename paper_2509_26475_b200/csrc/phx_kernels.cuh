@@ -270,6 +270,10 @@ cudaError_t launch_chunk_ssq(int32_t n, const double* x, const double* inv, doub
                              cudaStream_t st);
 // x = x * s (mode 0) or x / s (mode 1)
 cudaError_t launch_scale(int32_t n, double* x, double s, int mode, cudaStream_t st);
+// stableNorm's per-chunk invScale from the chunk maxima, on the device (the
+// host then needs one read-back: the maxima and the scaled partial sums)
+cudaError_t launch_stable_inv(int32_t nch, const unsigned long long* chunkmax, double* inv,
+                              cudaStream_t st);
 // host col-major block (device copy, ld n) <-> nothing else needed; apply on
 // k columns: Y = A X (mode 0) or (A - xi I) X (mode 1), column-major, ld n
 cudaError_t launch_spmm_cols(int32_t n, int32_t k, const int32_t* rp, const int32_t* ci,

@@ -470,3 +470,28 @@ def test_c5_production_size_bitwise(golden_dir, monkeypatch, bulk):
         meta["s_effective"], meta["series_len_S"], meta["series_lens_F"], meta["matvecs"])
     assert np.array_equal(res.W[arr["sample_rows"]], arr["sample_W"])
     assert sha(res.W) == meta["W_sha256"]
+
+
+@pytest.mark.parametrize("scales", [(0.0, 1e-310, 1.0, 0.0), (1e-300, 0.0, 1e300, 1e-5),
+                                    (0.0, 0.0, 0.0, 3.0), (5e-324, 2.0, 1e-320, 1e10)])
+def test_selection_stablenorm_branches_bitwise(scales):
+    """select_parameters on diagonal operators whose 4096-row chunks carry very
+    different magnitudes (all-zero chunks, subnormal and huge entries): the
+    stableNorm's per-chunk invScale comes from the device's parallel prefix
+    scan and the fold from the host; ScalingShift bitwise the oracle's."""
+    p = P()
+    rng = np.random.default_rng(11)
+    n = 4096 * len(scales)
+    d = np.concatenate([s * (1.0 + rng.random(4096)) for s in scales]) * -1.0
+    rp = np.arange(n + 1, dtype=np.int64)
+    ci = np.arange(n, dtype=np.int32)
+    op = p.CsrOperator(n, rp, ci, d)
+    oop = O.csr_from_arrays(n, rp, ci, d)
+    for tol in (2.0 ** -53, 1e-8):
+        try:
+            ss = p.select_parameters(op, 61, tol).astuple()
+        except Exception as e:  # the same rejection as the oracle's
+            with pytest.raises(type(e)):
+                O.select_parameters(oop, 61, tol)
+            continue
+        assert ss == O.select_parameters(oop, 61, tol).astuple()
