@@ -155,7 +155,10 @@ struct BulkParam<true> {
 __device__ __forceinline__ const BlockArgs& part_args(const BlockArgs& g, int) { return g; }
 __device__ __forceinline__ const BlockArgs& part_args(const BulkPartArgs& g, int q) { return g.pa[q]; }
 
-template <bool PART>
+// SW: the launch has recovery sweeps (s_eff > 1).  Launches without (C2, C3,
+// C4: s_eff = 1) run an instantiation that compiles no recovery, sweep-end or
+// F-promotion code, so the S-term loop gets the registers to itself.
+template <bool PART, bool SW = true>
 __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename BulkParam<PART>::type gp) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring[];
@@ -945,7 +948,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
   // F_L = fl(fl(A S_L * t_i) + v0) (unshifted A), F_R = S block p
   double* Fc = a.F0;
   double* Fn = a.F1;
-  const bool sweeps = a.s_eff > 1;
+  const bool sweeps = SW && a.s_eff > 1;
   const unsigned long long mf = bulk_phase(
       GF, fc, w, a.S, 2, nullptr, nullptr,
       // gathers S block-0 columns (left F columns live at the same column
@@ -1005,6 +1008,9 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     finish(kStOk, 0, L_S, 1);
     return;
   }
+  if constexpr (!SW) {
+    return;  // (unreachable: s_eff = 1 launches finish above)
+  } else {
   double fnorm, dummy;
   sync_step(mf, mf, fnorm, dummy);
 
@@ -1206,6 +1212,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     }
   }
   finish(err, err_idx, L_S, 0);
+  }
 }
 
 }  // namespace
@@ -1222,7 +1229,8 @@ cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st) {
   BlockArgs copy = a;
   void* args[] = {&copy};
   const size_t smem = size_t(a.bulk_ns) * size_t(a.bulk_stage_bytes);
-  const void* f = reinterpret_cast<const void*>(k_phimv_bulk<false>);
+  const void* f = a.s_eff > 1 ? reinterpret_cast<const void*>(k_phimv_bulk<false, true>)
+                              : reinterpret_cast<const void*>(k_phimv_bulk<false, false>);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   count_launch();
@@ -1233,7 +1241,8 @@ cudaError_t launch_phimv_bulk_parts(const BulkPartArgs& pa, int grid, cudaStream
   void* args[] = {const_cast<BulkPartArgs*>(&pa)};
   const BlockArgs& a = pa.pa[pa.pa[0].plo];
   const size_t smem = size_t(a.bulk_ns) * size_t(a.bulk_stage_bytes);
-  const void* f = reinterpret_cast<const void*>(k_phimv_bulk<true>);
+  const void* f = a.s_eff > 1 ? reinterpret_cast<const void*>(k_phimv_bulk<true, true>)
+                              : reinterpret_cast<const void*>(k_phimv_bulk<true, false>);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   count_launch();
