@@ -151,3 +151,26 @@ def test_partitioned_full_c3_bulk_bitwise(golden_dir, parts):
     assert res.stats.series_len_S == meta["series_len_S"]
     h = hashlib.sha256(np.asfortranarray(res.W).tobytes(order="F")).hexdigest()
     assert h == meta["W_sha256"]
+
+
+@pytest.mark.parametrize("cfg,size,bulk", [(3, 20, "1"), (2, 64, "0"), (5, 3000, "1")])
+def test_multi_device_partition_bitwise(cfg, size, bulk, monkeypatch):
+    """Parts on DISTINCT devices (one launch per device, peer gathers / peer
+    bulk copies over NVLink, system-scope mailboxes): bitwise the one-GPU
+    evaluation.  Needs >= 2 GPUs (skipped on a one-GPU box)."""
+    import torch
+    ndev = torch.cuda.device_count()
+    if ndev < 2:
+        pytest.skip("needs >= 2 GPUs")
+    monkeypatch.setenv("PHX_BULK", bulk)
+    p = P()
+    wl = p.workload(cfg, size)
+    whole = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    ss = p.select_parameters(whole, 61, wl.tol)
+    ref = p.phimv_block(whole, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    parts = min(ndev, 4)
+    part = p.CsrOperator(wl.n, wl.rp, wl.ci, wl.av, parts=parts, devices=list(range(parts)))
+    res = p.phimv_block(part, p.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, ss))
+    assert res.stats.series_len_S == ref.stats.series_len_S
+    assert res.stats.series_lens_F == ref.stats.series_lens_F
+    assert np.array_equal(res.W, ref.W)
