@@ -475,6 +475,7 @@ def main():
     peak, peak_src = measured_peak()
     prec = P.RunRecord(rec.s_effective, rec.series_len_S, rec.series_lens_F, rec.matvecs)
     alg = algorithmic_bytes(wl, prec, bulk)
+    ref_flow = algorithmic_bytes(wl, prec, False)  # the reference data flow
     kernel_s = statistics.mean(kms) / 1e3
     achieved = alg / kernel_s / 1e9
     kname = "k_phimv_bulk" if bulk else "k_phimv_block"
@@ -512,6 +513,11 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": kname,
                      "peak_source": peak_src, "alg_bytes_per_launch": alg,
+                     "reference_flow_bytes_per_launch": ref_flow,
+                     "reference_flow_frac": ref_flow / kernel_s / 1e9 / peak,
+                     "bytes_note": "achieved/frac count the bytes the kernel moves (paired S terms "
+                                   "skip stores the reference data flow makes); reference_flow_* "
+                                   "count the Alg. 3 data flow of SURVEY.md 8(d) at the same time",
                      "kernel_ms": kernel_s * 1e3,
                      "timing": "CUDA events around the launch on the operator's stream "
                                "(phx_last_eval_stats), mean over the timed steps"},
