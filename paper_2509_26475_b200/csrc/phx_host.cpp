@@ -6,6 +6,7 @@
 // CPU fallback for n-sized work: without a device every call fails with
 // PHX_ECUDA.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -261,6 +262,15 @@ bool short_batch(phx_op op, int32_t QT, int32_t V, int32_t R) {
   return R == 1 ? op->frac_le5 >= 0.99 : op->frac_le2 >= 0.99;
 }
 
+// NVTX ranges around the host-side phases (header-only NVTX3: a no-op unless
+// a profiler injects itself, e.g. nsys / ncu --nvtx)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -382,6 +392,7 @@ double log_binomial(int m, int j) {  // params.cpp:15-17
 
 // build_power_basis (params.cpp:81-154) with the n-sized work on the device
 phx_basis_s* build_basis(phx_op op, int m, double delta) {
+  NvtxRange nv("phx::build_power_basis");
   require_whole(op, "build_power_basis");
   if (m < 1) throw_phx(PHX_EINVAL, "build_power_basis: m must be >= 1");
   if (!(delta > 0.0 && delta <= 1.0))
@@ -574,6 +585,7 @@ double brent_minimize(const std::function<double(double)>& f, double a, double b
 
 // minimize_shift (params.cpp:172-189)
 std::pair<double, double> minimize_shift_dev(phx_basis_s* b, std::vector<double>* path) {
+  NvtxRange nv("phx::minimize_shift");
   const double n = double(b->op->n);
   const double half_width = std::sqrt(n) * b->s0;
   const auto f = [b](double xi) { return objective_dev(b, xi); };
@@ -618,6 +630,7 @@ double log_shifted_power_dev(phx_basis_s* b, double xi, int m) {
 
 // parameters_for_shift (params.cpp:213-239)
 phx_scaling_shift params_for_shift_dev(phx_basis_s* b, double xi, double tol) {
+  NvtxRange nv("phx::parameters_for_shift");
   if (!(tol > 0.0)) throw_phx(PHX_EINVAL, "parameters_for_shift: tol must be positive");
   const int m = b->m;
   const double f_basis = objective_dev(b, xi);
@@ -825,6 +838,7 @@ struct PendingEval {
 void launch_parts(phx_op op, const EvalIn& in, phx::BlockArgs base, const std::vector<double>& coef,
                   int64_t s_eff, int32_t* h_status, int32_t* h_lens, int64_t nsw,
                   int64_t trace_cap, float* ms_out) {
+  NvtxRange nv("phx::phimv_block partitioned");
   const int P = op->nparts;
   const int32_t r = base.r, p = base.p, ldb = base.ldb, ldf = base.ldf;
   if (in.single || in.h_exp_v0 || in.h_tail)
@@ -1157,6 +1171,7 @@ struct Lease {
 // synchronizes the stream and calls finish_eval(*defer, rec)
 void evaluate(phx_op op, Workspace& ws, const EvalIn& in, phx_run_record* rec,
               PendingEval* defer = nullptr) {
+  NvtxRange nv(in.single ? "phx::phimv" : "phx::phimv_block");
   const char* who = in.single ? "phimv" : "phimv_block";
   const int64_t n = op->n;
   const int32_t r = in.r;
@@ -1937,6 +1952,7 @@ phx_status phx_parameters_for_shift(phx_op op, phx_basis b, double xi, double to
 
 phx_status phx_select_parameters(phx_op op, int32_t m, double tol, double delta,
                                  phx_scaling_shift* out) {
+  NvtxRange nv("phx::select_parameters");
   return guarded([&] {
     if (!op) throw_phx(PHX_ELOGIC, "LinearOperator::apply: operator is empty");
     std::lock_guard<std::mutex> lk(op->mu);
