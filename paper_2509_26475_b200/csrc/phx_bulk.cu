@@ -138,7 +138,10 @@ __device__ __forceinline__ void publish_b(unsigned long long a, unsigned long lo
 #ifdef PHX_BULK_MAXNREG
 #define PHX_BULK_BOUNDS __maxnreg__(PHX_BULK_MAXNREG)
 #else
-#define PHX_BULK_BOUNDS __launch_bounds__(kBulkThreads, kBulkConsumers > 8 ? 1 : 2)
+#ifndef PHX_BULK_MINB
+#define PHX_BULK_MINB (kBulkConsumers > 8 ? 1 : 2)  // CTAs per SM the register budget is sized for
+#endif
+#define PHX_BULK_BOUNDS __launch_bounds__(kBulkThreads, PHX_BULK_MINB)
 #endif
 // the kernel's parameter: one BlockArgs, or (PART) every part's BlockArgs
 // (n = the part's rows, its buffers, CSR and plan) in the parameter space --
@@ -216,6 +219,10 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;  // writes this launch's status
   const int nblk = (n + kPlanT - 1) / kPlanT;  // row blocks = plan tiles
   int kpipe = 0;                               // ring stages used so far (producer == consumers)
+#ifndef PHX_PROBE
+#define PHX_PROBE 0  // developer diagnostics: SM-cycle totals of ring waits and work
+#endif
+  long long pr_pwait = 0, pr_pwork = 0, pr_cwait = 0, pr_cwork = 0, pr_stages = 0;
   int step = 0, tr_len = 0;
 
   if (master && a.tstamp != nullptr && a.tstamp_cap > kCtaStampBase) {  // diagnostics: launch start
@@ -302,7 +309,24 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     }
     ++step;
   };
+  // PHX_PROBE: lane 0 of the producer and of consumer warp 0 add their
+  // totals into tstamp[cap - 8 ..] (SM cycles): producer wait / work,
+  // consumer wait / work, consumer stages
+  auto probe_flush = [&]() {
+    if (PHX_PROBE && a.tstamp != nullptr && lane == 0 && (warp == kProd || warp == 0)) {
+      unsigned long long* o = a.tstamp + (a.tstamp_cap - 8);
+      if (warp == kProd) {
+        atomicAdd(o + 0, (unsigned long long)pr_pwait);
+        atomicAdd(o + 1, (unsigned long long)pr_pwork);
+      } else {
+        atomicAdd(o + 2, (unsigned long long)pr_cwait);
+        atomicAdd(o + 3, (unsigned long long)pr_cwork);
+        atomicAdd(o + 4, (unsigned long long)pr_stages);
+      }
+    }
+  };
   auto finish = [&](int err, int idx, int L_S, int extra_steps) {
+    probe_flush();
     if (lead) {
       a.status[0] = err;
       a.status[1] = idx;
@@ -420,10 +444,12 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
           // descriptors in processing order (merged stages: natural order)
           const int t = posA + j < npos ? (M == 1 ? d[5] : posA + j) : -1;
           const int s = kpipe % NS;
+          const long long pc0 = PHX_PROBE ? clock64() : 0;
           if (sleepw)
             mbar_wait_sleep(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
           else
             mbar_wait(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
+          const long long pc1 = PHX_PROBE ? clock64() : 0;
           unsigned char* st = ring + size_t(s) * size_t(SB);
           unsigned long long* bf = &bar_full[s];
           const int nsgl = (t >= 0 && M == 1) ? d[1] : 0;
@@ -468,6 +494,10 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
             copy_rows(st + L.dr + (kPlanT + 2 + lane) * width * 8, X, xsel, width, col, 1, bf, plast);
           }
           __syncwarp();
+          if (PHX_PROBE) {
+            pr_pwait += pc1 - pc0;
+            pr_pwork += clock64() - pc1;
+          }
           ++kpipe;
           if (t < 0) {
             more = false;
@@ -487,10 +517,12 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     const bool cv = c < ow;
     for (;;) {
       const int s = kpipe % NS;
+      const long long cc0 = PHX_PROBE ? clock64() : 0;
       if (sleepw)
         mbar_wait_sleep(&bar_full[s], (kpipe / NS) & 1);
       else
         mbar_wait(&bar_full[s], (kpipe / NS) & 1);
+      const long long cc1 = PHX_PROBE ? clock64() : 0;
       const unsigned char* st = ring + size_t(s) * size_t(SB);
       const int t = *reinterpret_cast<const int*>(st + L.hdr);
       ++kpipe;
@@ -521,6 +553,11 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
         }
       }
       __syncwarp();
+      if (PHX_PROBE) {
+        pr_cwait += cc1 - cc0;
+        pr_cwork += clock64() - cc1;
+        ++pr_stages;
+      }
       if (lane == 0) mbar_arrive(&bar_empty[s]);
       if (t < 0) break;
     }

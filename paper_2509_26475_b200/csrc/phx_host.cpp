@@ -1490,6 +1490,14 @@ void evaluate(phx_op op, Workspace& ws, const EvalIn& in, phx_run_record* rec,
     for (size_t q = 1; q < ts.size() && ts[q] != 0 && q < 48; ++q)
       std::fprintf(stderr, " %.1f", double(ts[q] - ts[q - 1]) * 1e-3);
     std::fprintf(stderr, "\n");
+    {
+      const unsigned long long* o = ts.data() + ts.size() - 8;
+      if (o[4] != 0)
+        std::fprintf(stderr,
+                     "[phx] probe (SM cycles, summed over CTAs): producer wait %llu work %llu | "
+                     "consumer warp0 wait %llu work %llu | stages %llu\n",
+                     o[0], o[1], o[2], o[3], o[4]);
+    }
     if (const char* path = std::getenv("PHX_CTA_TIMES")) {  // raw CTA arrivals
       if (FILE* f = std::fopen(path, "wb")) {
         const int32_t hdr[2] = {grid, phx::kCtaStampBase};
