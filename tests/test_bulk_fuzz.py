@@ -98,13 +98,13 @@ def _case(seed, parts):
     return var
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(96))
 def test_random_bulk_bitwise(seed):
     var = _case(20000 + seed, 1)
     if var is not None:
         assert var["dynamic_tail"] == 2  # the bulk kernel ran
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(32))
 def test_random_bulk_partitioned_bitwise(seed):
     _case(30000 + seed, 2 + seed % 3)
