@@ -54,6 +54,29 @@ constexpr int kProd = kBulkConsumers;    // the producer warp
 constexpr int kPB = 4;                   // tile positions per counter grab
 constexpr int kMaxMerge = 8;             // window-only plans: tiles merged per stage
 
+// columns per consumer lane of a bulk phase (compile time)
+template <int N>
+struct IC {
+  static constexpr int value = N;
+};
+#ifndef PHX_CPL4
+#define PHX_CPL4 1  // S terms with 4 columns per consumer lane
+#endif
+
+// canonical |.| row sum (group_rowsum's pairwise tree) of a CPL-4 row: the
+// lane holds columns (c, c+1) and (c + 2GL, c + 2GL + 1); the tree's levels
+// below 2GL columns run on both halves, its last level is lo + hi
+__device__ __forceinline__ double quad_rowsum(const double (&v)[4], int GL) {
+  double lo = v[0] + v[1], hi = v[2] + v[3];
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1)
+    if (m < GL) {  // GL is warp-uniform
+      lo = lo + __shfl_xor_sync(kFull, lo, m);
+      hi = hi + __shfl_xor_sync(kFull, hi, m);
+    }
+  return lo + hi;
+}
+
 __device__ __forceinline__ unsigned su32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -218,7 +241,16 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
   const bool master = blockIdx.x == 0 && threadIdx.x == 0 && (!PART || ga.plo == 0);
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;  // writes this launch's status
   const int nblk = (n + kPlanT - 1) / kPlanT;  // row blocks = plan tiles
-  int kpipe = 0;                               // ring stages used so far (producer == consumers)
+  // ring position (the same sequence in the producer and the consumers):
+  // stage index and the parity of its use, advanced without division
+  int kst = 0;
+  unsigned kpar = 0;
+  auto ring_next = [&]() {
+    if (++kst == NS) {
+      kst = 0;
+      kpar ^= 1u;
+    }
+  };
 #ifndef PHX_PROBE
 #define PHX_PROBE 0  // developer diagnostics: SM-cycle totals of ring waits and work
 #endif
@@ -380,8 +412,16 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
       cnt -= c;
     }
   };
-  auto bulk_phase = [&](int G, int ow, int width, const double* X, int xsel, const double* A,
+  // cpl: columns per consumer lane (compile time).  2: lane lg of a row's G
+  // lanes owns columns (2lg, 2lg+1).  4: lane lg of a row's G/2 lanes owns
+  // (2lg, 2lg+1) and (G+2lg, G+2lg+1) -- twice the rows per warp, so the
+  // per-entry slot / value / address work and the per-row loop, store and
+  // shuffle work are shared by twice the columns; each staged row is still
+  // read as contiguous 128-byte runs (no bank conflicts), and the canonical
+  // row-sum tree is unchanged (its last level becomes the in-lane lo + hi).
+  auto bulk_phase = [&](auto cpl, int G, int ow, int width, const double* X, int xsel, const double* A,
                         const double* B, auto&& gath, auto&& epi) -> unsigned long long {
+    constexpr int CPL = decltype(cpl)::value;
     const int nst = (A ? 1 : 0) + (B ? 1 : 0);
     int M = 1;
     if (a.plan_merge)
@@ -443,12 +483,12 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
           const int* d = pdesc[cur][j];
           // descriptors in processing order (merged stages: natural order)
           const int t = posA + j < npos ? (M == 1 ? d[5] : posA + j) : -1;
-          const int s = kpipe % NS;
+          const int s = kst;
           const long long pc0 = PHX_PROBE ? clock64() : 0;
           if (sleepw)
-            mbar_wait_sleep(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
+            mbar_wait_sleep(&bar_empty[s], kpar ^ 1u);
           else
-            mbar_wait(&bar_empty[s], ((kpipe / NS) & 1) ^ 1);
+            mbar_wait(&bar_empty[s], kpar ^ 1u);
           const long long pc1 = PHX_PROBE ? clock64() : 0;
           unsigned char* st = ring + size_t(s) * size_t(SB);
           unsigned long long* bf = &bar_full[s];
@@ -498,7 +538,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
             pr_pwait += pc1 - pc0;
             pr_pwork += clock64() - pc1;
           }
-          ++kpipe;
+          ring_next();
           if (t < 0) {
             more = false;
             break;
@@ -512,20 +552,21 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
       return mx;
     }
     // ---- consumers
-    const int gpw = 32 / G, g = lane / G, lg = lane % G;
-    const int c = 2 * lg;
-    const bool cv = c < ow;
+    const int GL = CPL == 4 ? (G > 1 ? G >> 1 : 1) : G;  // lanes per row
+    const int gpw = 32 / GL, g = lane / GL, lg = lane % GL;
+    const int c = 2 * lg, ch = c + 2 * GL;  // ch: the lane's second pair (CPL 4)
+    const bool cv = c < ow, cvh = ch < ow;
     for (;;) {
-      const int s = kpipe % NS;
+      const int s = kst;
       const long long cc0 = PHX_PROBE ? clock64() : 0;
       if (sleepw)
-        mbar_wait_sleep(&bar_full[s], (kpipe / NS) & 1);
+        mbar_wait_sleep(&bar_full[s], kpar);
       else
-        mbar_wait(&bar_full[s], (kpipe / NS) & 1);
+        mbar_wait(&bar_full[s], kpar);
       const long long cc1 = PHX_PROBE ? clock64() : 0;
       const unsigned char* st = ring + size_t(s) * size_t(SB);
       const int t = *reinterpret_cast<const int*>(st + L.hdr);
-      ++kpipe;
+      ring_next();
       if (t >= 0) {
         const int* rps = reinterpret_cast<const int*>(st + L.rp);
         const double* dr = reinterpret_cast<const double*>(st + L.dr);
@@ -539,17 +580,25 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
         for (int r0 = warp * gpw; r0 < rows; r0 += kBulkConsumers * gpw) {
           const int rr = r0 + g;
           const bool v = rr < rows && cv;
-          double a0 = 0.0, a1 = 0.0;
           // merged stages: the sub-tile's window starts dj rows into the stage's
           const int dj = max(row0 + base + (rr / kPlanT) * kPlanT - 1, 0) - wlo;
           if (PHX_CHECKS && v)
             for (int e = rps[rr] - e_lo; e < rps[rr + 1] - e_lo; ++e)
               PHX_CHECK(e >= 0 && e < a.plan_emax * M && int(sls[e]) + dj < (M > 1 ? TM + 2 : a.plan_rows));
-          if (v) gath(dr + dj * width, sls, avs, rps[rr] - e_lo, rps[rr + 1] - e_lo, c, a0, a1);
           const double* self = dr + (row0 + base + rr - wlo) * width;  // the row itself (window)
-          const unsigned long long m =
-              epi(v, rr < rows, base + rr, c, a0, a1, self, sa + rr * width + c, sb + rr * width + c, lg, G);
-          mx = umax64(mx, m);
+          if constexpr (CPL == 4) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (v) gath(dr + dj * width, sls, avs, rps[rr] - e_lo, rps[rr + 1] - e_lo, c, ch, cvh, acc);
+            const unsigned long long m = epi(v, v && cvh, rr < rows, base + rr, c, ch, acc, self,
+                                             sa + rr * width, sb + rr * width, GL);
+            mx = umax64(mx, m);
+          } else {
+            double a0 = 0.0, a1 = 0.0;
+            if (v) gath(dr + dj * width, sls, avs, rps[rr] - e_lo, rps[rr + 1] - e_lo, c, a0, a1);
+            const unsigned long long m =
+                epi(v, rr < rows, base + rr, c, a0, a1, self, sa + rr * width + c, sb + rr * width + c, lg, G);
+            mx = umax64(mx, m);
+          }
         }
       }
       __syncwarp();
@@ -573,6 +622,29 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
         const double av = avs[e];
         a0 = a0 + av * x.x;
         a1 = a1 + av * x.y;
+      }
+    };
+  };
+  // CPL 4: columns (c, c+1) and (ch, ch+1) of every entry's staged row, in
+  // CSR order (the second pair only where it exists: vh)
+  auto gath_quad = [&](int width) {
+    return [width](const double* dr, const unsigned char* sls, const double* avs, int e0, int e1,
+                   int c, int ch, bool vh, double(&acc)[4]) {
+      // the second pair's byte offset; a lane without one re-reads its first
+      // pair (unused), so no load is predicated
+      const int hb = vh ? (ch - c) * 8 : 0;
+      const unsigned rb = unsigned(width) * 8u;
+      const unsigned char* lo = reinterpret_cast<const unsigned char*>(dr + c);
+#pragma unroll 4
+      for (int e = e0; e < e1; ++e) {
+        const unsigned char* xr = lo + unsigned(sls[e]) * rb;
+        const double2 x = *reinterpret_cast<const double2*>(xr);
+        const double2 y = *reinterpret_cast<const double2*>(xr + hb);
+        const double av = avs[e];
+        acc[0] = acc[0] + av * x.x;
+        acc[1] = acc[1] + av * x.y;
+        acc[2] = acc[2] + av * y.x;
+        acc[3] = acc[3] + av * y.y;
       }
     };
   };
@@ -703,7 +775,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     double* const Dn1 = Dn;
     const double sig1 = sigma, rsig1 = 1.0 / sigma;
     const unsigned long long mdb = bulk_phase(
-        GS, w, p1e, a.D0, 0, nullptr, nullptr,
+        IC<2>{}, GS, w, p1e, a.D0, 0, nullptr, nullptr,
         // acc = sum_e av_e * Vw_1[col_e] = av_e * fl(V[col_e][src] * g)
         [&](const double* dr, const unsigned char* sls, const double* avs, int e0, int e1, int,
             double& a0, double& a1) {
@@ -781,29 +853,36 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     double dmy1, dmy2;
     sync_step(0ull, 0ull, dmy1, dmy2);
   }
+#if !PHX_CPL4
   // the lane's S-term column coefficients (fixed for the whole launch)
   int jjS[2];
   double kdS[2], kaS[2], tosS[2];
-  {
-    const int c = 2 * (lane % GS);
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int cc = c + e;
-      const bool ok = cc < w;
-      jjS[e] = ok ? cc / r : 0;
-      kdS[e] = ok ? __ldg(a.colKd + cc) : 0.0;
-      kaS[e] = ok ? __ldg(a.colKa + cc) : 0.0;
-      tosS[e] = ok ? __ldg(a.colTos + cc) : 0.0;
-    }
-  }
-  // The lane's Vw column coefficients of block j - 1 (column c - r): the
+  // kaL: the lane's Vw column coefficients of block j - 1 (column c - r): the
   // fold term recomputes Vw_{k-1}[c - r] from Vw_{k-2}.
   double kaL[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int cc = 2 * (lane % GS) + e;
-    kaL[e] = (cc < w && cc >= r) ? __ldg(a.colKa + (cc - r)) : 0.0;
+    const bool ok = cc < w;
+    jjS[e] = ok ? cc / r : 0;
+    kdS[e] = ok ? __ldg(a.colKd + cc) : 0.0;
+    kaS[e] = ok ? __ldg(a.colKa + cc) : 0.0;
+    tosS[e] = ok ? __ldg(a.colTos + cc) : 0.0;
+    kaL[e] = (ok && cc >= r) ? __ldg(a.colKa + (cc - r)) : 0.0;
   }
+#else
+  // CPL 4: the block index j of the lane's columns (c, c+1, ch, ch+1), a
+  // byte each; the column coefficients are read per pair (__ldg, L1-resident)
+  unsigned jjq = 0;
+  {
+    const int GLS = GS > 1 ? GS >> 1 : 1;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int cc = 2 * (lane % GLS) + (e < 2 ? 0 : 2 * GLS) + (e & 1);
+      jjq |= unsigned(cc < w ? cc / r : 0) << (8 * e);
+    }
+  }
+#endif
   // Paired S terms (bitwise the reference's per-term data flow, 25% fewer
   // bytes): S_k = S_{k-1} + D_k / sigma_k and Vw_k = Vw_{k-1} Kiter are
   // STORED only every other term.  A skip term (odd k >= 3) reads Vw_{k-1},
@@ -846,24 +925,140 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     double* const Dnn = Dn;
     const double sig = sigma, sigp = sig_prev, rsig = 1.0 / sigma, rsigp = 1.0 / sig_prev;
     // Vw_k[c] = fl(fl(+0 + Vw_{k-1}[c - r] Ka) + Vw_{k-1}[c] Kd) (:98)
-    auto vw_next = [&](int e, double vw, double vl) {
+    auto vw_nx = [&](int jj, double kd, double ka, double vw, double vl) {
       double g2 = 0.0;
-      if (jjS[e] >= 2) g2 = g2 + vl * kaS[e];
-      g2 = g2 + vw * kdS[e];
+      if (jj >= 2) g2 = g2 + vl * ka;
+      g2 = g2 + vw * kd;
       return g2;
     };
-    auto d_next = [&](int e, double acc, double ds, double g2) {
-      // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
+    // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
+    auto d_nx = [&](double tos, double acc, double ds, double g2) {
       double y = acc;
       if (has_xi) y = y - a.xi * ds;
-      y = y * tosS[e];
+      y = y * tos;
       return y + g2;
     };
+#if !PHX_CPL4
+    auto vw_next = [&](int e, double vw, double vl) { return vw_nx(jjS[e], kdS[e], kaS[e], vw, vl); };
+    auto d_next = [&](int e, double acc, double ds, double g2) { return d_nx(tosS[e], acc, ds, g2); };
+#endif
     unsigned long long mdb;
+#if PHX_CPL4
+    // CPL 4 (see bulk_phase): the lane's column pairs h = 0, 1 at cp = c, ch;
+    // the pairs' coefficients are read per row (__ldg: L1-resident); pa / pb:
+    // the row's staged stream rows.  With r even (double2 shifts) the
+    // optional shifted loads are unconditional -- every such address stays
+    // inside the stage -- and zeroed by select, which is bitwise the branchy
+    // form: fl(+0 + 0 * Ka) = +0 for the finite Ka.
+    auto jsel = [](bool on, double2 x) { return on ? x : make_double2(0.0, 0.0); };
+    auto vw_b = [&](double kd, double ka, double vw, double vl) {  // vl = 0 where j < 2
+      double g2 = 0.0;
+      g2 = g2 + vl * ka;
+      g2 = g2 + vw * kd;
+      return g2;
+    };
     if (!s_stale) {
       // skip term: Vw_{k-1} in, D_k out
       mdb = bulk_phase(
-          GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, nullptr, gath_pair(w),
+          IC<4>{}, GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, nullptr, gath_quad(w),
+          [&](bool v0, bool v1, bool rvalid, int row, int c, int ch, const double(&acc)[4],
+              const double* self, const double* pa, const double*, int GL) -> unsigned long long {
+            double ad[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int cp = h ? ch : c;
+              if (h ? v1 : v0) {
+                const unsigned jx = (jjq >> (16 * h)) & 0xffu, jy = (jjq >> (16 * h + 8)) & 0xffu;
+                const double2 kd = __ldg(reinterpret_cast<const double2*>(a.colKd + cp));
+                const double2 ka = __ldg(reinterpret_cast<const double2*>(a.colKa + cp));
+                const double2 tos = __ldg(reinterpret_cast<const double2*>(a.colTos + cp));
+                const double2 vw = *reinterpret_cast<const double2*>(pa + cp);
+                double2 vl = make_double2(0.0, 0.0);
+                if (vwl_vec) {
+                  vl = jsel(jx >= 2, *reinterpret_cast<const double2*>(pa + cp - r));
+                } else {
+                  if (jx >= 2) vl.x = pa[cp - r];
+                  if (jy >= 2) vl.y = pa[cp + 1 - r];
+                }
+                double2 ds = make_double2(0.0, 0.0);
+                if (has_xi) ds = *reinterpret_cast<const double2*>(self + cp);
+                const double d0 = d_nx(tos.x, acc[2 * h], ds.x, vw_b(kd.x, ka.x, vw.x, vl.x));
+                const double d1 = d_nx(tos.y, acc[2 * h + 1], ds.y, vw_b(kd.y, ka.y, vw.y, vl.y));
+                ad[2 * h] = fabs(d0);
+                ad[2 * h + 1] = fabs(d1);
+                __stcs(reinterpret_cast<double2*>(Dnn + (unsigned(row) * ldb + cp)), make_double2(d0, d1));
+              }
+            }
+            const double rd = quad_rowsum(ad, GL);
+            return rvalid ? abs_bits(rd) : 0ull;
+          });
+    } else {
+      // fold term: Vw_{k-2} and S_{k-2} in; Vw_k, D_k, S_k out
+      mdb = bulk_phase(
+          IC<4>{}, GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, a.S, gath_quad(w),
+          [&](bool v0, bool v1, bool rvalid, int row, int c, int ch, const double(&acc)[4],
+              const double* self, const double* pa, const double* pb, int GL) -> unsigned long long {
+            double ad[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int cp = h ? ch : c;
+              if (h ? v1 : v0) {
+                const unsigned jx = (jjq >> (16 * h)) & 0xffu, jy = (jjq >> (16 * h + 8)) & 0xffu;
+                const double2 kd2 = __ldg(reinterpret_cast<const double2*>(a.colKd + cp));
+                const double2 ka2 = __ldg(reinterpret_cast<const double2*>(a.colKa + cp));
+                const double2 tos2 = __ldg(reinterpret_cast<const double2*>(a.colTos + cp));
+                // Vw_{k-2}[c], [c - r], [c - 2r] (zeros where the block has none)
+                const double2 x0 = *reinterpret_cast<const double2*>(pa + cp);
+                double2 x1 = make_double2(0.0, 0.0), x2 = make_double2(0.0, 0.0);
+                if (vwl_vec) {
+                  x1 = jsel(jx >= 1, *reinterpret_cast<const double2*>(pa + cp - r));
+                  x2 = jsel(jx >= 2, *reinterpret_cast<const double2*>(pa + cp - 2 * r));
+                } else {
+                  if (jx >= 1) x1.x = pa[cp - r];
+                  if (jy >= 1) x1.y = pa[cp + 1 - r];
+                  if (jx >= 2) x2.x = pa[cp - 2 * r];
+                  if (jy >= 2) x2.y = pa[cp + 1 - 2 * r];
+                }
+                const double2 so = *reinterpret_cast<const double2*>(pb + cp);
+                const double2 dp = *reinterpret_cast<const double2*>(self + cp);  // D_{k-1}
+                const double v0v[2] = {x0.x, x0.y}, v1v[2] = {x1.x, x1.y}, v2v[2] = {x2.x, x2.y},
+                             sov[2] = {so.x, so.y}, dpv[2] = {dp.x, dp.y};
+                const unsigned jjv[2] = {jx, jy};
+                const double kdv[2] = {kd2.x, kd2.y}, kav[2] = {ka2.x, ka2.y}, tov[2] = {tos2.x, tos2.y};
+                double vn[2], dn[2], sn[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                  // Vw_{k-1}[c] (x1 = 0 where j < 2) and Vw_{k-1}[c - r] (j >= 2:
+                  // fl(fl(+0 + Vw[c - 2r] Ka(c - r)) + Vw[c - r] Kd), x2 = 0 where j < 3)
+                  const double wc = vw_b(kdv[q], kav[q], v0v[q], jjv[q] >= 2 ? v1v[q] : 0.0);
+                  double wl = 0.0;
+                  if (jjv[q] >= 2) {
+                    const double kl = __ldg(a.colKa + (cp + q - r));  // Ka of column c - r
+                    wl = 0.0;
+                    wl = wl + (jjv[q] >= 3 ? v2v[q] : 0.0) * kl;
+                    wl = wl + v1v[q] * kdv[q];
+                  }
+                  vn[q] = vw_b(kdv[q], kav[q], wc, wl);                // Vw_k
+                  dn[q] = d_nx(tov[q], acc[2 * h + q], dpv[q], vn[q]);  // D_k (ds = D_{k-1} row)
+                  const double s1 = sov[q] + div_rcp(dpv[q], sigp, rsigp);  // S_{k-1} (:105)
+                  sn[q] = s1 + div_rcp(dn[q], sig, rsig);                   // S_k
+                  ad[2 * h + q] = fabs(dn[q]);
+                }
+                const unsigned o = unsigned(row) * ldb + cp;
+                __stcs(reinterpret_cast<double2*>(a.Vw + o), make_double2(vn[0], vn[1]));
+                __stcs(reinterpret_cast<double2*>(Dnn + o), make_double2(dn[0], dn[1]));
+                __stcs(reinterpret_cast<double2*>(a.S + o), make_double2(sn[0], sn[1]));
+              }
+            }
+            const double rd = quad_rowsum(ad, GL);
+            return rvalid ? abs_bits(rd) : 0ull;
+          });
+    }
+#else
+    if (!s_stale) {
+      // skip term: Vw_{k-1} in, D_k out
+      mdb = bulk_phase(
+          IC<2>{}, GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, nullptr, gath_pair(w),
           [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
               const double* pa, const double*, int, int G) -> unsigned long long {
             double ad[1][2] = {{0.0, 0.0}};
@@ -890,7 +1085,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     } else {
       // fold term: Vw_{k-2} and S_{k-2} in; Vw_k, D_k, S_k out
       mdb = bulk_phase(
-          GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, a.S, gath_pair(w),
+          IC<2>{}, GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, a.S, gath_pair(w),
           [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
               const double* pa, const double* pb, int, int G) -> unsigned long long {
             double ad[1][2] = {{0.0, 0.0}};
@@ -937,6 +1132,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
             return rvalid ? abs_bits(rd) : 0ull;
           });
     }
+#endif
     s_stale = !s_stale;
     double maxD, dmy;
     sync_step(mdb, mdb, maxD, dmy);
@@ -987,7 +1183,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
   double* Fn = a.F1;
   const bool sweeps = SW && a.s_eff > 1;
   const unsigned long long mf = bulk_phase(
-      GF, fc, w, a.S, 2, nullptr, nullptr,
+      IC<2>{}, GF, fc, w, a.S, 2, nullptr, nullptr,
       // gathers S block-0 columns (left F columns live at the same column
       // index in S); a pair straddling the left/right split gathers one extra
       // column, unused
@@ -1115,7 +1311,7 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
       const double dkk = double(kk), rkk = 1.0 / dkk;
       double* const Fnn = Fn;
       const unsigned long long mfb = bulk_phase(
-          GF, fc, fc, Fc, Fc == a.F0 ? 3 : 4, a.E, nullptr, gath_pair(fc),
+          IC<2>{}, GF, fc, fc, Fc, Fc == a.F0 ? 3 : 4, a.E, nullptr, gath_pair(fc),
           [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
               const double* pa, const double*, int, int G) -> unsigned long long {
             double ay[1][2] = {{0.0, 0.0}};
