@@ -62,6 +62,9 @@ struct IC {
 #ifndef PHX_CPL4
 #define PHX_CPL4 1  // S terms with 4 columns per consumer lane
 #endif
+#ifndef PHX_FAST_S
+#define PHX_FAST_S (!PHX_CHECKS)  // specialised S-term consumer (8 lanes per row, r even, w <= 32)
+#endif
 
 // canonical |.| row sum (group_rowsum's pairwise tree) of a CPL-4 row: the
 // lane holds columns (c, c+1) and (c + 2GL, c + 2GL + 1); the tree's levels
@@ -194,6 +197,9 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
   __shared__ const double* gtab[5][PART ? kMaxParts : 1];  // [D0, D1, S, F0, F1][part]
   __shared__ int sbnd[PART ? kMaxParts + 1 : 1];           // part row boundaries (global)
   __shared__ double gmax[2];
+  // the S-term column coefficients Kd, Ka, t/s and Ka of column c - r
+  // (columns 0..31, zeros past w) for the specialised S-term consumer
+  __shared__ __align__(16) double ctab[4][32];
   const double INF = __longlong_as_double(0x7FF0000000000000ll);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const BlockArgs& ga = part_args(gp, 0);  // the fields common to all parts
@@ -567,7 +573,10 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
       const unsigned char* st = ring + size_t(s) * size_t(SB);
       const int t = *reinterpret_cast<const int*>(st + L.hdr);
       ring_next();
-      if (t >= 0) {
+      if constexpr (CPL == 8) {
+        // the specialised S-term consumer: `gath` is the stage body
+        if (t >= 0) mx = umax64(mx, gath(st, L, t, TM, M));
+      } else if (t >= 0) {
         const int* rps = reinterpret_cast<const int*>(st + L.rp);
         const double* dr = reinterpret_cast<const double*>(st + L.dr);
         const double* sa = reinterpret_cast<const double*>(st + L.sa);
@@ -883,6 +892,181 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     }
   }
 #endif
+  // The specialised S-term consumer (skip and fold terms of the common
+  // shape: 16 < w <= 32, i.e. 8 lanes per row and 4 rows per warp pass; r
+  // even; xi != 0).  The same per-element operations in the same order as the
+  // general CPL-4 consumer below -- bitwise unchanged -- with what that
+  // consumer decides at run time fixed at compile time: the lane's second
+  // column pair sits 128 bytes after its first (immediate offsets, loaded
+  // unconditionally and masked at the stores), the column coefficients come
+  // from the shared table ctab (lane-constant addresses) instead of global
+  // loads, a row's entries are gathered in blocks of 4 / 2 / 1 with a
+  // block's loads issued before its arithmetic, and the row-sum tree has its
+  // three shuffle levels unrolled.
+  const bool fastS = PHX_FAST_S && PHX_CPL4 && GS == 16 && (r % 2) == 0 && w <= 32 && has_xi &&
+                     (a.bulk_flags & 4) == 0;
+  if (fastS) {
+    if (threadIdx.x < 32) {
+      const int cc = threadIdx.x;
+      const bool ok = cc < w;
+      ctab[0][cc] = ok ? __ldg(a.colKd + cc) : 0.0;
+      ctab[1][cc] = ok ? __ldg(a.colKa + cc) : 0.0;
+      ctab[2][cc] = ok ? __ldg(a.colTos + cc) : 0.0;
+      ctab[3][cc] = (ok && cc >= r) ? __ldg(a.colKa + (cc - r)) : 0.0;
+    }
+    __syncthreads();
+  }
+  auto s_fast = [&](auto foldc, double* Dnn, double sig, double sigp) {
+    constexpr bool FOLD = decltype(foldc)::value != 0;
+    const int lg = lane & 7, g = lane >> 3;
+    const int c = 2 * lg;              // the lane's pairs: columns (c, c+1) and (16+c, 17+c)
+    const bool v1 = 16 + c < w;        // the second pair exists (the first always does: w > 16)
+    const int jA = c / r, jB = v1 ? (16 + c) / r : 0;  // the pairs' block index (r even)
+    const unsigned rb = unsigned(w) * 8u, cb = unsigned(c) * 8u, r8 = unsigned(r) * 8u;
+    const double* const ct = &ctab[0][c];
+    const double xi = a.xi;
+    return [=, &a](const unsigned char* st, const BulkStage& L, int t, int TM, int M) -> unsigned long long {
+      const int base = t * TM, rows = min(TM, n - base);
+      const int* const rps = reinterpret_cast<const int*>(st + L.rp);
+      const int e_lo = rps[0];
+      // indexed by the absolute entry number
+      const unsigned char* const sls = st + L.sl + ((e_lo & 15) - e_lo);
+      const double* const avs = reinterpret_cast<const double*>(st + L.av) + ((e_lo & 1) - e_lo);
+      const int wlo = max(row0 + base - 1, 0);
+      const unsigned char* const xb = st + L.dr + cb;
+      const unsigned char* const selfb = xb + unsigned(row0 + base - wlo) * rb;
+      const unsigned char* const pab = st + L.sa + cb;
+      const unsigned char* const pbb = st + L.sb + cb;
+      unsigned long long mx = 0;
+#ifdef PHX_DIAG
+      if (a.bulk_flags & 16) return 0x3ff0000000000000ull;  // developer: consumers idle
+#endif
+      for (int r0 = warp * 4; r0 < rows; r0 += kBulkConsumers * 4) {
+        const int rr = r0 + g;
+        const bool rv = rr < rows;
+        int e = 0, e1 = 0;
+        if (rv) {
+          e = rps[rr];
+          e1 = rps[rr + 1];
+        }
+#ifdef PHX_DIAG
+        if (a.bulk_flags & 8) e1 = e;  // developer: no gather
+#endif
+        const unsigned char* xr = xb;
+        if (M > 1) xr += unsigned(max(row0 + base + (rr / kPlanT) * kPlanT - 1, 0) - wlo) * rb;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        // NB entries: all loads first, then the products and sums in CSR order
+#define PHX_GBLK(NB)                                                                   \
+  {                                                                                    \
+    unsigned sl_[NB];                                                                  \
+    double av_[NB];                                                                    \
+    double2 x_[NB], y_[NB];                                                            \
+    _Pragma("unroll") for (int q = 0; q < NB; ++q) {                                   \
+      sl_[q] = sls[e + q];                                                             \
+      av_[q] = avs[e + q];                                                             \
+    }                                                                                  \
+    _Pragma("unroll") for (int q = 0; q < NB; ++q) {                                   \
+      const unsigned char* xe = xr + sl_[q] * rb;                                      \
+      x_[q] = *reinterpret_cast<const double2*>(xe);                                   \
+      y_[q] = *reinterpret_cast<const double2*>(xe + 128);                             \
+    }                                                                                  \
+    _Pragma("unroll") for (int q = 0; q < NB; ++q) {                                   \
+      acc[0] = acc[0] + av_[q] * x_[q].x;                                              \
+      acc[1] = acc[1] + av_[q] * x_[q].y;                                              \
+      acc[2] = acc[2] + av_[q] * y_[q].x;                                              \
+      acc[3] = acc[3] + av_[q] * y_[q].y;                                              \
+    }                                                                                  \
+  }
+        for (; e + 4 <= e1; e += 4) PHX_GBLK(4)
+        if (e + 2 <= e1) {
+          PHX_GBLK(2)
+          e += 2;
+        }
+        if (e < e1) PHX_GBLK(1)
+#undef PHX_GBLK
+        const unsigned char* const par = pab + unsigned(rr) * rb;
+        const unsigned char* const selfr = selfb + unsigned(rr) * rb;
+        const unsigned o = unsigned(base + rr) * ldb + unsigned(c);
+        double ad[4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int off = 128 * h;
+          const bool hv = rv && (h == 0 || v1);
+          const int jj = h ? jB : jA;
+          const double2 kd = *reinterpret_cast<const double2*>(ct + 16 * h);
+          const double2 ka = *reinterpret_cast<const double2*>(ct + 32 + 16 * h);
+          const double2 tos = *reinterpret_cast<const double2*>(ct + 64 + 16 * h);
+          const double2 x0 = *reinterpret_cast<const double2*>(par + off);
+          const double2 x1r = *reinterpret_cast<const double2*>(par + off - r8);
+          const double2 ds = *reinterpret_cast<const double2*>(selfr + off);
+          // Vw_k[c] = fl(fl(+0 + Vw_{k-1}[c - r] Ka) + Vw_{k-1}[c] Kd) (:98)
+          auto vwb = [](double kd_, double ka_, double vw, double vl) {
+            double g2 = 0.0;
+            g2 = g2 + vl * ka_;
+            g2 = g2 + vw * kd_;
+            return g2;
+          };
+          // D = (A - xi I) D (:99), * t_i/s (:101), + Vw (:102)
+          auto dnx = [xi](double tos_, double ac, double dsv, double g2) {
+            double y = ac - xi * dsv;
+            y = y * tos_;
+            return y + g2;
+          };
+          const bool j2 = jj >= 2;
+          const double2 x1 = make_double2(j2 ? x1r.x : 0.0, j2 ? x1r.y : 0.0);
+          if constexpr (!FOLD) {
+            // skip term: Vw_{k-1} in, D_k out
+            const double d0 = dnx(tos.x, acc[2 * h], ds.x, vwb(kd.x, ka.x, x0.x, x1.x));
+            const double d1 = dnx(tos.y, acc[2 * h + 1], ds.y, vwb(kd.y, ka.y, x0.y, x1.y));
+            ad[2 * h] = hv ? fabs(d0) : 0.0;
+            ad[2 * h + 1] = hv ? fabs(d1) : 0.0;
+            if (hv) __stcs(reinterpret_cast<double2*>(Dnn + (o + 16 * h)), make_double2(d0, d1));
+          } else {
+            // fold term: Vw_{k-2} and S_{k-2} in; Vw_k, D_k, S_k out (ds = D_{k-1})
+            const double2 kl = *reinterpret_cast<const double2*>(ct + 96 + 16 * h);
+            const double2 x2r = *reinterpret_cast<const double2*>(par + off - 2 * r8);
+            const double2 so = *reinterpret_cast<const double2*>(pbb + unsigned(rr) * rb + off);
+            const bool j3 = jj >= 3;
+            const double2 x2 = make_double2(j3 ? x2r.x : 0.0, j3 ? x2r.y : 0.0);
+            double vn[2], dn[2], sn[2];
+            const double kdv[2] = {kd.x, kd.y}, kav[2] = {ka.x, ka.y}, tov[2] = {tos.x, tos.y},
+                         klv[2] = {kl.x, kl.y}, x0v[2] = {x0.x, x0.y}, x1v[2] = {x1.x, x1.y},
+                         x1rv[2] = {x1r.x, x1r.y}, x2v[2] = {x2.x, x2.y}, sov[2] = {so.x, so.y},
+                         dpv[2] = {ds.x, ds.y};
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              // Vw_{k-1}[c] and Vw_{k-1}[c - r], as the skip term formed them
+              const double wc = vwb(kdv[q], kav[q], x0v[q], x1v[q]);
+              double wl = 0.0;
+              wl = wl + x2v[q] * klv[q];
+              wl = wl + x1rv[q] * kdv[q];
+              wl = j2 ? wl : 0.0;
+              vn[q] = vwb(kdv[q], kav[q], wc, wl);                 // Vw_k
+              dn[q] = dnx(tov[q], acc[2 * h + q], dpv[q], vn[q]);  // D_k
+              const double s1 = sov[q] + dpv[q] / sigp;            // S_{k-1} (:105)
+              sn[q] = s1 + dn[q] / sig;                            // S_k
+              ad[2 * h + q] = hv ? fabs(dn[q]) : 0.0;
+            }
+            if (hv) {
+              __stcs(reinterpret_cast<double2*>(a.Vw + (o + 16 * h)), make_double2(vn[0], vn[1]));
+              __stcs(reinterpret_cast<double2*>(Dnn + (o + 16 * h)), make_double2(dn[0], dn[1]));
+              __stcs(reinterpret_cast<double2*>(a.S + (o + 16 * h)), make_double2(sn[0], sn[1]));
+            }
+          }
+        }
+        // the canonical row sum: pairwise tree over the 32 (padded) columns
+        double lo = ad[0] + ad[1], hi = ad[2] + ad[3];
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1) {
+          lo = lo + __shfl_xor_sync(kFull, lo, m);
+          hi = hi + __shfl_xor_sync(kFull, hi, m);
+        }
+        const double rd = lo + hi;
+        if (rv) mx = umax64(mx, abs_bits(rd));
+      }
+      return mx;
+    };
+  };
   // Paired S terms (bitwise the reference's per-term data flow, 25% fewer
   // bytes): S_k = S_{k-1} + D_k / sigma_k and Vw_k = Vw_{k-1} Kiter are
   // STORED only every other term.  A skip term (odd k >= 3) reads Vw_{k-1},
@@ -957,7 +1141,14 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
       g2 = g2 + vw * kd;
       return g2;
     };
-    if (!s_stale) {
+    if (fastS) {
+      if (!s_stale)
+        mdb = bulk_phase(IC<8>{}, GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, nullptr,
+                         s_fast(IC<0>{}, Dnn, sig, sigp), 0);
+      else
+        mdb = bulk_phase(IC<8>{}, GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, a.S,
+                         s_fast(IC<1>{}, Dnn, sig, sigp), 0);
+    } else if (!s_stale) {
       // skip term: Vw_{k-1} in, D_k out
       mdb = bulk_phase(
           IC<4>{}, GS, w, w, Dc, Dc == a.D0 ? 0 : 1, a.Vw, nullptr, gath_quad(w),
@@ -1277,6 +1468,119 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     }
   }
 
+  // The specialised recovery-term consumer (8 < fc <= 16: 4 lanes per row
+  // with 4 columns each, 8 rows per warp pass; block variant; xi != 0): the
+  // general consumer's per-element operations in the same order -- bitwise
+  // unchanged -- at half the lanes per row, so the per-entry slot / value /
+  // address work, the row bookkeeping and the row-sum shuffles are shared by
+  // twice the columns.  Odd rows take their two column pairs in the opposite
+  // order, so a quarter-warp's 16-byte loads (two rows of 128 bytes) cover
+  // all 32 banks.
+  const bool fastF = PHX_FAST_S && GF == 8 && !a.single_variant && has_xi && (a.bulk_flags & 4) == 0;
+  auto r_fast = [&](double* Fnn, double dkk) {
+    const int lg = lane & 3, g = lane >> 2;
+    const int cA = 2 * lg + ((g & 1) ? 8 : 0), cB = 2 * lg + ((g & 1) ? 0 : 8);  // the lane's pairs
+    const bool vA = cA < fc, vB = cB < fc;
+    const unsigned rb = unsigned(fc) * 8u, offA = unsigned(cA) * 8u;
+    const int dAB = (cB - cA) * 8;
+    double tA[2], tB[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int ca = cA + e, cb_ = cB + e;
+      tA[e] = ca < fc ? __ldg(a.colTos + (ca < r ? ca : ca - r)) : 0.0;
+      tB[e] = cb_ < fc ? __ldg(a.colTos + (cb_ < r ? cb_ : cb_ - r)) : 0.0;
+    }
+    const double tA0 = tA[0], tA1 = tA[1], tB0 = tB[0], tB1 = tB[1];
+    const double xi = a.xi;
+    return [=, &a](const unsigned char* st, const BulkStage& L, int t, int TM, int M) -> unsigned long long {
+      const int base = t * TM, rows = min(TM, n - base);
+      const int* const rps = reinterpret_cast<const int*>(st + L.rp);
+      const int e_lo = rps[0];
+      const unsigned char* const sls = st + L.sl + ((e_lo & 15) - e_lo);
+      const double* const avs = reinterpret_cast<const double*>(st + L.av) + ((e_lo & 1) - e_lo);
+      const int wlo = max(row0 + base - 1, 0);
+      const unsigned char* const xb = st + L.dr + offA;
+      const unsigned char* const selfb = xb + unsigned(row0 + base - wlo) * rb;
+      const unsigned char* const pab = st + L.sa + offA;
+      unsigned long long mx = 0;
+      for (int r0 = warp * 8; r0 < rows; r0 += kBulkConsumers * 8) {
+        const int rr = r0 + g;
+        const bool rv = rr < rows;
+        int e = 0, e1 = 0;
+        if (rv) {
+          e = rps[rr];
+          e1 = rps[rr + 1];
+        }
+        const unsigned char* xr = xb;
+        if (M > 1) xr += unsigned(max(row0 + base + (rr / kPlanT) * kPlanT - 1, 0) - wlo) * rb;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#define PHX_GBLK(NB)                                                                   \
+  {                                                                                    \
+    unsigned sl_[NB];                                                                  \
+    double av_[NB];                                                                    \
+    double2 x_[NB], y_[NB];                                                            \
+    _Pragma("unroll") for (int q = 0; q < NB; ++q) {                                   \
+      sl_[q] = sls[e + q];                                                             \
+      av_[q] = avs[e + q];                                                             \
+    }                                                                                  \
+    _Pragma("unroll") for (int q = 0; q < NB; ++q) {                                   \
+      const unsigned char* xe = xr + sl_[q] * rb;                                      \
+      x_[q] = *reinterpret_cast<const double2*>(xe);                                   \
+      y_[q] = *reinterpret_cast<const double2*>(xe + dAB);                             \
+    }                                                                                  \
+    _Pragma("unroll") for (int q = 0; q < NB; ++q) {                                   \
+      acc[0] = acc[0] + av_[q] * x_[q].x;                                              \
+      acc[1] = acc[1] + av_[q] * x_[q].y;                                              \
+      acc[2] = acc[2] + av_[q] * y_[q].x;                                              \
+      acc[3] = acc[3] + av_[q] * y_[q].y;                                              \
+    }                                                                                  \
+  }
+        for (; e + 4 <= e1; e += 4) PHX_GBLK(4)
+        if (e + 2 <= e1) {
+          PHX_GBLK(2)
+          e += 2;
+        }
+        if (e < e1) PHX_GBLK(1)
+#undef PHX_GBLK
+        const unsigned char* const par = pab + unsigned(rr) * rb;
+        const unsigned char* const selfr = selfb + unsigned(rr) * rb;
+        const double2 eoA = *reinterpret_cast<const double2*>(par);
+        const double2 eoB = *reinterpret_cast<const double2*>(par + dAB);
+        const double2 fsA = *reinterpret_cast<const double2*>(selfr);
+        const double2 fsB = *reinterpret_cast<const double2*>(selfr + dAB);
+        // y = ((A - xi I) F) / kk (:132) * t_i/s (:134-135); E += F (:138)
+        auto term = [xi, dkk](double ac, double fs, double tos_) {
+          double yv = ac - xi * fs;
+          yv = yv / dkk;
+          return yv * tos_;
+        };
+        const double yA0 = term(acc[0], fsA.x, tA0), yA1 = term(acc[1], fsA.y, tA1);
+        const double yB0 = term(acc[2], fsB.x, tB0), yB1 = term(acc[3], fsB.y, tB1);
+        const bool hA = rv && vA, hB = rv && vB;
+        const unsigned o = unsigned(base + rr) * ldf;
+        if (hA) {
+          __stcs(reinterpret_cast<double2*>(Fnn + (o + unsigned(cA))), make_double2(yA0, yA1));
+          __stcs(reinterpret_cast<double2*>(a.E + (o + unsigned(cA))), make_double2(eoA.x + yA0, eoA.y + yA1));
+        }
+        if (hB) {
+          __stcs(reinterpret_cast<double2*>(Fnn + (o + unsigned(cB))), make_double2(yB0, yB1));
+          __stcs(reinterpret_cast<double2*>(a.E + (o + unsigned(cB))), make_double2(eoB.x + yB0, eoB.y + yB1));
+        }
+        // the canonical row sum: pairwise tree over the 16 (padded) columns
+        double sA = (hA ? fabs(yA0) : 0.0) + (hA ? fabs(yA1) : 0.0);
+        double sB = (hB ? fabs(yB0) : 0.0) + (hB ? fabs(yB1) : 0.0);
+#pragma unroll
+        for (int m = 1; m < 4; m <<= 1) {
+          sA = sA + __shfl_xor_sync(kFull, sA, m);
+          sB = sB + __shfl_xor_sync(kFull, sB, m);
+        }
+        const double rd = sA + sB;
+        if (rv) mx = umax64(mx, abs_bits(rd));
+      }
+      return mx;
+    };
+  };
+
   // ================= recovery sweeps (phi_block.cpp:122-146)
   for (int sweep = 1; sweep < a.s_eff; ++sweep) {
     int kk = 0;
@@ -1310,7 +1614,9 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
       const double fac = a.single_variant ? a.t_single / (double(a.s_eff) * kk) : 0.0;
       const double dkk = double(kk), rkk = 1.0 / dkk;
       double* const Fnn = Fn;
-      const unsigned long long mfb = bulk_phase(
+      const unsigned long long mfb = fastF ? bulk_phase(IC<8>{}, GF, fc, fc, Fc, Fc == a.F0 ? 3 : 4, a.E,
+                                                        nullptr, r_fast(Fnn, dkk), 0)
+                                           : bulk_phase(
           IC<2>{}, GF, fc, fc, Fc, Fc == a.F0 ? 3 : 4, a.E, nullptr, gath_pair(fc),
           [&](bool v, bool rvalid, int row, int c, double a0, double a1, const double* self,
               const double* pa, const double*, int, int G) -> unsigned long long {

@@ -123,7 +123,9 @@ struct BlockArgs {
   int32_t bulk_ns;       // stages in the ring
   int32_t bulk_stage_bytes;
   int32_t bulk_flags;    // bit 0: gather copies evict_last (else evict_normal); bit 1: try_wait
-                         // with a suspend-time hint (waiting warps sleep instead of spinning)
+                         // with a suspend-time hint (waiting warps sleep instead of spinning);
+                         // bit 2: general consumers only (no specialised S-term / recovery-term
+                         // consumer: the A/B and test switch, PHX_BULK_FLAGS)
   // diagnostics (PHX_STEP_TIMES): %globaltimer after each grid step barrier
   // at [step]; CTA arrivals (time mod 2^48 | smid << 48) at
   // [kCtaStampBase + step * ncta + cta]

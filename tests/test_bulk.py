@@ -108,6 +108,54 @@ def test_groups_and_singles_bitwise_bulk(p_, r):
     assert np.array_equal(res.W, Wo)
 
 
+@pytest.mark.parametrize("p_,r", [(4, 6), (3, 8), (2, 6), (1, 8), (1, 6), (2, 10)])
+def test_specialised_consumers_bitwise(p_, r, monkeypatch):
+    """The specialised S-term consumer (16 < w <= 32, r even, xi != 0) and the
+    specialised recovery-term consumer (8 < 2r <= 16) against the oracle and
+    against the general consumers (PHX_BULK_FLAGS bit 2 switches them off):
+    groups, single rows, a ragged last tile, recovery sweeps."""
+    P_ = P()
+    n, rp, ci, av = _banded_with_far(20011 + 7 * r, 90 + p_ + r, 0.2, 20.0)
+    op = P_.CsrOperator(n, rp, ci, av)
+    oop = O.csr_from_arrays(n, rp, ci, av)
+    tol = 1e-10
+    ss = O.select_parameters(oop, 61, tol)
+    assert ss.xi != 0.0
+    rng = O.Rng(17 + p_ + r)
+    V = rng.matrix(n, p_ + 1)
+    t = (0.5 + rng.uniforms(r)) * (2.5 / ss.s)
+    alpha = -1.0 + 2.0 * rng.uniforms(r)
+    Wo, ro = O.phimv_block(oop, t, alpha, V, tol, ss)
+    req = P_.BlockPhiRequest(t, alpha, V, tol, P_.ScalingShift(*ss.astuple()))
+    res = P_.phimv_block(op, req)
+    assert bulk_used()
+    assert ro.s_effective > 1
+    assert (res.stats.series_len_S, res.stats.series_lens_F) == (ro.series_len_S, ro.series_lens_F)
+    assert np.array_equal(res.W, Wo)
+    monkeypatch.setenv("PHX_BULK_FLAGS", "6")  # the general consumers
+    gen = P_.phimv_block(op, req)
+    assert bulk_used()
+    assert np.array_equal(gen.W, Wo)
+
+
+def test_specialised_consumers_window_only_plan(monkeypatch):
+    """A banded operator whose plan merges tiles per stage (window-only, C5's
+    shape) with w = 32 and fc = 16: both specialised consumers on merged stages."""
+    P_ = P()
+    wl = P_.workload(5, (1 << 13) + 77)
+    op = P_.CsrOperator(wl.n, wl.rp, wl.ci, wl.av)
+    oop = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    ss = O.select_parameters(oop, 61, wl.tol)
+    Wo, ro = O.phimv_block(oop, wl.t, wl.alpha, wl.V, wl.tol, ss)
+    req = P_.BlockPhiRequest(wl.t, wl.alpha, wl.V, wl.tol, P_.ScalingShift(*ss.astuple()))
+    res = P_.phimv_block(op, req)
+    assert bulk_used()
+    assert (res.stats.series_len_S, res.stats.series_lens_F) == (ro.series_len_S, ro.series_lens_F)
+    assert np.array_equal(res.W, Wo)
+    monkeypatch.setenv("PHX_BULK_FLAGS", "6")
+    assert np.array_equal(P_.phimv_block(op, req).W, Wo)
+
+
 def test_single_variant_bulk():
     """phimv (Alg. 2, r = 1): w, exp_v0 and the tail through the bulk kernel."""
     P_ = P()
