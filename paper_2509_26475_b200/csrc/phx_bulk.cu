@@ -1476,7 +1476,10 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
   // twice the columns.  Odd rows take their two column pairs in the opposite
   // order, so a quarter-warp's 16-byte loads (two rows of 128 bytes) cover
   // all 32 banks.
-  const bool fastF = PHX_FAST_S && GF == 8 && !a.single_variant && has_xi && (a.bulk_flags & 4) == 0;
+  // (window-only plans: their merged stages hold >= 64 rows, so all consumer
+  // warps have a pass; a 32-row stage would leave half of them idle)
+  const bool fastF = PHX_FAST_S && GF == 8 && !a.single_variant && has_xi && a.plan_merge != 0 &&
+                     (a.bulk_flags & 4) == 0;
   auto r_fast = [&](double* Fnn, double dkk) {
     const int lg = lane & 3, g = lane >> 2;
     const int cA = 2 * lg + ((g & 1) ? 8 : 0), cB = 2 * lg + ((g & 1) ? 0 : 8);  // the lane's pairs
