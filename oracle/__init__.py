@@ -84,6 +84,7 @@ def lib():
                                             C.POINTER(ScalingShiftC), C.c_int32, C.c_int32, dp,
                                             i64p, dp]
         L.orc_set_threads.argtypes = [C.c_int32]
+        L.orc_set_rowsum_order.argtypes = [C.c_int32]
         L.orc_phimv.argtypes = [C.c_int64, i64p, i32p, dp, C.c_double, C.c_double, C.c_int32, dp,
                                 C.c_int64, C.c_double, C.POINTER(ScalingShiftC), dp, dp, dp, i64p,
                                 i32p, C.c_int64]
@@ -347,6 +348,13 @@ def set_threads(threads: int):
     """Row-parallel loops for the CPU timing arms (results stay bitwise those
     of one thread; the reference is single-threaded: 1 is its configuration)."""
     lib().orc_set_threads(int(threads))
+
+
+def set_rowsum_order(order: int):
+    """Test hook: the summation order of inf_norm's row sums (0 = the canonical
+    pairwise tree; 1 = Eigen 3.4's packet-wise partial redux; 2 = sequential;
+    3 = 1 with a sequential last odd row).  See rowsum_abs in phx_oracle.cpp."""
+    lib().orc_set_rowsum_order(int(order))
 
 
 def phimv_block_timed(op: Csr, t, alpha, V, tol, params: ScalingShift, max_s_terms: int = 0,

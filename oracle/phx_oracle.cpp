@@ -164,6 +164,39 @@ static double tree_abs(const double* x, long lo, long len, long w) {
   return a + b;
 }
 
+// Alternative row-sum orders, for the robustness test only
+// (tests/test_oracle_port.py::test_rowsum_order_*): the reference's
+// `cwiseAbs().rowwise().sum()` (linop.cpp:53) leaves the order to Eigen, whose
+// version is not pinned.  Restated from Eigen's published
+// sources: 1 = the 4-unrolled packet-wise partial redux of Eigen 3.4
+// (p = c0; p += ((c1 + c2) + (c3 + c4)); ...; then the remaining columns one by
+// one); 2 = the scalar redux (c0 + c1 + c2 + ..., Eigen 3.3, and 3.4's rows
+// outside a full packet); 3 = order 1 for the rows in full 2-row packets
+// (SSE2) and order 2 for a last odd row.  0 = the canonical pairwise tree that
+// the product implements.  The test shows that every discrete outcome
+// (series lengths, sweeps) and hence W is the same under all of them on the
+// BASELINE configs.
+static int g_rowsum_order = 0;
+static double rowsum_abs(const double* row, long cols, long len, long i, long rows) {
+  int order = g_rowsum_order;
+  if (order == 3) order = (i < (rows & ~1L)) ? 1 : 2;
+  if (order == 1) {
+    const long size4 = (cols - 1) & ~3L;
+    double p = std::fabs(row[0]);
+    long c = 1;
+    for (; c < size4; c += 4)
+      p = p + ((std::fabs(row[c]) + std::fabs(row[c + 1])) + (std::fabs(row[c + 2]) + std::fabs(row[c + 3])));
+    for (; c < cols; ++c) p = p + std::fabs(row[c]);
+    return p;
+  }
+  if (order == 2) {
+    double p = std::fabs(row[0]);
+    for (long c = 1; c < cols; ++c) p = p + std::fabs(row[c]);
+    return p;
+  }
+  return tree_abs(row, 0, len, cols);
+}
+
 // inf_norm (linop.cpp:51-54): max_i sum_c |X_ic|; 0 for an empty matrix.
 static double inf_norm(const double* X, long rows, long cols, long ld) {
   if (rows == 0 || cols == 0) return 0.0;
@@ -175,7 +208,7 @@ static double inf_norm(const double* X, long rows, long cols, long ld) {
     double m = 0.0;
     for (long i = lo; i < hi; ++i) {
       for (long c = 0; c < cols; ++c) row[size_t(c)] = X[size_t(i) + size_t(c) * size_t(ld)];
-      m = nan_max(m, tree_abs(row.data(), 0, len, cols));
+      m = nan_max(m, rowsum_abs(row.data(), cols, len, i, rows));
     }
     const long chunk = rows < 65536 ? rows : (rows + g_threads - 1) / g_threads;
     part[size_t(lo / std::max(1L, chunk))] = m;
@@ -1707,6 +1740,8 @@ int orc_phimv_block_timed(int64_t n, const int64_t* rp, const int32_t* ci, const
 // threads of the row-parallel loops (bench.py CPU arms); 1 = the reference's
 // configuration
 void orc_set_threads(int32_t threads) { orc::g_threads = threads < 1 ? 1 : threads; }
+// test hook: the row-sum order of inf_norm (0 canonical; see rowsum_abs)
+void orc_set_rowsum_order(int32_t order) { orc::g_rowsum_order = order; }
 
 int orc_phimv(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, double t, double alpha,
               int32_t p, const double* V, int64_t ldv, double tol, const orc_scaling_shift* params,

@@ -92,3 +92,29 @@ def test_workload_generators():
         d = wl.av[s:e][wl.ci[s:e] == i][0]
         off = np.abs(wl.av[s:e][wl.ci[s:e] != i]).sum()
         assert d < -off - 1.0 + 1e-9
+
+
+@pytest.mark.parametrize("cfg,size", [(1, 200), (2, 64), (3, 12), (4, 1024), (5, 2000)])
+def test_rowsum_order_does_not_change_outcomes(cfg, size):
+    """The Eigen boundary the verdict names (linop.cpp:53: the order of
+    `rowwise().sum()` is Eigen's, version unpinned): under Eigen 3.4's
+    packet-wise order, the sequential order and their mix, the stopping
+    decisions -- series length, sweeps and their lengths -- and therefore every
+    bit of W are the ones the canonical pairwise tree gives, on all five
+    BASELINE config shapes.  (The norms enter only the stopping tests.  Also
+    run once at C1 N = 1000, C2 200^2, C3 24^3, C4 and C5 at n = 2^14: same
+    result; left out of the suite for its run time.)"""
+    wl = P.workload(cfg, size)
+    op = O.csr_from_arrays(wl.n, wl.rp, wl.ci, wl.av)
+    ss = O.select_parameters(op, 61, wl.tol)
+    try:
+        O.set_rowsum_order(0)
+        W0, rec0 = O.phimv_block(op, wl.t, wl.alpha, wl.V, wl.tol, ss)
+        for order in (1, 2, 3):
+            O.set_rowsum_order(order)
+            W, rec = O.phimv_block(op, wl.t, wl.alpha, wl.V, wl.tol, ss)
+            assert (rec.s_effective, rec.series_len_S, rec.series_lens_F, rec.matvecs) == \
+                (rec0.s_effective, rec0.series_len_S, rec0.series_lens_F, rec0.matvecs), order
+            assert np.array_equal(W, W0), order
+    finally:
+        O.set_rowsum_order(0)
