@@ -705,6 +705,12 @@ void upload_plan(phx_op op, const int64_t* row_ptr, const int32_t* col_idx) {
 // Eligible: a tile plan, double2 lanes (both widths even) and single-chunk
 // rows (w <= 64), and a ring of >= 2 stages.  Two CTAs per SM with as many
 // stages (<= 4) as fit, else one CTA with up to 4.
+// stage size of window-only (merged-tile) plans; PHX_BULK_STAGE_KB: developer override
+static int32_t merged_stage_bytes() {
+  const char* e = std::getenv("PHX_BULK_STAGE_KB");
+  const int kb = e ? std::atoi(e) : 48;
+  return int32_t((kb < 8 ? 8 : kb > 200 ? 200 : kb) * 1024);
+}
 struct BulkChoice {
   bool use = false;
   int32_t ns = 0, stage_bytes = 0, per_sm = 0;
@@ -724,7 +730,7 @@ BulkChoice bulk_choice(phx_op op, int32_t V, int32_t QS, int32_t QF, int32_t w, 
   int32_t sb = std::max(ls.bytes, lf.bytes);
   // window-only plans merge tiles per stage (phx_bulk.cu): give their ring
   // fewer, larger stages (~48 KB)
-  if (op->plan_merge) sb = std::max(sb, int32_t(48 * 1024));
+  if (op->plan_merge) sb = std::max(sb, merged_stage_bytes());
   int optin = 0;
   PHX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, op->device));
   for (int want : {2, 1})
@@ -768,7 +774,7 @@ BulkPartChoice bulk_choice_parts(phx_op op, int32_t V, int32_t QS, int32_t QF, i
   const phx::BulkStage ls = phx::bulk_stage(bc.rows, bc.emax, w, 2);
   const phx::BulkStage lf = phx::bulk_stage(bc.rows, bc.emax, fcols, 1);
   int32_t sb = std::max(ls.bytes, lf.bytes);
-  if (bc.merge) sb = std::max(sb, int32_t(48 * 1024));
+  if (bc.merge) sb = std::max(sb, merged_stage_bytes());
   const int dev = op->parts[0].dev;
   DeviceGuard guard(dev);
   int optin = 0;
