@@ -68,7 +68,8 @@ def ncu_traffic(cfg, kernel="k_phimv_bulk"):
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(f"cfg{cfg}_{kernel}") or (d.get(f"cfg{cfg}") if kernel == "k_phimv_block" else None)
+        e = (d.get(f"cfg{cfg}_{kernel}_final") or d.get(f"cfg{cfg}_{kernel}")
+             or (d.get(f"cfg{cfg}") if kernel == "k_phimv_block" else None))
         return float(e["dram_bytes_per_launch"]) if e else None
     except Exception:
         return None

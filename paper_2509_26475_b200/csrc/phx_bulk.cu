@@ -63,7 +63,7 @@ struct IC {
 #define PHX_CPL4 1  // S terms with 4 columns per consumer lane
 #endif
 #ifndef PHX_FAST_S
-#define PHX_FAST_S (!PHX_CHECKS)  // specialised S-term consumer (8 lanes per row, r even, w <= 32)
+#define PHX_FAST_S 1  // specialised S-term / recovery-term consumers (see s_fast, r_fast)
 #endif
 
 // canonical |.| row sum (group_rowsum's pairwise tree) of a CPL-4 row: the
@@ -954,6 +954,12 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
 #endif
         const unsigned char* xr = xb;
         if (M > 1) xr += unsigned(max(row0 + base + (rr / kPlanT) * kPlanT - 1, 0) - wlo) * rb;
+        if (PHX_CHECKS && rv) {  // every entry and slot inside its stage region
+          const int dj = int((xr - xb) / rb);
+          PHX_CHECK(e >= e_lo && e1 >= e && e1 - e_lo <= a.plan_emax * M);
+          for (int q = e; q < e1; ++q) PHX_CHECK(int(sls[q]) + dj < (M > 1 ? TM + 2 : a.plan_rows));
+          PHX_CHECK(row0 + base + rr - wlo < (M > 1 ? TM + 2 : kPlanT + 2));
+        }
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         // NB entries: all loads first, then the products and sums in CSR order
 #define PHX_GBLK(NB)                                                                   \
@@ -1516,6 +1522,12 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
         }
         const unsigned char* xr = xb;
         if (M > 1) xr += unsigned(max(row0 + base + (rr / kPlanT) * kPlanT - 1, 0) - wlo) * rb;
+        if (PHX_CHECKS && rv) {  // every entry and slot inside its stage region
+          const int dj = int((xr - xb) / rb);
+          PHX_CHECK(e >= e_lo && e1 >= e && e1 - e_lo <= a.plan_emax * M);
+          for (int q = e; q < e1; ++q) PHX_CHECK(int(sls[q]) + dj < (M > 1 ? TM + 2 : a.plan_rows));
+          PHX_CHECK(row0 + base + rr - wlo < (M > 1 ? TM + 2 : kPlanT + 2));
+        }
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #define PHX_GBLK(NB)                                                                   \
   {                                                                                    \
