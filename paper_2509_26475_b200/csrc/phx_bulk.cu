@@ -1353,17 +1353,34 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     trace(1.0, c2, nS);
   }
   if (err == kStOk && s_stale) {
-    // the series ended on a skip term: S_L = fl(S_{L-1} + fl(D_L / sigma_L))
-    const int c = 2 * (lane % GS);
-    plain_rows(GS, [&](int row, bool rv, int) {
-      if (!rv || c >= w) return;
-      const unsigned o = unsigned(row) * ldb + c;
-      double2 x = *reinterpret_cast<const double2*>(a.S + o);
-      const double2 d = *reinterpret_cast<const double2*>(Dc + o);
-      x.x = x.x + d.x / sigma;
-      x.y = x.y + d.y / sigma;
-      *reinterpret_cast<double2*>(a.S + o) = x;
-    });
+    // the series ended on a skip term: S_L = fl(S_{L-1} + fl(D_L / sigma_L)).
+    // Row groups strided over all warps, NB groups per warp in flight (the
+    // pass is a pure stream; one group at a time left it latency-bound).
+    constexpr int NB = 4;
+    const int gpw = 32 / GS, g = lane / GS, c = 2 * (lane % GS);
+    const int nwarps = ncta * kBW, units = (n + gpw - 1) / gpw;
+    for (int u0 = cta * kBW + warp; u0 < units; u0 += NB * nwarps) {
+      double2 x[NB], d[NB];
+      unsigned o[NB];
+      bool v[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int u = u0 + b * nwarps, row = u * gpw + g;
+        v[b] = u < units && row < n && c < w;
+        o[b] = unsigned(row) * ldb + unsigned(c);
+        if (v[b]) {
+          x[b] = __ldcs(reinterpret_cast<const double2*>(a.S + o[b]));
+          d[b] = __ldcs(reinterpret_cast<const double2*>(Dc + o[b]));
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (v[b]) {
+          x[b].x = x[b].x + d[b].x / sigma;
+          x[b].y = x[b].y + d[b].y / sigma;
+          *reinterpret_cast<double2*>(a.S + o[b]) = x[b];
+        }
+    }
     double dmy1, dmy2;
     sync_step(0ull, 0ull, dmy1, dmy2);
     s_stale = false;
