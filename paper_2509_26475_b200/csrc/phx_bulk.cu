@@ -909,9 +909,13 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
     if (threadIdx.x < 32) {
       const int cc = threadIdx.x;
       const bool ok = cc < w;
-      ctab[0][cc] = ok ? __ldg(a.colKd + cc) : 0.0;
+      // (padding columns get Kd = t/s = 1: a lane without its second pair
+      // computes on the next row's values, never stores them, and must not
+      // produce the exact zeros that send a warp's IEEE division through its
+      // slow path on every row)
+      ctab[0][cc] = ok ? __ldg(a.colKd + cc) : 1.0;
       ctab[1][cc] = ok ? __ldg(a.colKa + cc) : 0.0;
-      ctab[2][cc] = ok ? __ldg(a.colTos + cc) : 0.0;
+      ctab[2][cc] = ok ? __ldg(a.colTos + cc) : 1.0;
       ctab[3][cc] = (ok && cc >= r) ? __ldg(a.colKa + (cc - r)) : 0.0;
     }
     __syncthreads();
