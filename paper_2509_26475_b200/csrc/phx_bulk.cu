@@ -1793,11 +1793,37 @@ __global__ void PHX_BULK_BOUNDS k_phimv_bulk(const __grid_constant__ typename Bu
 }  // namespace
 
 cudaError_t bulk_occupancy(size_t smem, int* per_sm, bool part) {
-  const void* f = part ? reinterpret_cast<const void*>(k_phimv_bulk<true>)
-                       : reinterpret_cast<const void*>(k_phimv_bulk<false>);
-  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  // both instantiations (with / without recovery code) of the variant must
+  // fit: the launch picks one of them by s_eff
+  const void* fs[2] = {part ? reinterpret_cast<const void*>(k_phimv_bulk<true, true>)
+                            : reinterpret_cast<const void*>(k_phimv_bulk<false, true>),
+                       part ? reinterpret_cast<const void*>(k_phimv_bulk<true, false>)
+                            : reinterpret_cast<const void*>(k_phimv_bulk<false, false>)};
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, f, kBulkThreads, smem);
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  int per = 1 << 30;
+  for (const void* f : fs) {
+    // the opt-in limit covers the kernel's static shared memory too: a ring
+    // that leaves no room for it does not fit (0 CTAs), which is not an error
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+    if (smem + fa.sharedSizeBytes > size_t(optin)) {
+      *per_sm = 0;
+      return cudaSuccess;
+    }
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int p1 = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, f, kBulkThreads, smem);
+    if (e != cudaSuccess) return e;
+    per = p1 < per ? p1 : per;
+  }
+  *per_sm = per;
+  return cudaSuccess;
 }
 
 cudaError_t launch_phimv_bulk(const BlockArgs& a, int grid, cudaStream_t st) {

@@ -108,3 +108,12 @@ def test_random_bulk_bitwise(seed):
 @pytest.mark.parametrize("seed", range(32))
 def test_random_bulk_partitioned_bitwise(seed):
     _case(30000 + seed, 2 + seed % 3)
+
+
+@pytest.mark.parametrize("seed,parts", [(50098, 1), (50153, 1), (50192, 2)])
+def test_ring_sizes_next_to_the_shared_memory_limit(seed, parts):
+    """Draws whose deepest candidate ring fits the opt-in shared-memory limit
+    by itself but not together with the kernel's static shared memory: the
+    ring search must take the next candidate (it once failed the evaluation
+    with `invalid argument`; found by tools/tools_fuzz_extended.py)."""
+    _case(seed, parts)
