@@ -40,10 +40,16 @@ struct CudaError {
   const char* what;
 };
 
+// (a failed call's error is also cleared from the runtime's per-thread state:
+// the launch wrappers check cudaGetLastError(), and a stale error would make
+// the caller's NEXT, unrelated call fail too)
 #define PHX_CUDA(call)                                   \
   do {                                                   \
     cudaError_t e_ = (call);                             \
-    if (e_ != cudaSuccess) throw CudaError{e_, #call};   \
+    if (e_ != cudaSuccess) {                             \
+      (void)cudaGetLastError();                          \
+      throw CudaError{e_, #call};                        \
+    }                                                    \
   } while (0)
 
 struct PhxError {
